@@ -1,0 +1,484 @@
+#!/usr/bin/env python
+"""Benchmark of the Baton hot path on B200 (BASELINE.json metric):
+
+    decode tokens/s of the 7B-shaped Baton batch (configs[1]: 32 heads x d128,
+    bf16 KV, batch 32 per GPU, ctx <= 2048, Poisson arrivals) + decode-attention
+    and splice HBM GB/s vs the measured peak.
+
+One "step" = one full Baton iteration of the hot path over the batch: removes +
+release, inserts (KV splice), mask update, and for all 32 layers KV append +
+decode attention -- every §8(a) row that the workload exercises.  Model GEMMs
+are not part of the path (no weights); q/k/v are synthetic keyed values.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl baton|reference]
+
+N > 1: launched by torch.distributed.run, one rank per GPU, 32 slots per GPU
+(weak scaling), one NCCL all-gather of completion flags per iteration.
+Rank 0 prints ONE JSON line.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+T0_DEFAULT = 512          # steady-state start iteration of the Poisson workload
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks sampler
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ workload helpers
+def bench_workload(world):
+    from baton_inputs import config_workload
+    from baton_inputs.workload import _mix_queries, CLASSES_7B, Workload
+    if world == 1:
+        return config_workload("7b")
+    # weak scaling: 32 slots, 512 queries and lambda = 0.08/iteration per GPU
+    rng = np.random.default_rng(18701)
+    qs = _mix_queries(rng, 512 * world, 32 * world, 0.08 * world, CLASSES_7B, 2048)
+    return Workload("7b", qs, layers=32, q_heads=32, kv_heads=32, head_dim=128,
+                    slots=32 * world, max_ctx=2048, gpus=world)
+
+
+def fast_forward(planner, t0):
+    """Advance the (host-only, deterministic) planner to iteration t0."""
+    while planner.t < t0:
+        flags = None
+        if planner.t > 0:
+            flags = sum((planner.local_completion_flags(r) for r in range(planner.world)), [])
+        planner.plan(flags)
+
+
+def window_plan(planner, n_iters, rank):
+    """Decode lists and fresh inserts of the next n_iters iterations (a copy of
+    the planner is stepped; the engine's own planner is untouched)."""
+    import copy
+    p = copy.deepcopy(planner)
+    decodes, inserts = [], []
+    for _ in range(n_iters):
+        dec = [(p.local(g), q, pos) for g, q, pos in p.decode_plan() if p.rank_of(g) == rank]
+        flags = sum((p.local_completion_flags(r) for r in range(p.world)), []) if p.t > 0 else None
+        d = p.plan(flags)
+        decodes.append(dec)
+        for g, q, n, home in d.inserts:
+            if p.rank_of(g) == rank and home is None:
+                inserts.append((q, n))
+    return decodes, inserts
+
+
+# ------------------------------------------------------------------ the CUDA arm
+def run_baton(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2410_18701_b200.engine import Engine
+    from paper_2410_18701_b200.baton import baton_keygen_tokens, baton_keygen_history
+    from paper_2410_18701_b200.scheduler import Planner
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    group = dist.group.WORLD if world > 1 else None
+    wl = bench_workload(world)
+    L, Hq, Hkv, D = wl.layers, wl.q_heads, wl.kv_heads, wl.head_dim
+    K_steps, W = args.steps, args.warmup
+    n_iters = W + K_steps
+
+    def make_engine(token_source, prefill_source):
+        eng = Engine(wl, rank=rank, world=world, device=dev, group=group,
+                     token_source=token_source, prefill_source=prefill_source)
+        fast_forward(eng.planner, args.t0)
+        return eng
+
+    # ---- warm start: materialise the t0 state through the ABI (insert every live
+    # query with its current history: S = max lens, pad = S - lens, exactly the
+    # state after the last release)
+    def warm_start(eng):
+        pl = eng.planner
+        slots, ks, vs, lens = [], [], [], []
+        for g, q in pl.live():
+            if pl.rank_of(g) != rank:
+                continue
+            n = pl.length[g]
+            Kp = torch.empty((L, Hkv, n, D), dtype=torch.bfloat16, device=dev)
+            Vp = torch.empty_like(Kp)
+            baton_keygen_history(Kp, L, Hkv, D, q, 0, n, 1, wl.seed, wl.scales[1])
+            baton_keygen_history(Vp, L, Hkv, D, q, 0, n, 2, wl.seed, wl.scales[2])
+            slots.append(pl.local(g))
+            ks.append(Kp)
+            vs.append(Vp)
+            lens.append(n)
+        eng.shard.baton_insert_many(slots, ks, vs, lens)
+        torch.cuda.synchronize()
+
+    # ---- inputs for the window, resident in HBM before timing
+    probe = Planner(wl, world)
+    fast_forward(probe, args.t0)
+    decodes, fresh = window_plan(probe, n_iters, rank)
+    B = probe.per_rank
+    q_all = torch.empty((n_iters, L, B, Hq, D), dtype=torch.bfloat16, device=dev)
+    k_all = torch.empty((n_iters, L, B, Hkv, D), dtype=torch.bfloat16, device=dev)
+    v_all = torch.empty_like(k_all)
+    for i, dec in enumerate(decodes):
+        qid = np.full(B, -1, np.int32)
+        pos = np.zeros(B, np.int32)
+        for b, q, p in dec:
+            qid[b], pos[b] = q, p
+        dq, dp = torch.from_numpy(qid).to(dev), torch.from_numpy(pos).to(dev)
+        baton_keygen_tokens(q_all[i], dq, dp, L, B, Hq, D, 0, 0, wl.seed, wl.scales[0])
+        baton_keygen_tokens(k_all[i], dq, dp, L, B, Hkv, D, 1, 0, wl.seed, wl.scales[1])
+        baton_keygen_tokens(v_all[i], dq, dp, L, B, Hkv, D, 2, 0, wl.seed, wl.scales[2])
+    pref = {}
+    for q, n in fresh:
+        Kp = torch.empty((L, Hkv, n, D), dtype=torch.bfloat16, device=dev)
+        Vp = torch.empty_like(Kp)
+        baton_keygen_history(Kp, L, Hkv, D, q, 0, n, 1, wl.seed, wl.scales[1])
+        baton_keygen_history(Vp, L, Hkv, D, q, 0, n, 2, wl.seed, wl.scales[2])
+        pref[q] = (Kp, Vp)
+    torch.cuda.synchronize()
+
+    t_base = args.t0
+    state = {"i": 0}
+
+    def token_dev(t, dec):
+        i = t - t_base
+        return q_all[i], k_all[i], v_all[i]
+
+    def prefill_dev(qid, n):
+        return pref[qid]
+
+    # ---------------------------------------------------------------- device-resident run
+    eng = make_engine(token_dev, prefill_dev)
+    warm_start(eng)
+    # the window starts with the decode of iteration t0 (the planner was fast-forwarded)
+    stream = torch.cuda.current_stream()
+
+    # per-launch timing of the dominant kernel (decode attention) via events
+    attn_events = []
+    orig_layer = eng.shard.baton_decode_layer
+
+    def timed_layer(layer, q, out, k_new=None, v_new=None, stream=None):
+        eng.shard.baton_append_kv(layer, k_new, v_new)
+        if state.get("timing"):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            eng.shard.baton_decode_attention(layer, q, out)
+            e1.record()
+            attn_events.append((e0, e1))
+        else:
+            eng.shard.baton_decode_attention(layer, q, out)
+        return out
+
+    eng.shard.baton_decode_layer = timed_layer
+
+    stats_w = [eng.iteration() for _ in range(W)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    state["timing"] = True
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    stats = [eng.iteration() for _ in range(K_steps)]
+    ev1.record()
+    torch.cuda.synchronize()
+    state["timing"] = False
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    attn_ms = [a.elapsed_time(b) for a, b in attn_events]
+
+    tokens = sum(s.decoded for s in stats)
+    live_rows = sum(s.live_rows for s in stats)   # per layer, summed over iterations
+    splice_rows = sum(s.insert_rows + s.extract_rows + s.compact_rows for s in stats)
+    n_launch = sum(1 + 2 * L + (1 if s.removed or s.released else 0) + s.stored
+                   + (2 if s.stored else 0) + (2 if s.inserted else 0) for s in stats)
+    tau = 2 * Hkv * D * 2       # K+V bytes per token per layer
+    attn_bytes_total = L * (live_rows * tau + sum(s.decoded for s in stats) * Hq * D * 2 * 2)
+    attn_time_s = sum(attn_ms) / 1e3
+    attn_launches = len(attn_ms)
+
+    # ---------------------------------------------------------------- e2e run (host buffers)
+    e2e = None
+    if not args.no_e2e:
+        q_h = q_all.cpu().pin_memory()
+        k_h = k_all.cpu().pin_memory()
+        v_h = v_all.cpu().pin_memory()
+        pref_h = {q: (a.cpu().pin_memory(), b.cpu().pin_memory()) for q, (a, b) in pref.items()}
+        del q_all, k_all, v_all
+        pref.clear()
+        qd = torch.empty((L, B, Hq, D), dtype=torch.bfloat16, device=dev)
+        kd = torch.empty((L, B, Hkv, D), dtype=torch.bfloat16, device=dev)
+        vd = torch.empty_like(kd)
+        res_h = torch.empty((B, Hq, D), dtype=torch.bfloat16).pin_memory()
+        counters = {"h2d": 0, "d2h": 0}
+
+        def token_host(t, dec):
+            i = t - t_base
+            qd.copy_(q_h[i], non_blocking=True)
+            kd.copy_(k_h[i], non_blocking=True)
+            vd.copy_(v_h[i], non_blocking=True)
+            counters["h2d"] += (q_h[i].numel() + k_h[i].numel() + v_h[i].numel()) * 2
+            return qd, kd, vd
+
+        def prefill_host(qid, n):
+            a, b = pref_h[qid]
+            counters["h2d"] += (a.numel() + b.numel()) * 2
+            return a.to(dev, non_blocking=True), b.to(dev, non_blocking=True)
+
+        del eng, timed_layer, orig_layer
+        import gc
+        gc.collect()
+        torch.cuda.empty_cache()
+        eng2 = make_engine(token_host, prefill_host)
+        warm_start(eng2)
+        for _ in range(W):
+            eng2.iteration()
+            res_h.copy_(eng2.out[L - 1], non_blocking=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        counters["h2d"] = counters["d2h"] = 0
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        st2 = []
+        for _ in range(K_steps):
+            st2.append(eng2.iteration())
+            res_h.copy_(eng2.out[L - 1], non_blocking=True)   # the step's result to the host
+            counters["d2h"] += res_h.numel() * 2
+        e1.record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms2 = e0.elapsed_time(e1)
+        tok2 = sum(s.decoded for s in st2)
+        e2e = {"ms": ms2, "tokens": tok2, "h2d": counters["h2d"] / K_steps,
+               "d2h": counters["d2h"] / K_steps}
+        del eng2
+
+    return dict(ms=ms, tokens=tokens, attn_bytes=attn_bytes_total, attn_time_s=attn_time_s,
+                attn_launches=attn_launches, splice_rows=splice_rows, tau=tau, L=L,
+                n_launch=n_launch, clocks=clk, e2e=e2e, iters=K_steps,
+                live_slots=tokens / K_steps, live_rows=live_rows)
+
+
+# ------------------------------------------------------------------ the oracle arm
+def oracle_sample(budget_s=15.0, t0=T0_DEFAULT, max_steps=None):
+    """Time the fp64 oracle (O-2 Shard.step, as it stands) on a bounded sample of
+    the same workload: ONE layer of the 7B batch at iteration t0, all live slots.
+    Returns seconds per layer-iteration and the live slot count."""
+    from baton_inputs import config_workload, KIND_K, KIND_V, KIND_Q, bf16_bits_to_f64
+    from baton_inputs import query_history_bits, query_token_bits
+    from oracle import Shard, Simulator
+    wl = config_workload("7b")
+    sim = Simulator(wl, kv=False)
+    while sim.t <= t0:
+        sim.iteration()
+    osh = sim.shards[0]
+    sh = Shard(wl.slots, 1, wl.q_heads, wl.kv_heads, wl.head_dim, wl.max_ctx, kv=True)
+    occ = [b for b in range(wl.slots) if osh.qid[b] >= 0]
+    lens = osh.lens()
+    for b in sorted(occ, key=lambda b: -lens[b]):
+        q = int(osh.qid[b])
+        n = int(lens[b])
+        K = bf16_bits_to_f64(query_history_bits(wl.seed, KIND_K, 1, q, 0, n, wl.kv_heads, wl.head_dim, 0))
+        V = bf16_bits_to_f64(query_history_bits(wl.seed, KIND_V, 1, q, 0, n, wl.kv_heads, wl.head_dim, 0))
+        sh.insert(b, q, n, K, V)
+    times = []
+    step = 0
+    while True:
+        qids = np.zeros(wl.slots, np.int64)
+        pos = np.zeros(wl.slots, np.int64)
+        cur = sh.lens()
+        for b in occ:
+            qids[b], pos[b] = sh.qid[b], cur[b]
+        qv = bf16_bits_to_f64(query_token_bits(wl.seed, KIND_Q, 0, qids, pos, wl.q_heads, wl.head_dim, 0))[None]
+        kv = bf16_bits_to_f64(query_token_bits(wl.seed, KIND_K, 0, qids, pos, wl.kv_heads, wl.head_dim, 0))[None]
+        vv = bf16_bits_to_f64(query_token_bits(wl.seed, KIND_V, 0, qids, pos, wl.kv_heads, wl.head_dim, 0))[None]
+        t1 = time.perf_counter()
+        sh.step(qv, kv, vv)
+        times.append(time.perf_counter() - t1)
+        step += 1
+        if sum(times) >= budget_s or (max_steps and step >= max_steps):
+            break
+    return float(np.mean(times)), len(occ), wl.layers, step
+
+
+def run_reference(args):
+    t_step, live, L, n = oracle_sample(budget_s=args.ref_budget, t0=args.t0,
+                                       max_steps=args.steps + args.warmup)
+    value = live / (L * t_step)
+    cores = 1
+    line = {
+        "impl": "reference", "metric": "decode tokens/s (7B-shape Baton batch)",
+        "value": value, "unit": "tokens/s", "n_gpus": args.gpus, "steps": n, "warmup": 0,
+        "ms_per_step": t_step * L * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (keyed generator)",
+        "config": {"workload": "7b", "t0": args.t0},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                         "sample": f"O-2 Shard.step (fp64 NumPy), 1 of {L} layers, {live} live slots "
+                                   f"at iteration {args.t0}, {n} steps; extrapolated x{L} layers"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="baton", choices=["baton", "reference"])
+    ap.add_argument("--t0", type=int, default=T0_DEFAULT)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-budget", type=float, default=20.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    r = run_baton(args, rank, world, local_rank)
+
+    # max over ranks of the device time; tokens summed over ranks
+    ms, tokens = r["ms"], r["tokens"]
+    e2e_ms = r["e2e"]["ms"] if r["e2e"] else 0.0
+    e2e_tok = r["e2e"]["tokens"] if r["e2e"] else 0
+    if world > 1:
+        t = torch.tensor([ms, e2e_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, e2e_ms = t.tolist()
+        c = torch.tensor([tokens, e2e_tok], dtype=torch.float64, device="cuda")
+        dist.all_reduce(c)
+        tokens, e2e_tok = [int(x) for x in c.tolist()]
+
+    if rank == 0:
+        peak, peak_kind = _peaks()
+        achieved = r["attn_bytes"] / r["attn_time_s"] / 1e9 if r["attn_time_s"] else 0.0
+        per_launch = r["attn_bytes"] / max(1, r["attn_launches"])
+        line = {
+            "metric": "decode tokens/s (7B-shape Baton batch)",
+            "value": tokens / (ms / 1e3),
+            "unit": "tokens/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms / args.steps,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "bf16",
+            "data": "synthetic (keyed q/k/v generator, D1-style length mix, Poisson arrivals)",
+            "config": {"workload": "7b: Llama-2-7B-shaped attention, 32 layers x 32 heads x d128, "
+                                   "bf16 KV, 32 slots/GPU, ctx<=2048, Poisson 0.08/iter",
+                       "t0": args.t0, "slots_per_gpu": 32, "parallelism": f"slots/{world} GPU",
+                       "l2": "inputs larger than L2 (32 GiB KV cache, ~12 GiB read per step)",
+                       "live_slots_per_step": r["live_slots"]},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": "decode_attention_kernel<128>",
+                         "bytes_per_launch": per_launch,
+                         "peak_source": peak_kind,
+                         "avg_launch_us": 1e6 * r["attn_time_s"] / max(1, r["attn_launches"])},
+            "gpu_launches": r["n_launch"],
+            "clocks": r["clocks"],
+        }
+        if r["e2e"]:
+            line["e2e"] = {"value": e2e_tok / (e2e_ms / 1e3), "unit": "tokens/s",
+                           "h2d_bytes_per_step": int(r["e2e"]["h2d"]),
+                           "d2h_bytes_per_step": int(r["e2e"]["d2h"])}
+        if world == 1 and not args.no_cpu_baseline:
+            t_step, live, L, n = oracle_sample(budget_s=15.0, t0=args.t0)
+            line["cpu_baseline"] = {
+                "value": live / (L * t_step), "unit": "tokens/s", "cores": 1, "kind": "oracle",
+                "sample": f"O-2 Shard.step (fp64 NumPy, single thread), 1 of {L} layers, {live} live "
+                          f"slots at iteration {args.t0}, {n} steps, extrapolated x{L} layers"}
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

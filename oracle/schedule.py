@@ -16,9 +16,11 @@ P:L101 and P:L124, DESIGN.md §3 C5):
   5. resize   -- control input: change the number of active slots; shrinking moves
                  queries out: victims as in 4 if the remaining rows do
                  not fit, then compaction (C19)
-  6. insert   -- arrivals join the FCFS queue; the queue head takes the lowest
-                 free active global slot, ascending (C7, C8); global slot g lives
-                 on shard floor(g / B_g) (C20)
+  6. insert   -- arrivals join the FCFS queue; repeatedly the first queue entry
+                 that has an eligible free active slot takes the lowest such
+                 global slot (C7, C8); global slot g lives on shard floor(g / B_g)
+                 (C20).  A stored (preempted) query is eligible only for slots of
+                 the shard holding its stored K/V (C20b); a fresh query for any.
 
 Iteration 0 runs only step 6.  A query's tokens are keyed by (qid, position) so a
 decode step of a query with live length n (after the append) handles position
@@ -69,7 +71,7 @@ class Simulator:
         self.generated = {q.qid: 0 for q in wl.queries}
         self.inserted_at = {}
         self.arrivals = deque(sorted(wl.queries, key=lambda q: (q.arrival, q.qid)))
-        self.queue = deque()     # entries: (qid, length, K, V)
+        self.queue = deque()     # entries: (qid, length, K, V, home shard or None)
         self.n_active = wl.initial_active()
         self.outputs: Dict[Tuple[int, int], np.ndarray] = {}
         self.masks: List[List[np.ndarray]] = []
@@ -112,7 +114,7 @@ class Simulator:
         length = int(sh.lens()[b])
         sh.remove(b)
         rec.preempted.append((qid, g))
-        return (qid, length, K, V)
+        return (qid, length, K, V, r)
 
     # ------------------------------------------------------------------ phases
     def _decode(self, rec):
@@ -223,15 +225,25 @@ class Simulator:
     def _insert_phase(self, rec):
         while self.arrivals and self.arrivals[0].arrival <= self.t:
             q = self.arrivals.popleft()
-            self.queue.append((q.qid, q.l_q, None, None))
+            self.queue.append((q.qid, q.l_q, None, None, None))
         a = self.active_per_shard()
         while self.queue:
             free = [r * self.Bg + b for r, sh in enumerate(self.shards) for b in range(a)
                     if sh.qid[b] < 0]
             if not free:
                 break
-            g = free[0]
-            qid, length, K, V = self.queue.popleft()
+            pick = None
+            for i, entry in enumerate(self.queue):
+                home = entry[4]
+                elig = [g for g in free if home is None or g // self.Bg == home]
+                if elig:
+                    pick = (i, elig[0])
+                    break
+            if pick is None:
+                break
+            i, g = pick
+            qid, length, K, V, _ = self.queue[i]
+            del self.queue[i]
             if self.kv and K is None:
                 K, V = self._prefill(qid, length)
             r, b = self._loc(g)

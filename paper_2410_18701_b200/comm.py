@@ -1,0 +1,27 @@
+"""The one cross-GPU exchange of the hot path.
+
+Slots are partitioned across GPUs (global slot g on rank g // B_g) and every
+step of attention and splice is GPU-local.  Once per iteration each rank
+contributes int32 completion flags for its B_g slots; one
+``all_gather_into_tensor`` (NCCL over NVLink on the GPU box, gloo in the CPU
+tests) gives every rank the same view, and the replicated planner
+(scheduler.py) then takes identical insert/remove decisions without a
+broadcast.
+"""
+import torch
+import torch.distributed as dist
+
+
+def gather_completion_flags(local_flags, world, group=None, device=None):
+    if world == 1:
+        return list(local_flags)
+    backend = dist.get_backend(group)
+    dev = device if (backend == "nccl" and device is not None) else torch.device("cpu")
+    t = torch.tensor(local_flags, dtype=torch.int32, device=dev)
+    if backend == "nccl":
+        out = torch.empty(world * len(local_flags), dtype=torch.int32, device=dev)
+        dist.all_gather_into_tensor(out, t, group=group)
+        return out.cpu().tolist()
+    parts = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(parts, t, group=group)
+    return torch.cat(parts).tolist()

@@ -1,0 +1,419 @@
+// baton_api.cu -- the C ABI of libbaton (include/baton.h, include/baton_keygen.h):
+// argument validation against the host mirror of the logical state, then
+// asynchronous launches on the caller's stream.  The host mirror follows the
+// paper's state machine (P:L96 step, P:L105 remove, P:L124 release, P:L137
+// embedding, P:L144 store, P:L147 scaling) on metadata only; every byte of
+// device data is touched by the kernels in decode_attention.cu / meta.cu /
+// splice.cu.
+#include <algorithm>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include <cuda_bf16.h>
+
+#include "../../include/baton.h"
+#include "../../include/baton_keygen.h"
+#include "kernels.h"
+
+using namespace baton;
+
+struct baton_state {
+    baton_config cfg;
+    baton_shape sh;
+    int S = 0;
+    std::vector<int32_t> pad, lens, occ;
+    int32_t *d_S = nullptr, *d_lens = nullptr, *d_pad = nullptr;
+    int32_t *tickets = nullptr;
+    float *partial = nullptr;
+    int max_chunks = 0;
+    size_t layer_elems = 0;   // elements of one layer of the K (or V) cache
+};
+
+namespace {
+
+thread_local int g_cuda_error = 0;
+
+inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+int cuda_status(cudaError_t e) {
+    if (e == cudaSuccess) return BATON_OK;
+    g_cuda_error = (int)e;
+    return BATON_E_CUDA;
+}
+
+bool shape_ok(const baton_shape *s) {
+    if (!s) return false;
+    return s->layers >= 1 && s->slots >= 1 && s->slots <= MAX_SLOTS && s->q_heads >= 1 &&
+           s->kv_heads >= 1 && s->q_heads % s->kv_heads == 0 &&
+           decode_supported_head_dim(s->head_dim) && s->max_ctx >= 16 && s->max_ctx % 16 == 0 &&
+           s->max_ctx <= 65536;
+}
+
+size_t meta_bytes(const baton_shape *s) { return align256((1 + 2 * (size_t)s->slots) * 4); }
+size_t ticket_region(const baton_shape *s) { return align256(decode_ticket_bytes(s->slots, s->q_heads)); }
+
+cudaStream_t as_stream(void *s) { return static_cast<cudaStream_t>(s); }
+
+__nv_bfloat16 *layer_ptr(void *base, const baton_state *st, int layer) {
+    return static_cast<__nv_bfloat16 *>(base) + (size_t)layer * st->layer_elems;
+}
+
+int push_meta(baton_state *st, const std::vector<MaskOp> &ops, cudaStream_t s) {
+    return cuda_status(launch_mask_splice(st->cfg.mask, st->sh.slots, st->sh.max_ctx, ops.data(),
+                                          (int)ops.size(), st->d_S, st->d_lens, st->d_pad, st->S,
+                                          st->lens.data(), st->pad.data(), s));
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t baton_decode_workspace_bytes(const baton_shape *s) {
+    if (!shape_ok(s)) return 0;
+    return ticket_region(s) + align256(decode_partial_bytes(s->slots, s->q_heads, s->head_dim, s->max_ctx));
+}
+
+size_t baton_workspace_bytes(const baton_shape *s) {
+    if (!shape_ok(s)) return 0;
+    return meta_bytes(s) + baton_decode_workspace_bytes(s);
+}
+
+int baton_create(const baton_config *cfg, void *stream, baton_state **out) {
+    if (!cfg || !out || !shape_ok(&cfg->shape) || !cfg->k_cache || !cfg->v_cache || !cfg->mask ||
+        !cfg->workspace)
+        return BATON_E_INVALID;
+    if (cfg->workspace_bytes < baton_workspace_bytes(&cfg->shape)) return BATON_E_INVALID;
+    if ((reinterpret_cast<uintptr_t>(cfg->workspace) & 255) ||
+        (reinterpret_cast<uintptr_t>(cfg->k_cache) & 15) ||
+        (reinterpret_cast<uintptr_t>(cfg->v_cache) & 15) || (reinterpret_cast<uintptr_t>(cfg->mask) & 15))
+        return BATON_E_INVALID;
+    baton_state *st = new (std::nothrow) baton_state;
+    if (!st) return BATON_E_INVALID;
+    st->cfg = *cfg;
+    st->sh = cfg->shape;
+    const baton_shape &s = st->sh;
+    st->pad.assign(s.slots, 0);
+    st->lens.assign(s.slots, 0);
+    st->occ.assign(s.slots, 0);
+    uint8_t *ws = static_cast<uint8_t *>(cfg->workspace);
+    st->d_S = reinterpret_cast<int32_t *>(ws);
+    st->d_lens = st->d_S + 1;
+    st->d_pad = st->d_lens + s.slots;
+    st->tickets = reinterpret_cast<int32_t *>(ws + meta_bytes(&s));
+    st->partial = reinterpret_cast<float *>(ws + meta_bytes(&s) + ticket_region(&s));
+    st->max_chunks = ceil_div(s.max_ctx, CHUNK);
+    st->layer_elems = (size_t)s.slots * s.kv_heads * s.max_ctx * s.head_dim;
+    cudaStream_t cs = as_stream(stream);
+    cudaError_t e = cudaMemsetAsync(cfg->mask, 0, (size_t)s.slots * s.max_ctx, cs);
+    if (e == cudaSuccess) e = cudaMemsetAsync(cfg->workspace, 0, baton_workspace_bytes(&s), cs);
+    if (e != cudaSuccess) {
+        delete st;
+        return cuda_status(e);
+    }
+    *out = st;
+    return BATON_OK;
+}
+
+void baton_destroy(baton_state *st) { delete st; }
+
+int baton_device_meta(const baton_state *st, int32_t **S, int32_t **lens, int32_t **pad_start) {
+    if (!st) return BATON_E_INVALID;
+    if (S) *S = st->d_S;
+    if (lens) *lens = st->d_lens;
+    if (pad_start) *pad_start = st->d_pad;
+    return BATON_OK;
+}
+
+int baton_query(const baton_state *st, int32_t *S, int32_t *pad_start, int32_t *lens,
+                int32_t *occupied) {
+    if (!st) return BATON_E_INVALID;
+    const int B = st->sh.slots;
+    if (S) *S = st->S;
+    if (pad_start) std::memcpy(pad_start, st->pad.data(), B * 4);
+    if (lens) std::memcpy(lens, st->lens.data(), B * 4);
+    if (occupied) std::memcpy(occupied, st->occ.data(), B * 4);
+    return BATON_OK;
+}
+
+// ---------------------------------------------------------------- a1
+int baton_mask_update(baton_state *st, void *stream) {
+    if (!st) return BATON_E_INVALID;
+    if (st->S + 1 > st->sh.max_ctx) return BATON_E_CAPACITY;
+    int r = cuda_status(launch_mask_update(st->cfg.mask, st->d_S, st->d_lens, st->sh.slots,
+                                           st->sh.max_ctx, as_stream(stream)));
+    if (r) return r;
+    st->S += 1;
+    for (int b = 0; b < st->sh.slots; ++b)
+        if (st->occ[b]) st->lens[b] += 1;
+    return BATON_OK;
+}
+
+// ---------------------------------------------------------------- a2
+int baton_append_kv(baton_state *st, int layer, const void *k_new, const void *v_new, void *stream) {
+    if (!st || !k_new || !v_new || layer < 0 || layer >= st->sh.layers) return BATON_E_INVALID;
+    return cuda_status(launch_append_kv(layer_ptr(st->cfg.k_cache, st, layer),
+                                        layer_ptr(st->cfg.v_cache, st, layer), k_new, v_new,
+                                        st->d_lens, st->sh.slots, st->sh.kv_heads,
+                                        st->sh.head_dim, st->sh.max_ctx, as_stream(stream)));
+}
+
+// ---------------------------------------------------------------- a3
+int baton_decode_attention(const void *q, const void *k, const void *v, const uint8_t *mask,
+                           const int32_t *lens, const int32_t *pad_start, void *out,
+                           const baton_shape *shape, float scale, void *workspace,
+                           size_t workspace_bytes, void *stream) {
+    if (!q || !k || !v || !lens || !pad_start || !out || !workspace || !shape_ok(shape))
+        return BATON_E_INVALID;
+    if (workspace_bytes < baton_decode_workspace_bytes(shape)) return BATON_E_INVALID;
+    if (!(scale > 0.f)) return BATON_E_INVALID;
+    DecodeArgs a;
+    a.q = q;
+    a.k = k;
+    a.v = v;
+    a.mask = mask;
+    a.lens = lens;
+    a.pad = pad_start;
+    a.out = out;
+    a.tickets = static_cast<int32_t *>(workspace);
+    a.partial = reinterpret_cast<float *>(static_cast<uint8_t *>(workspace) + ticket_region(shape));
+    a.slots = shape->slots;
+    a.q_heads = shape->q_heads;
+    a.kv_heads = shape->kv_heads;
+    a.head_dim = shape->head_dim;
+    a.max_ctx = shape->max_ctx;
+    a.max_chunks = ceil_div(shape->max_ctx, CHUNK);
+    a.scale = scale;
+    return cuda_status(launch_decode_attention(a, as_stream(stream)));
+}
+
+int baton_decode_layer(baton_state *st, int layer, const void *q, const void *k_new,
+                       const void *v_new, void *out, void *stream) {
+    if (!st || !q || !out || layer < 0 || layer >= st->sh.layers) return BATON_E_INVALID;
+    if ((k_new == nullptr) != (v_new == nullptr)) return BATON_E_INVALID;
+    if (k_new) {
+        int r = baton_append_kv(st, layer, k_new, v_new, stream);
+        if (r) return r;
+    }
+    const baton_shape &s = st->sh;
+    return baton_decode_attention(q, layer_ptr(st->cfg.k_cache, st, layer),
+                                  layer_ptr(st->cfg.v_cache, st, layer), st->cfg.mask, st->d_lens,
+                                  st->d_pad, out, &s, 1.0f / sqrtf((float)s.head_dim),
+                                  reinterpret_cast<uint8_t *>(st->tickets),
+                                  baton_decode_workspace_bytes(&s), stream);
+}
+
+// ---------------------------------------------------------------- a4
+int baton_remove(baton_state *st, const int32_t *slots, int n, int32_t *released, void *stream) {
+    if (!st || n < 0 || (n > 0 && !slots)) return BATON_E_INVALID;
+    const int B = st->sh.slots;
+    std::vector<char> seen(B, 0);
+    for (int i = 0; i < n; ++i) {
+        const int b = slots[i];
+        if (b < 0 || b >= B || seen[b]) return BATON_E_INVALID;
+        if (!st->occ[b]) return BATON_E_SLOT_EMPTY;
+        seen[b] = 1;
+    }
+    std::vector<MaskOp> ops;
+    for (int i = 0; i < n; ++i) {
+        const int b = slots[i];
+        ops.push_back({MOP_ZERO_ROW, b, 0, 0});
+        st->occ[b] = 0;
+        st->lens[b] = 0;
+        st->pad[b] = 0;
+    }
+    // release [0 : min(index_i)] over occupied slots (everything if none, C5)
+    int p = st->S;
+    for (int b = 0; b < B; ++b)
+        if (st->occ[b]) p = std::min(p, (int)st->pad[b]);
+    if (p > 0) {
+        ops.push_back({MOP_SHIFT_LEFT, -1, p, 0});
+        for (int b = 0; b < B; ++b)
+            if (st->occ[b]) st->pad[b] -= p;
+        st->S -= p;
+    }
+    if (released) *released = p;
+    if (ops.empty()) return BATON_OK;   // nothing removed, nothing to release
+    return push_meta(st, ops, as_stream(stream));
+}
+
+// ---------------------------------------------------------------- a5
+int baton_insert_many(baton_state *st, int n, const int32_t *slots, const void *const *k_pref,
+                      const void *const *v_pref, const int32_t *lens, void *stream) {
+    if (!st || n < 0) return BATON_E_INVALID;
+    if (n == 0) return BATON_OK;
+    if (!slots || !k_pref || !v_pref || !lens) return BATON_E_INVALID;
+    const baton_shape &s = st->sh;
+    std::vector<char> seen(s.slots, 0);
+    for (int i = 0; i < n; ++i) {
+        const int b = slots[i];
+        if (b < 0 || b >= s.slots || seen[b] || !k_pref[i] || !v_pref[i]) return BATON_E_INVALID;
+        if (st->occ[b]) return BATON_E_SLOT_BUSY;
+        if (lens[i] < 1 || lens[i] > s.max_ctx) return BATON_E_CAPACITY;
+        if ((reinterpret_cast<uintptr_t>(k_pref[i]) & 15) || (reinterpret_cast<uintptr_t>(v_pref[i]) & 15))
+            return BATON_E_INVALID;
+        seen[b] = 1;
+    }
+    std::vector<MaskOp> ops;
+    std::vector<CopyJob> jobs;
+    for (int i = 0; i < n; ++i) {
+        const int b = slots[i];
+        const int len = lens[i];
+        if (len <= st->S) {   // P:L137 case 1: end-aligned
+            st->pad[b] = st->S - len;
+        } else {              // P:L137 case 2: expand on the left by e
+            const int e = len - st->S;
+            ops.push_back({MOP_SHIFT_RIGHT, -1, e, 0});
+            for (int c = 0; c < s.slots; ++c)
+                if (st->occ[c]) st->pad[c] += e;
+            st->S = len;
+            st->pad[b] = 0;
+        }
+        ops.push_back({MOP_SET_ROW, b, st->pad[b], st->S});
+        st->occ[b] = 1;
+        st->lens[b] = len;
+        CopyJob j;
+        j.src_k = k_pref[i];
+        j.src_v = v_pref[i];
+        j.dst_k = static_cast<__nv_bfloat16 *>(st->cfg.k_cache) + (size_t)b * s.kv_heads * s.max_ctx * s.head_dim;
+        j.dst_v = static_cast<__nv_bfloat16 *>(st->cfg.v_cache) + (size_t)b * s.kv_heads * s.max_ctx * s.head_dim;
+        j.src_hs = (int64_t)len * s.head_dim;
+        j.src_ls = j.src_hs * s.kv_heads;
+        j.dst_hs = (int64_t)s.max_ctx * s.head_dim;
+        j.dst_ls = (int64_t)st->layer_elems;
+        j.rows = len;
+        j.pad_ = 0;
+        jobs.push_back(j);
+    }
+    cudaStream_t cs = as_stream(stream);
+    for (size_t i0 = 0; i0 < jobs.size(); i0 += MAX_SPLICE_JOBS) {
+        const int nj = (int)std::min(jobs.size() - i0, (size_t)MAX_SPLICE_JOBS);
+        int r = cuda_status(launch_kv_copy(jobs.data() + i0, nj, s.layers, s.kv_heads, s.head_dim, cs));
+        if (r) return r;
+    }
+    return push_meta(st, ops, cs);
+}
+
+int baton_insert(baton_state *st, int slot, const void *k_pref, const void *v_pref, int len,
+                 void *stream) {
+    const void *kp[1] = {k_pref};
+    const void *vp[1] = {v_pref};
+    const int32_t sl[1] = {slot};
+    const int32_t ln[1] = {len};
+    return baton_insert_many(st, 1, sl, kp, vp, ln, stream);
+}
+
+// ---------------------------------------------------------------- a6
+int baton_extract(baton_state *st, int slot, void *k_out, void *v_out, void *stream) {
+    if (!st || !k_out || !v_out) return BATON_E_INVALID;
+    const baton_shape &s = st->sh;
+    if (slot < 0 || slot >= s.slots) return BATON_E_INVALID;
+    if (!st->occ[slot]) return BATON_E_SLOT_EMPTY;
+    if ((reinterpret_cast<uintptr_t>(k_out) & 15) || (reinterpret_cast<uintptr_t>(v_out) & 15))
+        return BATON_E_INVALID;
+    const int len = st->lens[slot];
+    CopyJob j;
+    j.src_k = static_cast<__nv_bfloat16 *>(st->cfg.k_cache) + (size_t)slot * s.kv_heads * s.max_ctx * s.head_dim;
+    j.src_v = static_cast<__nv_bfloat16 *>(st->cfg.v_cache) + (size_t)slot * s.kv_heads * s.max_ctx * s.head_dim;
+    j.dst_k = k_out;
+    j.dst_v = v_out;
+    j.src_hs = (int64_t)s.max_ctx * s.head_dim;
+    j.src_ls = (int64_t)st->layer_elems;
+    j.dst_hs = (int64_t)len * s.head_dim;
+    j.dst_ls = j.dst_hs * s.kv_heads;
+    j.rows = len;
+    j.pad_ = 0;
+    return cuda_status(launch_kv_copy(&j, 1, s.layers, s.kv_heads, s.head_dim, as_stream(stream)));
+}
+
+// ---------------------------------------------------------------- a7
+int baton_compact(baton_state *st, int n_active, int32_t *old_to_new, void *stream) {
+    if (!st) return BATON_E_INVALID;
+    const baton_shape &s = st->sh;
+    if (n_active < 1 || n_active > s.slots) return BATON_E_INVALID;
+    int n_occ_hi = 0, n_free_lo = 0;
+    for (int b = 0; b < s.slots; ++b) {
+        if (b >= n_active && st->occ[b]) ++n_occ_hi;
+        if (b < n_active && !st->occ[b]) ++n_free_lo;
+    }
+    if (n_occ_hi > n_free_lo) return BATON_E_CAPACITY;
+    std::vector<int32_t> src, dst;
+    std::vector<CopyJob> jobs;
+    std::vector<int32_t> o2n(s.slots);
+    for (int b = 0; b < s.slots; ++b) o2n[b] = b;
+    int f = 0;
+    for (int b = n_active; b < s.slots; ++b) {
+        if (!st->occ[b]) continue;
+        while (st->occ[f]) ++f;   // lowest free slot < n_active (C19)
+        src.push_back(b);
+        dst.push_back(f);
+        o2n[b] = f;
+        CopyJob j;
+        const size_t slot_elems = (size_t)s.kv_heads * s.max_ctx * s.head_dim;
+        j.src_k = static_cast<__nv_bfloat16 *>(st->cfg.k_cache) + (size_t)b * slot_elems;
+        j.src_v = static_cast<__nv_bfloat16 *>(st->cfg.v_cache) + (size_t)b * slot_elems;
+        j.dst_k = static_cast<__nv_bfloat16 *>(st->cfg.k_cache) + (size_t)f * slot_elems;
+        j.dst_v = static_cast<__nv_bfloat16 *>(st->cfg.v_cache) + (size_t)f * slot_elems;
+        j.src_hs = j.dst_hs = (int64_t)s.max_ctx * s.head_dim;
+        j.src_ls = j.dst_ls = (int64_t)st->layer_elems;
+        j.rows = st->lens[b];
+        j.pad_ = 0;
+        jobs.push_back(j);
+        st->occ[f] = 1;
+        st->lens[f] = st->lens[b];
+        st->pad[f] = st->pad[b];
+        st->occ[b] = 0;
+        st->lens[b] = 0;
+        st->pad[b] = 0;
+    }
+    if (old_to_new) std::memcpy(old_to_new, o2n.data(), s.slots * 4);
+    cudaStream_t cs = as_stream(stream);
+    for (size_t i0 = 0; i0 < jobs.size(); i0 += MAX_SPLICE_JOBS) {
+        const int nj = (int)std::min(jobs.size() - i0, (size_t)MAX_SPLICE_JOBS);
+        int r = cuda_status(launch_kv_copy(jobs.data() + i0, nj, s.layers, s.kv_heads, s.head_dim, cs));
+        if (r) return r;
+    }
+    return cuda_status(launch_mask_move(st->cfg.mask, s.slots, s.max_ctx, src.data(), dst.data(),
+                                        (int)src.size(), st->d_S, st->d_lens, st->d_pad, st->S,
+                                        st->lens.data(), st->pad.data(), cs));
+}
+
+// ---------------------------------------------------------------- misc
+const char *baton_error_string(int code) {
+    switch (code) {
+        case BATON_OK: return "ok";
+        case BATON_E_INVALID: return "invalid argument";
+        case BATON_E_SLOT_BUSY: return "slot busy";
+        case BATON_E_SLOT_EMPTY: return "slot empty";
+        case BATON_E_CAPACITY: return "capacity exceeded";
+        case BATON_E_CUDA: return "CUDA error";
+        default: return "unknown error";
+    }
+}
+
+int baton_cuda_error(void) { return g_cuda_error; }
+
+// ---------------------------------------------------------------- harness keygen
+int baton_keygen_tokens(void *out, const int32_t *qids, const int32_t *pos, int layers, int n_slots,
+                        int heads, int head_dim, int kind, int layer0, uint64_t seed, int scale_exp,
+                        void *stream) {
+    if (!out || !qids || !pos || layers < 0 || n_slots < 0 || heads < 1 || heads > 64 ||
+        head_dim < 1 || head_dim > 128 || kind < 0 || kind > 2 || layer0 < 0 || layer0 + layers > 128)
+        return BATON_E_INVALID;
+    return cuda_status(launch_keygen_tokens(out, qids, pos, layers, n_slots, heads, head_dim, kind,
+                                            layer0, seed, scale_exp, as_stream(stream)));
+}
+
+int baton_keygen_history(void *out, int layers, int heads, int head_dim, int qid, int pos_begin,
+                         int n, int kind, uint64_t seed, int scale_exp, int64_t head_stride,
+                         int64_t layer_stride, void *stream) {
+    if (!out || layers < 0 || layers > 128 || heads < 1 || heads > 64 || head_dim < 1 ||
+        head_dim > 128 || qid < 0 || qid >= (1 << 20) || pos_begin < 0 || n < 0 ||
+        pos_begin + n > 4096 || kind < 0 || kind > 2)
+        return BATON_E_INVALID;
+    return cuda_status(launch_keygen_history(out, layers, heads, head_dim, qid, pos_begin, n, kind,
+                                             seed, scale_exp, head_stride, layer_stride,
+                                             as_stream(stream)));
+}
+
+}  // extern "C"

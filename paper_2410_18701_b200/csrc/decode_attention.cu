@@ -1,0 +1,429 @@
+// decode_attention.cu -- a3 of the hot path: masked decode attention over the
+// slot-relative KV cache (§2.1 SDPA; P:L52/P:L132 decode with the latest
+// single token; masked padding skipped).
+//
+// Design:
+//   * work item = (slot b, q head h, chunk c) of BATON_CHUNK = 256 keys counted
+//     from the slot's live start (fixed chunking -> batch-invariant results);
+//     items ordered (b, c, h), distributed round-robin over persistent CTAs
+//     (2 per SM).
+//   * one PRODUCER warp (one elected lane) streams 64-key K and V tiles plus the
+//     tile's mask bytes and, on an item's first tile, the query vector into a
+//     3-stage shared-memory ring with 1-D bulk copies (cp.async.bulk -> UBLKCP,
+//     the TMA engine), completion tracked by mbarrier transaction counts.
+//     Rows outside [0, lens) are never requested.
+//   * four CONSUMER warps each own 16 rows of a tile.  A warp reads two 256-B
+//     rows per 16-B-per-lane shared load (conflict-free), forms partial dot
+//     products on 8 dims per lane and finishes them with a transposing
+//     butterfly (8 shuffles per 16 keys), keeps an online softmax (running max
+//     m, running sum l, unnormalised o) in fp32, exp2-based with scale*log2(e)
+//     folded into q.
+//   * an item's four warp states are merged in shared memory; a single-chunk
+//     query writes its bf16 output directly, otherwise the chunk partial
+//     (m, l, o[D]) goes to the workspace and the LAST CTA to finish a
+//     (b, h) (atomic ticket) merges the chunk partials in ascending chunk order.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace baton {
+namespace {
+
+constexpr int CWARPS = 4;                 // consumer warps
+constexpr int ROWS_PER_WARP = 16;
+constexpr int TILE = CWARPS * ROWS_PER_WARP;   // 64 keys per stage
+constexpr int STAGES = 3;
+constexpr int THREADS = (CWARPS + 1) * 32;
+constexpr int TILES_PER_CHUNK = CHUNK / TILE;
+
+constexpr int F_FIRST = 1, F_LAST = 2, F_END = 4;
+
+__device__ __forceinline__ int ceil_div_dev(int L) { return (L + CHUNK - 1) / CHUNK; }
+
+struct StageDesc {
+    int32_t b, h, c, nrows, flags, moff, nchunks, pad_;
+};
+
+template <int D>
+struct __align__(16) Stage {
+    __nv_bfloat16 k[TILE * D];
+    __nv_bfloat16 v[TILE * D];
+    __nv_bfloat16 q[D < 8 ? 8 : D];
+    uint8_t mask[TILE + 16];
+    StageDesc desc;
+};
+
+struct Params {
+    const __nv_bfloat16 *q, *k, *v;
+    const uint8_t *mask;
+    const int32_t *lens, *pad;
+    __nv_bfloat16 *out;
+    float *partial;
+    int32_t *tickets;
+    int B, Hq, Hkv, max_ctx, max_chunks;
+    float scale_log2;
+};
+
+template <int D>
+struct Smem {
+    Stage<D> st[STAGES];
+    uint64_t full[STAGES], empty[STAGES];
+    int32_t prefix[MAX_SLOTS + 1];
+    int32_t lens[MAX_SLOTS];
+    int32_t pad[MAX_SLOTS];
+    float red_o[CWARPS][D];
+    float red_m[CWARPS], red_l[CWARPS];
+    int32_t last_flag;
+};
+
+template <int D>
+__global__ void __launch_bounds__(THREADS, 2) decode_attention_kernel(const Params p) {
+    constexpr int LPR = D / 8;                 // lanes per key row (16 B of bf16 per lane)
+    constexpr int RPL = 32 / LPR;              // rows per warp-wide load
+    constexpr int NL = ROWS_PER_WARP / RPL;    // loads per lane per tile
+    static_assert(NL * 2 == LPR || (LPR == 2 && NL == 1), "row mapping");
+
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    Smem<D> &sm = *reinterpret_cast<Smem<D> *>(smem_raw);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&sm.full[s], 1);
+            mbar_init(&sm.empty[s], CWARPS);
+        }
+        fence_mbar_init();
+    }
+    // Empty slots produce a zero output row (C6).
+    for (int b = blockIdx.x; b < p.B; b += gridDim.x) {
+        if (p.lens[b] <= 0) {
+            uint4 *o = reinterpret_cast<uint4 *>(p.out + (size_t)b * p.Hq * D);
+            for (int i = threadIdx.x; i < p.Hq * D / 8; i += THREADS) o[i] = make_uint4(0, 0, 0, 0);
+        }
+    }
+    __syncthreads();
+
+    if (warp == CWARPS) {
+        // ============================ producer warp ============================
+        // Item enumeration: items per slot = nchunks(b) * Hq, prefix-summed.
+        int running = 0;
+        for (int b0 = 0; b0 < p.B; b0 += 32) {
+            int b = b0 + lane;
+            int L = 0, P = 0;
+            if (b < p.B) {
+                L = p.lens[b];
+                P = p.pad[b];
+                sm.lens[b] = L;
+                sm.pad[b] = P;
+            }
+            int n = (L > 0 ? ceil_div_dev(L) : 0) * p.Hq;
+            int incl = n;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int t = __shfl_up_sync(FULL_MASK, incl, o);
+                if (lane >= o) incl += t;
+            }
+            if (b < p.B) sm.prefix[b] = running + incl - n;
+            running += __shfl_sync(FULL_MASK, incl, 31);
+        }
+        if (lane == 0) sm.prefix[p.B] = running;
+        __syncwarp();
+        if (lane != 0) return;
+        const int total = running;
+        const uint64_t pol = policy_evict_first();
+        int stage = 0;
+        uint32_t phase = 0;
+        int b = 0;
+        for (int w = blockIdx.x; w < total; w += gridDim.x) {
+            while (sm.prefix[b + 1] <= w) ++b;
+            const int L = sm.lens[b];
+            const int nch = ceil_div_dev(L);
+            const int rem = w - sm.prefix[b];
+            const int c = rem / p.Hq;
+            const int h = rem - c * p.Hq;
+            const int g = h * p.Hkv / p.Hq;
+            const int r0 = c * CHUNK;
+            const int rows = min(CHUNK, L - r0);
+            const size_t head_off = ((size_t)(b * p.Hkv + g) * p.max_ctx + r0) * D;
+            const __nv_bfloat16 *kb = p.k + head_off;
+            const __nv_bfloat16 *vb = p.v + head_off;
+            const int ntiles = (rows + TILE - 1) / TILE;
+            for (int t = 0; t < ntiles; ++t) {
+                const int nr = min(TILE, rows - t * TILE);
+                mbar_wait(&sm.empty[stage], phase ^ 1);
+                Stage<D> &st = sm.st[stage];
+                uint32_t bytes = 2u * nr * D * 2;
+                int moff = 0;
+                uint32_t mbytes = 0;
+                const uint8_t *msrc = nullptr;
+                if (p.mask) {
+                    // aligned superset of the tile's mask bytes (row start is 16-B aligned)
+                    const size_t row0 = (size_t)b * p.max_ctx;
+                    const size_t j0 = row0 + sm.pad[b] + r0 + t * TILE;
+                    const size_t a0 = j0 & ~(size_t)15;
+                    const size_t row_end = row0 + p.max_ctx;
+                    size_t need = (j0 + nr - a0 + 15) & ~(size_t)15;
+                    if (a0 + need > row_end) need = row_end - a0;
+                    msrc = p.mask + a0;
+                    mbytes = (uint32_t)need;
+                    moff = (int)(j0 - a0);
+                    bytes += mbytes;
+                }
+                if (t == 0) bytes += D * 2;
+                st.desc.b = b;
+                st.desc.h = h;
+                st.desc.c = c;
+                st.desc.nrows = nr;
+                st.desc.flags = (t == 0 ? F_FIRST : 0) | (t == ntiles - 1 ? F_LAST : 0);
+                st.desc.moff = moff;
+                st.desc.nchunks = nch;
+                mbar_arrive_expect_tx(&sm.full[stage], bytes);
+                bulk_g2s_evict_first(st.k, kb + (size_t)t * TILE * D, nr * D * 2, &sm.full[stage], pol);
+                bulk_g2s_evict_first(st.v, vb + (size_t)t * TILE * D, nr * D * 2, &sm.full[stage], pol);
+                if (mbytes) bulk_g2s(st.mask, msrc, mbytes, &sm.full[stage]);
+                if (t == 0) bulk_g2s(st.q, p.q + (size_t)(b * p.Hq + h) * D, D * 2, &sm.full[stage]);
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+        mbar_wait(&sm.empty[stage], phase ^ 1);
+        sm.st[stage].desc.flags = F_END;
+        mbar_arrive(&sm.full[stage]);
+        return;
+    }
+
+    // ============================ consumer warps ============================
+    const int g = lane / LPR;        // row group within a warp-wide load
+    const int s = lane % LPR;        // 16-B column chunk: dims [8s, 8s+8)
+    const int my_row = (s >> 1) * RPL + g;   // row whose score this lane ends up holding
+    float qf[8], o[8];
+    float m = -INFINITY, l = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] = qf[i] = 0.f;
+
+    int stage = 0;
+    uint32_t phase = 0;
+    while (true) {
+        mbar_wait(&sm.full[stage], phase);
+        Stage<D> &st = sm.st[stage];
+        const StageDesc d = st.desc;
+        if (d.flags & F_END) break;
+        if (d.flags & F_FIRST) {
+            const uint4 qv = *reinterpret_cast<const uint4 *>(st.q + s * 8);
+            const uint32_t qw[4] = {qv.x, qv.y, qv.z, qv.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                qf[2 * i] = bf16lo(qw[i]) * p.scale_log2;
+                qf[2 * i + 1] = bf16hi(qw[i]) * p.scale_log2;
+            }
+            m = -INFINITY;
+            l = 0.f;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) o[i] = 0.f;
+        }
+        const int base = warp * ROWS_PER_WARP;
+        if (base < d.nrows) {
+            // ---- scores: partial dots over this lane's 8 dims, NL rows
+            float part[NL];
+#pragma unroll
+            for (int i = 0; i < NL; ++i) {
+                const uint4 kv =
+                    *reinterpret_cast<const uint4 *>(st.k + (base + i * RPL + g) * D + s * 8);
+                const uint32_t kw[4] = {kv.x, kv.y, kv.z, kv.w};
+                float acc = 0.f;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    acc = fmaf(qf[2 * j], bf16lo(kw[j]), acc);
+                    acc = fmaf(qf[2 * j + 1], bf16hi(kw[j]), acc);
+                }
+                part[i] = acc;
+            }
+            // ---- transposing butterfly: after it, lane holds the full dot of my_row
+#pragma unroll
+            for (int step = 0, n = NL, msk = LPR / 2; n > 1; ++step, n >>= 1, msk >>= 1) {
+                const bool upper = (lane & msk) != 0;
+#pragma unroll
+                for (int k2 = 0; k2 < n / 2; ++k2) {
+                    const float send = upper ? part[k2] : part[k2 + n / 2];
+                    const float keep = upper ? part[k2 + n / 2] : part[k2];
+                    part[k2] = keep + __shfl_xor_sync(FULL_MASK, send, msk);
+                }
+            }
+            float sc = part[0] + __shfl_xor_sync(FULL_MASK, part[0], 1);
+            const int row = base + my_row;
+            bool valid = row < d.nrows;
+            if (p.mask) valid = valid && (st.mask[d.moff + (valid ? row : 0)] != 0);
+            sc = valid ? sc : -INFINITY;
+            float tmax = sc;
+#pragma unroll
+            for (int o2 = 16; o2 > 0; o2 >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(FULL_MASK, tmax, o2));
+            const float m_new = fmaxf(m, tmax);
+            if (m_new != -INFINITY) {
+                const float alpha = ex2(m - m_new);     // m = -inf -> 0
+                const float pe = ex2(sc - m_new);       // masked -> 0
+                l = l * alpha + pe;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) o[i] *= alpha;
+                const bool all_valid = __all_sync(FULL_MASK, valid);
+#pragma unroll
+                for (int i = 0; i < NL; ++i) {
+                    const int src = g * LPR + 2 * i;
+                    float pi = __shfl_sync(FULL_MASK, pe, src);
+                    uint4 vv = *reinterpret_cast<const uint4 *>(st.v + (base + i * RPL + g) * D + s * 8);
+                    if (!all_valid) {
+                        const bool vi = __shfl_sync(FULL_MASK, valid, src);
+                        if (!vi) {
+                            pi = 0.f;
+                            vv = make_uint4(0, 0, 0, 0);
+                        }
+                    }
+                    const uint32_t vw[4] = {vv.x, vv.y, vv.z, vv.w};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        o[2 * j] = fmaf(pi, bf16lo(vw[j]), o[2 * j]);
+                        o[2 * j + 1] = fmaf(pi, bf16hi(vw[j]), o[2 * j + 1]);
+                    }
+                }
+                m = m_new;
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[stage]);
+        if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+        }
+
+        if (d.flags & F_LAST) {
+            // ---- merge the four warp states of this item
+            float lsum = l;
+#pragma unroll
+            for (int o2 = 16; o2 > 0; o2 >>= 1) lsum += __shfl_xor_sync(FULL_MASK, lsum, o2);
+            lsum *= 0.5f;   // every row's weight is held by two lanes
+#pragma unroll
+            for (int mk = LPR; mk < 32; mk <<= 1)
+#pragma unroll
+                for (int i = 0; i < 8; ++i) o[i] += __shfl_xor_sync(FULL_MASK, o[i], mk);
+            if (lane < LPR) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) sm.red_o[warp][s * 8 + i] = o[i];
+            }
+            if (lane == 0) {
+                sm.red_m[warp] = m;
+                sm.red_l[warp] = lsum;
+            }
+            named_bar_sync(1, CWARPS * 32);
+            const int t = threadIdx.x;
+            float M = -INFINITY;
+#pragma unroll
+            for (int w2 = 0; w2 < CWARPS; ++w2) M = fmaxf(M, sm.red_m[w2]);
+            const size_t bh = (size_t)d.b * p.Hq + d.h;
+            if (t < D) {
+                float Lt = 0.f, Ot = 0.f;
+#pragma unroll
+                for (int w2 = 0; w2 < CWARPS; ++w2) {
+                    const float mw = sm.red_m[w2];
+                    const float f = (mw == -INFINITY) ? 0.f : ex2(mw - M);
+                    Lt = fmaf(f, sm.red_l[w2], Lt);
+                    Ot = fmaf(f, sm.red_o[w2][t], Ot);
+                }
+                if (d.nchunks == 1) {
+                    p.out[bh * D + t] = __float2bfloat16_rn(Lt > 0.f ? Ot / Lt : 0.f);
+                } else {
+                    float *pp = p.partial + (bh * p.max_chunks + d.c) * (D + 2);
+                    pp[t] = Ot;
+                    if (t == 0) {
+                        pp[D] = M;
+                        pp[D + 1] = Lt;
+                    }
+                    __threadfence();
+                }
+            }
+            if (d.nchunks > 1) {
+                named_bar_sync(1, CWARPS * 32);
+                if (t == 0) {
+                    const int old = atomicAdd(&p.tickets[bh], 1);
+                    sm.last_flag = (old == d.nchunks - 1);
+                }
+                named_bar_sync(1, CWARPS * 32);
+                if (sm.last_flag) {
+                    __threadfence();
+                    if (t < D) {
+                        const float *pp = p.partial + bh * p.max_chunks * (D + 2);
+                        float Mc = -INFINITY;
+                        for (int c = 0; c < d.nchunks; ++c) Mc = fmaxf(Mc, __ldcg(pp + c * (D + 2) + D));
+                        float Lc = 0.f, Oc = 0.f;
+                        for (int c = 0; c < d.nchunks; ++c) {
+                            const float mc = __ldcg(pp + c * (D + 2) + D);
+                            const float f = (mc == -INFINITY) ? 0.f : ex2(mc - Mc);
+                            Lc = fmaf(f, __ldcg(pp + c * (D + 2) + D + 1), Lc);
+                            Oc = fmaf(f, __ldcg(pp + c * (D + 2) + t), Oc);
+                        }
+                        p.out[bh * D + t] = __float2bfloat16_rn(Lc > 0.f ? Oc / Lc : 0.f);
+                    }
+                    if (t == 0) p.tickets[bh] = 0;
+                }
+            }
+            named_bar_sync(1, CWARPS * 32);
+        }
+    }
+}
+
+template <int D>
+cudaError_t launch_d(const DecodeArgs &a, cudaStream_t s) {
+    static int num_sms = 0;
+    if (!num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const size_t smem = sizeof(Smem<D>);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(decode_attention_kernel<D>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    Params p;
+    p.q = static_cast<const __nv_bfloat16 *>(a.q);
+    p.k = static_cast<const __nv_bfloat16 *>(a.k);
+    p.v = static_cast<const __nv_bfloat16 *>(a.v);
+    p.mask = a.mask;
+    p.lens = a.lens;
+    p.pad = a.pad;
+    p.out = static_cast<__nv_bfloat16 *>(a.out);
+    p.partial = a.partial;
+    p.tickets = a.tickets;
+    p.B = a.slots;
+    p.Hq = a.q_heads;
+    p.Hkv = a.kv_heads;
+    p.max_ctx = a.max_ctx;
+    p.max_chunks = a.max_chunks;
+    p.scale_log2 = a.scale * 1.4426950408889634f;
+    decode_attention_kernel<D><<<2 * num_sms, THREADS, smem, s>>>(p);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+size_t decode_partial_bytes(int slots, int q_heads, int head_dim, int max_ctx) {
+    return (size_t)slots * q_heads * ceil_div(max_ctx, CHUNK) * (head_dim + 2) * sizeof(float);
+}
+size_t decode_ticket_bytes(int slots, int q_heads) { return (size_t)slots * q_heads * sizeof(int32_t); }
+bool decode_supported_head_dim(int d) { return d == 16 || d == 32 || d == 64 || d == 128; }
+
+cudaError_t launch_decode_attention(const DecodeArgs &a, cudaStream_t s) {
+    switch (a.head_dim) {
+        case 16: return launch_d<16>(a, s);
+        case 32: return launch_d<32>(a, s);
+        case 64: return launch_d<64>(a, s);
+        case 128: return launch_d<128>(a, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace baton

@@ -1,0 +1,75 @@
+// kernels.h -- internal launcher interface between the C ABI (baton_api.cu) and
+// the sm_100a kernels.  Not part of the public boundary (include/baton.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace baton {
+
+constexpr int CHUNK = 256;      // split-K chunk (keys), == BATON_CHUNK
+constexpr int MAX_SLOTS = 256;  // per-shard slot limit (kernel-parameter and smem arrays)
+constexpr int MAX_SPLICE_JOBS = 64;
+constexpr int MAX_MASK_OPS = 2 * MAX_SLOTS + 2;
+
+inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+// ------------------------------------------------------------ decode attention
+struct DecodeArgs {
+    const void *q, *k, *v;
+    const uint8_t *mask;            // nullable
+    const int32_t *lens, *pad;
+    void *out;
+    float *partial;                 // [slots][q_heads][max_chunks][head_dim + 2]
+    int32_t *tickets;               // [slots][q_heads], zero between calls
+    int slots, q_heads, kv_heads, head_dim, max_ctx, max_chunks;
+    float scale;
+};
+size_t decode_partial_bytes(int slots, int q_heads, int head_dim, int max_ctx);
+size_t decode_ticket_bytes(int slots, int q_heads);
+bool decode_supported_head_dim(int head_dim);
+cudaError_t launch_decode_attention(const DecodeArgs &a, cudaStream_t s);
+
+// ------------------------------------------------------------ metadata / mask
+cudaError_t launch_mask_update(uint8_t *mask, int32_t *S, int32_t *lens, int slots, int max_ctx,
+                               cudaStream_t s);
+cudaError_t launch_append_kv(void *k_layer, void *v_layer, const void *k_new, const void *v_new,
+                             const int32_t *lens, int slots, int kv_heads, int head_dim,
+                             int max_ctx, cudaStream_t s);
+
+enum MaskOpKind : int32_t { MOP_ZERO_ROW = 0, MOP_SHIFT_LEFT = 1, MOP_SHIFT_RIGHT = 2, MOP_SET_ROW = 3 };
+struct MaskOp {
+    int32_t kind, slot, a, b;   // ZERO_ROW(slot); SHIFT_LEFT(a=p); SHIFT_RIGHT(a=e); SET_ROW(slot, a=pad, b=S)
+};
+// Applies `ops` in order to every mask row, then writes S/lens/pad (host values) to the device.
+cudaError_t launch_mask_splice(uint8_t *mask, int slots, int max_ctx, const MaskOp *ops, int nops,
+                               int32_t *d_S, int32_t *d_lens, int32_t *d_pad, int S,
+                               const int32_t *lens, const int32_t *pad, cudaStream_t s);
+// Moves mask rows src->dst (dst rows are free), zeroes src, then writes metadata.
+cudaError_t launch_mask_move(uint8_t *mask, int slots, int max_ctx, const int32_t *src,
+                             const int32_t *dst, int nmoves, int32_t *d_S, int32_t *d_lens,
+                             int32_t *d_pad, int S, const int32_t *lens, const int32_t *pad,
+                             cudaStream_t s);
+
+// ------------------------------------------------------------ KV splice copies
+// For every job, layer l < layers, kv head h < kv_heads and K/V:
+//   copy `rows` rows of head_dim bf16 from  src + l*src_ls + h*src_hs
+//                                      to   dst + l*dst_ls + h*dst_hs   (strides in elements)
+struct CopyJob {
+    const void *src_k, *src_v;
+    void *dst_k, *dst_v;
+    int64_t src_ls, src_hs, dst_ls, dst_hs;
+    int32_t rows, pad_;
+};
+cudaError_t launch_kv_copy(const CopyJob *jobs, int njobs, int layers, int kv_heads, int head_dim,
+                           cudaStream_t s);
+
+// ------------------------------------------------------------ harness generator
+cudaError_t launch_keygen_tokens(void *out, const int32_t *qids, const int32_t *pos, int layers,
+                                 int n_slots, int heads, int head_dim, int kind, int layer0,
+                                 uint64_t seed, int scale_exp, cudaStream_t s);
+cudaError_t launch_keygen_history(void *out, int layers, int heads, int head_dim, int qid,
+                                  int pos_begin, int n, int kind, uint64_t seed, int scale_exp,
+                                  int64_t head_stride, int64_t layer_stride, cudaStream_t s);
+
+}  // namespace baton

@@ -1,0 +1,183 @@
+"""Decode-loop engine: executes the planner's decisions on one GPU's shard.
+
+One process per GPU.  Per iteration (reading of P:L101 / P:L124):
+
+    [t > 0]  tokens for the decoding slots (harness: keyed generator, or a
+             pre-generated HBM buffer in the benchmark)
+             baton_mask_update                       (a1)
+             for every layer: baton_decode_layer     (a2 append + a3 attention)
+             completion flags -> all_gather over NCCL (the only collective)
+             baton_remove(finished)  (+ release)     (a4)
+             baton_extract + baton_remove(victims)   (a6)
+             baton_compact                            (a7)
+    baton_insert_many(new queries)                   (a5)
+
+Every device byte is produced by libbaton kernels (plus the harness keygen).
+"""
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Tuple
+
+import numpy as np
+import torch
+
+from .baton import BatonShard, baton_keygen_tokens, baton_keygen_history
+from .comm import gather_completion_flags
+from .scheduler import Planner
+
+KIND_Q, KIND_K, KIND_V = 0, 1, 2
+
+
+@dataclass
+class StepStats:
+    t: int
+    decoded: int = 0
+    inserted: int = 0
+    removed: int = 0
+    stored: int = 0
+    released: int = 0
+    live_rows: int = 0          # sum of lens over decoding slots (keys read per layer per head group)
+    insert_rows: int = 0        # prefilled rows embedded
+    extract_rows: int = 0
+    compact_rows: int = 0
+
+
+class Engine:
+    def __init__(self, wl, rank=0, world=1, device=None, group=None, keep_outputs=False,
+                 keep_layers=None, token_source=None, prefill_source=None):
+        self.wl = wl
+        self.rank = rank
+        self.world = world
+        self.group = group
+        self.device = torch.device(device or "cuda")
+        self.planner = Planner(wl, world)
+        self.B = self.planner.per_rank
+        self.shard = BatonShard(wl.layers, self.B, wl.q_heads, wl.kv_heads, wl.head_dim,
+                                wl.max_ctx, device=self.device)
+        L, B, D = wl.layers, self.B, wl.head_dim
+        self.q = torch.zeros((L, B, wl.q_heads, D), dtype=torch.bfloat16, device=self.device)
+        self.k_new = torch.zeros((L, B, wl.kv_heads, D), dtype=torch.bfloat16, device=self.device)
+        self.v_new = torch.zeros_like(self.k_new)
+        self.out = torch.zeros((L, B, wl.q_heads, D), dtype=torch.bfloat16, device=self.device)
+        self.d_qid = torch.full((B,), -1, dtype=torch.int32, device=self.device)
+        self.d_pos = torch.zeros((B,), dtype=torch.int32, device=self.device)
+        self.stash: Dict[int, Tuple[torch.Tensor, torch.Tensor]] = {}
+        self.keep_outputs = keep_outputs
+        self.keep_layers = keep_layers
+        self.outputs: Dict[Tuple[int, int], np.ndarray] = {}
+        self.token_source = token_source
+        self.prefill_source = prefill_source
+        self.flag_buf = None
+        self.last_decisions = None
+
+    # ---------------------------------------------------------------- inputs (harness)
+    def _gen_tokens(self, dec_local):
+        wl = self.wl
+        qid = np.full(self.B, -1, np.int32)
+        pos = np.zeros(self.B, np.int32)
+        for b, q, p in dec_local:
+            qid[b], pos[b] = q, p
+        self.d_qid.copy_(torch.from_numpy(qid))
+        self.d_pos.copy_(torch.from_numpy(pos))
+        L, B, D = wl.layers, self.B, wl.head_dim
+        baton_keygen_tokens(self.q, self.d_qid, self.d_pos, L, B, wl.q_heads, D, KIND_Q, 0,
+                            wl.seed, wl.scales[0])
+        baton_keygen_tokens(self.k_new, self.d_qid, self.d_pos, L, B, wl.kv_heads, D, KIND_K, 0,
+                            wl.seed, wl.scales[1])
+        baton_keygen_tokens(self.v_new, self.d_qid, self.d_pos, L, B, wl.kv_heads, D, KIND_V, 0,
+                            wl.seed, wl.scales[2])
+        return self.q, self.k_new, self.v_new
+
+    def _prefill(self, qid, length):
+        if self.prefill_source is not None:
+            return self.prefill_source(qid, length)
+        wl = self.wl
+        shape = (wl.layers, wl.kv_heads, length, wl.head_dim)
+        K = torch.empty(shape, dtype=torch.bfloat16, device=self.device)
+        V = torch.empty_like(K)
+        baton_keygen_history(K, wl.layers, wl.kv_heads, wl.head_dim, qid, 0, length, KIND_K,
+                             wl.seed, wl.scales[1])
+        baton_keygen_history(V, wl.layers, wl.kv_heads, wl.head_dim, qid, 0, length, KIND_V,
+                             wl.seed, wl.scales[2])
+        return K, V
+
+    # ---------------------------------------------------------------- one iteration
+    def done(self):
+        return self.planner.finished_all()
+
+    def decode(self, stats):
+        """a1 + per layer a2/a3 for the slots the planner says are live."""
+        pl = self.planner
+        dec = [(pl.local(g), q, p) for g, q, p in pl.decode_plan() if pl.rank_of(g) == self.rank]
+        stats.decoded = len(dec)
+        stats.live_rows = sum(p + 1 for _, _, p in dec)
+        if self.token_source is not None:
+            q, k, v = self.token_source(pl.t, dec)
+        else:
+            q, k, v = self._gen_tokens(dec)
+        sh = self.shard
+        sh.baton_mask_update()
+        for l in range(self.wl.layers):
+            sh.baton_decode_layer(l, q[l], self.out[l], k[l], v[l])
+        if self.keep_outputs and dec:
+            layers = self.keep_layers if self.keep_layers is not None else range(self.wl.layers)
+            o = self.out[list(layers)].float().cpu().numpy()
+            for b, qq, p in dec:
+                self.outputs[(qq, p)] = o[:, b].copy()
+        return dec
+
+    def _gather_flags(self, local_flags):
+        return gather_completion_flags(local_flags, self.world, self.group, self.device)
+
+    def iteration(self):
+        pl = self.planner
+        stats = StepStats(pl.t)
+        flags = None
+        if pl.t > 0:
+            self.decode(stats)
+            local = pl.local_completion_flags(self.rank)
+            # completion flags + occupancy summary of every rank
+            flags = self._gather_flags(local) if self.world > 1 else None
+        d = pl.plan(flags)
+        self.last_decisions = d
+        sh = self.shard
+        fin = [pl.local(g) for g, _ in d.finished if pl.rank_of(g) == self.rank]
+        if d.t > 0:
+            # removal + release every iteration (C5); a no-op call enqueues nothing
+            stats.released += sh.baton_remove(fin)
+            stats.removed = len(fin)
+        vic = [(pl.local(g), q, n) for g, q, n in d.victims if pl.rank_of(g) == self.rank]
+        if vic:
+            for b, q, n in vic:
+                self.stash[q] = sh.baton_extract(b)
+                stats.extract_rows += n
+            stats.released += sh.baton_remove([b for b, _, _ in vic])
+            stats.stored = len(vic)
+        if d.resize is not None:
+            before = sh.baton_query()
+            o2n = sh.baton_compact(d.resize)
+            stats.compact_rows = int(sum(before["lens"][b] for b in range(self.B) if o2n[b] != b))
+        ins = [(pl.local(g), q, n, home) for g, q, n, home in d.inserts
+               if pl.rank_of(g) == self.rank]
+        if ins:
+            slots, ks, vs, lens = [], [], [], []
+            for b, q, n, home in ins:
+                if home is not None:
+                    K, V = self.stash.pop(q)
+                else:
+                    K, V = self._prefill(q, n)
+                slots.append(b)
+                ks.append(K)
+                vs.append(V)
+                lens.append(n)
+            sh.baton_insert_many(slots, ks, vs, lens)
+            stats.inserted = len(ins)
+            stats.insert_rows = sum(lens)
+        return stats
+
+    def run(self, max_iters=None):
+        all_stats = []
+        while not self.done():
+            all_stats.append(self.iteration())
+            if max_iters is not None and len(all_stats) >= max_iters:
+                break
+        return all_stats

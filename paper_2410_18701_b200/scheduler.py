@@ -1,0 +1,198 @@
+"""Host-side relay-race scheduler of the product path (replicated on every rank).
+
+Baton inserts a new query "as soon as inference of any query is completed, like
+a relay race" and, with P&D decoupling, every query in the
+batch decodes width-1.  This module only DECIDES (which slots finish, which
+queries are stored/re-inserted, where each query goes); the engine
+(``engine.py``) executes the decisions through libbaton.  It is deterministic
+and replicated: every rank runs the same planner on the same inputs (the
+workload, the control events, and the per-iteration completion flags that the
+engine all-gathers), so no rank ever broadcasts a decision.
+
+Policy readings: C5 release after removals and before inserts;
+C7 inserts of an iteration in ascending slot order; C8 FCFS, lowest free slot,
+stored queries re-enter at the queue head; C9 A decode iterations per query;
+C17 victims = most recently inserted, ties by higher qid; C18/C19 resize and
+stable compaction; C20 global slot g lives on rank g // B_g; C20b a stored
+query may only re-enter on the rank holding its stored K/V.
+"""
+from collections import deque
+from dataclasses import dataclass, field
+from typing import List, Optional, Tuple
+
+
+@dataclass
+class QueueEntry:
+    qid: int
+    length: int                 # prefilled / stored K/V length
+    home: Optional[int] = None  # rank holding stored K/V (None = fresh query)
+
+
+@dataclass
+class Decisions:
+    t: int
+    decode: List[Tuple[int, int, int]] = field(default_factory=list)    # (gslot, qid, pos)
+    finished: List[Tuple[int, int]] = field(default_factory=list)       # (gslot, qid)
+    victims: List[Tuple[int, int, int]] = field(default_factory=list)   # (gslot, qid, length)
+    resize: Optional[int] = None                                         # new active per rank
+    inserts: List[Tuple[int, int, int, Optional[int]]] = field(default_factory=list)  # (gslot, qid, len, home)
+
+
+class Planner:
+    def __init__(self, wl, world=1):
+        self.wl = wl
+        self.world = world
+        if wl.slots % world:
+            raise ValueError("slots must divide evenly across ranks")
+        self.per_rank = wl.slots // world
+        self.active = wl.initial_active() // world          # active slots per rank
+        self.occupant = [-1] * wl.slots                      # gslot -> qid
+        self.length = [0] * wl.slots                         # gslot -> live length
+        self.meta = {q.qid: q for q in wl.queries}
+        self.done_tokens = {q.qid: 0 for q in wl.queries}
+        self.entered = {}                                    # qid -> iteration of last insert
+        self.pending = sorted(wl.queries, key=lambda q: (q.arrival, q.qid))
+        self.next_arrival = 0
+        self.queue = deque()
+        self.t = 0
+
+    # ---------------------------------------------------------------- queries
+    def rank_of(self, g):
+        return g // self.per_rank
+
+    def local(self, g):
+        return g % self.per_rank
+
+    def live(self):
+        return [(g, q) for g, q in enumerate(self.occupant) if q >= 0]
+
+    def finished_all(self):
+        if self.wl.iterations >= 0 and self.t >= self.wl.iterations:
+            return True
+        return self.next_arrival >= len(self.pending) and not self.queue and not self.live()
+
+    # ---------------------------------------------------------------- phase 1: decode
+    def decode_plan(self):
+        """Slots that decode this iteration and the position each one handles."""
+        return [(g, q, self.length[g]) for g, q in self.live()]
+
+    def local_completion_flags(self, rank):
+        """Per local slot: 1 if the query there produced its last token in the
+        decode just executed (the engine all-gathers these)."""
+        flags = []
+        for b in range(self.per_rank):
+            g = rank * self.per_rank + b
+            q = self.occupant[g]
+            flags.append(int(q >= 0 and self.done_tokens[q] + 1 >= self.meta[q].A))
+        return flags
+
+    def _victims(self, candidates, n):
+        order = sorted(candidates, key=lambda gq: (self.entered[gq[1]], gq[1]), reverse=True)
+        return order[:n]
+
+    # ---------------------------------------------------------------- one iteration
+    def plan(self, all_flags=None):
+        """Decide iteration t.  ``all_flags``: concatenated completion flags of
+        every rank (from the all-gather) -- used instead of local bookkeeping
+        so the decision depends on what the ranks reported."""
+        d = Decisions(self.t)
+        if self.t > 0:
+            d.decode = self.decode_plan()
+            for g, q, _ in d.decode:
+                self.done_tokens[q] += 1
+                self.length[g] += 1
+            for g, q in self.live():
+                done = (all_flags[g] != 0) if all_flags is not None else (
+                    self.done_tokens[q] >= self.meta[q].A)
+                if done:
+                    d.finished.append((g, q))
+            for g, _ in d.finished:
+                self.occupant[g] = -1
+                self.length[g] = 0
+            stored = []
+            ctl = self.wl.control
+            n_pre = 0
+            if self.t in ctl.preempt:
+                n_pre = ctl.preempt[self.t]
+            elif self.t in ctl.preempt_frac:
+                n_pre = int(ctl.preempt_frac[self.t] * len(self.live()))
+            n_pre = min(n_pre, len(self.live()))
+            if n_pre > 0:
+                for g, q in self._victims(self.live(), n_pre):
+                    stored.append(self._store(g, q, d))
+            if self.t in ctl.resize:
+                stored += self._resize(ctl.resize[self.t], d)
+            for e in reversed(stored):
+                self.queue.appendleft(e)
+        self._admit()
+        self._fill(d)
+        self.t += 1
+        return d
+
+    def _store(self, g, q, d):
+        d.victims.append((g, q, self.length[g]))
+        e = QueueEntry(q, self.length[g], self.rank_of(g))
+        self.occupant[g] = -1
+        self.length[g] = 0
+        return e
+
+    def _resize(self, ev, d):
+        if ev == "halve":
+            new = max(1, self.active // 2)
+        elif ev == "double":
+            new = min(self.per_rank, self.active * 2)
+        else:
+            new = max(1, min(self.per_rank, int(ev) // self.world))
+        out = []
+        if new < self.active:
+            for r in range(self.world):
+                base = r * self.per_rank
+                occ = [(base + b, self.occupant[base + b]) for b in range(self.per_rank)
+                       if self.occupant[base + b] >= 0]
+                over = sum(1 for g, _ in occ if g - base >= new)
+                room = sum(1 for b in range(new) if self.occupant[base + b] < 0)
+                if over > room:
+                    for g, q in self._victims(occ, over - room):
+                        out.append(self._store(g, q, d))
+                # stable compaction into the lowest free slots (mirrors baton_compact)
+                for b in range(new, self.per_rank):
+                    g = base + b
+                    if self.occupant[g] < 0:
+                        continue
+                    f = next(base + x for x in range(new) if self.occupant[base + x] < 0)
+                    self.occupant[f], self.length[f] = self.occupant[g], self.length[g]
+                    self.occupant[g], self.length[g] = -1, 0
+        self.active = new
+        d.resize = new
+        return out
+
+    def _admit(self):
+        while (self.next_arrival < len(self.pending)
+               and self.pending[self.next_arrival].arrival <= self.t):
+            q = self.pending[self.next_arrival]
+            self.queue.append(QueueEntry(q.qid, q.l_q, None))
+            self.next_arrival += 1
+
+    def _fill(self, d):
+        while self.queue:
+            free = [r * self.per_rank + b for r in range(self.world) for b in range(self.active)
+                    if self.occupant[r * self.per_rank + b] < 0]
+            if not free:
+                return
+            chosen = None
+            for idx, e in enumerate(self.queue):
+                for g in free:
+                    if e.home is None or self.rank_of(g) == e.home:
+                        chosen = (idx, g)
+                        break
+                if chosen:
+                    break
+            if chosen is None:
+                return
+            idx, g = chosen
+            e = self.queue[idx]
+            del self.queue[idx]
+            self.occupant[g] = e.qid
+            self.length[g] = e.length
+            self.entered[e.qid] = self.t
+            d.inserts.append((g, e.qid, e.length, e.home))

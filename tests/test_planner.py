@@ -1,0 +1,67 @@
+"""The product planner (paper_2410_18701_b200/scheduler.py) takes exactly the
+decisions of the oracle's serving loop (oracle/schedule.py) -- the two are
+independent implementations of readings C5-C9, C17-C20b.  Slot indices are
+compared bit-exactly after every iteration."""
+import numpy as np
+import pytest
+
+from baton_inputs import w1_workload, random_stream, config_workload
+from oracle import Simulator
+from paper_2410_18701_b200.scheduler import Planner
+
+
+def _compare(wl, G=None, max_iters=100000):
+    G = G or wl.gpus
+    sim = Simulator(wl, G=G)
+    pl = Planner(wl, G)
+    n = 0
+    while True:
+        rec = sim.iteration()
+        d = pl.plan()
+        assert d.t == rec.t
+        assert sorted(d.decode) == sorted(rec.decoded), rec.t
+        assert sorted(g for g, _ in d.finished) == sorted(rec.removed), rec.t
+        assert [(q, g) for g, q, _ in d.victims] == rec.preempted, rec.t
+        if rec.resized is not None:
+            assert d.resize * G == rec.resized
+        assert [(g, q, l) for g, q, l, _ in d.inserts] == rec.inserted, rec.t
+        occ = np.concatenate(rec.qid)
+        assert list(occ) == pl.occupant, rec.t
+        lens = np.concatenate(rec.lens)
+        assert list(lens) == pl.length, rec.t
+        n += 1
+        if sim.done() or n >= max_iters:
+            assert pl.finished_all() == sim.done()
+            break
+    return n
+
+
+def test_w1():
+    assert _compare(w1_workload()) == 19
+
+
+@pytest.mark.parametrize("seed", range(0, 200, 5))
+def test_random_streams(seed):
+    _compare(random_stream(seed))
+
+
+@pytest.mark.parametrize("name,G", [("7b", 1), ("13b", 1), ("13b", 2), ("13b", 8), ("70b", 8)])
+def test_configs(name, G):
+    wl = config_workload(name, gpus=G, n_queries=150 if name != "13b" else 300)
+    _compare(wl, G)
+
+
+@pytest.mark.parametrize("G", [1, 2, 8])
+def test_stress_with_preemption_and_resize(G):
+    wl = config_workload("stress", gpus=G, n_queries=400)
+    wl.iterations = 200
+    _compare(wl, G)
+
+
+def test_flags_path_equals_local_bookkeeping():
+    wl = config_workload("13b", gpus=4, n_queries=200)
+    a, b = Planner(wl, 4), Planner(wl, 4)
+    for _ in range(60):
+        flags = sum((b.local_completion_flags(r) for r in range(4)), []) if b.t > 0 else None
+        da, db = a.plan(), b.plan(flags)
+        assert da == db
