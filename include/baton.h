@@ -179,6 +179,22 @@ int  baton_extract(baton_state *st, int slot, void *k_out, void *v_out, void *st
  * Errors: BATON_E_CAPACITY if the occupied slots do not fit. */
 int  baton_compact(baton_state *st, int n_active, int32_t *old_to_new, void *stream);
 
+/* ---------------------------------------------------------------- prefill side
+ * a8 -- P:L132 "all original queries awaiting processing are initially
+ * prefilled by the model", decoupled from decoding (P&D, P:L215 asynchronous).
+ * Causal scaled-dot-product attention of a new query over its own prompt:
+ *     O[h][i] = sum_{j <= i} softmax_j(scale * Q[h][i] . K[g][j]) V[g][j],
+ * g = h*kv_heads/q_heads (C11), i.e. for every i the decode attention (a3) of
+ * the prefix [0, i].  Runs on the tensor cores (tcgen05.mma, TMEM accumulators,
+ * TMA tiles); P is rounded to bf16 for the P.V product.
+ *   Q, O : device bf16 [q_heads][len][head_dim];  K, V : [kv_heads][len][head_dim]
+ *          (one layer of the prefilled K/V that baton_insert embeds)
+ *   head_dim must be 128; 16-B aligned pointers.  Run it on a side stream to
+ *   overlap the decode loop (the insert then waits on an event).
+ * Errors: BATON_E_INVALID. */
+int  baton_prefill_attention(const void *q, const void *k, const void *v, void *out, int len,
+                             const baton_shape *shape, float scale, void *stream);
+
 /* ---------------------------------------------------------------- misc */
 const char *baton_error_string(int code);
 /* The cudaError_t of the last BATON_E_CUDA returned on this thread. */

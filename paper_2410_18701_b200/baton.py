@@ -52,6 +52,18 @@ def baton_decode_attention(q, k, v, mask, lens, pad_start, out, shape, scale, wo
     return out
 
 
+def baton_prefill_attention(q, k, v, out, length, q_heads, kv_heads, head_dim, scale=None,
+                            stream=None):
+    """a8 (see include/baton.h): causal attention of a new query over its prompt.
+    q, out: [q_heads][len][head_dim]; k, v: [kv_heads][len][head_dim] (bf16, CUDA)."""
+    shape = make_shape(1, 1, q_heads, kv_heads, head_dim, 16)
+    check(lib.baton_prefill_attention(_ptr(q), _ptr(k), _ptr(v), _ptr(out), length,
+                                      ctypes.byref(shape),
+                                      ctypes.c_float(scale or 1.0 / math.sqrt(head_dim)),
+                                      _stream(stream)), "baton_prefill_attention")
+    return out
+
+
 def baton_keygen_tokens(out, qids, pos, layers, n_slots, heads, head_dim, kind, layer0, seed,
                         scale_exp, stream=None):
     check(lib.baton_keygen_tokens(_ptr(out), _ptr(qids), _ptr(pos), layers, n_slots, heads,
@@ -169,9 +181,10 @@ class BatonShard:
               "baton_insert_many")
 
     def baton_extract(self, slot, k_out=None, v_out=None, stream=None):
-        n = int(self.baton_query()["lens"][slot])
+        n = int(self.baton_query()["lens"][slot]) if 0 <= slot < self.B else 0
         if k_out is None:
-            k_out = torch.empty((self.L, self.Hkv, n, self.D), dtype=torch.bfloat16,
+            # an empty slot still gets (1-row) buffers so the call reports SLOT_EMPTY
+            k_out = torch.empty((self.L, self.Hkv, max(n, 1), self.D), dtype=torch.bfloat16,
                                 device=self.device)
             v_out = torch.empty_like(k_out)
         check(lib.baton_extract(self._h, slot, _ptr(k_out), _ptr(v_out), _stream(stream)),

@@ -378,6 +378,19 @@ int baton_compact(baton_state *st, int n_active, int32_t *old_to_new, void *stre
                                         st->lens.data(), st->pad.data(), cs));
 }
 
+// ---------------------------------------------------------------- a8
+int baton_prefill_attention(const void *q, const void *k, const void *v, void *out, int len,
+                            const baton_shape *shape, float scale, void *stream) {
+    if (!q || !k || !v || !out || !shape || len < 1 || !(scale > 0.f)) return BATON_E_INVALID;
+    if (shape->q_heads < 1 || shape->kv_heads < 1 || shape->q_heads % shape->kv_heads ||
+        !prefill_supported(shape->head_dim))
+        return BATON_E_INVALID;
+    for (const void *ptr : {q, k, v, (const void *)out})
+        if (reinterpret_cast<uintptr_t>(ptr) & 15) return BATON_E_INVALID;
+    return cuda_status(launch_prefill_attention(q, k, v, out, len, shape->q_heads, shape->kv_heads,
+                                                shape->head_dim, scale, as_stream(stream)));
+}
+
 // ---------------------------------------------------------------- misc
 const char *baton_error_string(int code) {
     switch (code) {

@@ -64,6 +64,12 @@ struct CopyJob {
 cudaError_t launch_kv_copy(const CopyJob *jobs, int njobs, int layers, int kv_heads, int head_dim,
                            cudaStream_t s);
 
+// ------------------------------------------------------------ a8 prefill attention (tcgen05)
+bool prefill_supported(int head_dim);
+cudaError_t launch_prefill_attention(const void *q, const void *k, const void *v, void *out, int len,
+                                     int q_heads, int kv_heads, int head_dim, float scale,
+                                     cudaStream_t s);
+
 // ------------------------------------------------------------ harness generator
 cudaError_t launch_keygen_tokens(void *out, const int32_t *qids, const int32_t *pos, int layers,
                                  int n_slots, int heads, int head_dim, int kind, int layer0,

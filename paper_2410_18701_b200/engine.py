@@ -51,8 +51,11 @@ class Engine:
         self.device = torch.device(device or "cuda")
         self.planner = Planner(wl, world)
         self.B = self.planner.per_rank
+        # libbaton requires max_ctx % 16 == 0 (16-B aligned mask rows for the bulk
+        # copies); a larger capacity changes no result (C24 caps l_q + A anyway)
+        cap = (wl.max_ctx + 15) // 16 * 16
         self.shard = BatonShard(wl.layers, self.B, wl.q_heads, wl.kv_heads, wl.head_dim,
-                                wl.max_ctx, device=self.device)
+                                cap, device=self.device)
         L, B, D = wl.layers, self.B, wl.head_dim
         self.q = torch.zeros((L, B, wl.q_heads, D), dtype=torch.bfloat16, device=self.device)
         self.k_new = torch.zeros((L, B, wl.kv_heads, D), dtype=torch.bfloat16, device=self.device)

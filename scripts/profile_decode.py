@@ -1,0 +1,75 @@
+"""Time / profile decode attention alone on the cfg2 (7B) batch at iteration t0.
+
+    python scripts/profile_decode.py [--iters N] [--layers L]
+
+Builds one 7B-shaped shard (L layers, default 2), embeds every live query of the
+t0 state with its keyed history through baton_insert_many, runs one mask update,
+then launches baton_decode_attention N times per layer and reports the per-launch
+time (CUDA events) and algorithmic GB/s.  Used under ncu for the profiles/."""
+import argparse
+import json
+import math
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from baton_inputs import config_workload                                   # noqa: E402
+from paper_2410_18701_b200.baton import BatonShard, baton_keygen_history   # noqa: E402
+from paper_2410_18701_b200.scheduler import Planner                        # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--layers", type=int, default=4)
+    ap.add_argument("--t0", type=int, default=512)
+    ap.add_argument("--config", default="7b")
+    args = ap.parse_args()
+    wl = config_workload(args.config)
+    if args.config == "70b":
+        wl.slots, wl.gpus = 16, 1
+    pl = Planner(wl, 1)
+    while pl.t < args.t0:
+        pl.plan()
+    L = args.layers
+    sh = BatonShard(L, wl.slots, wl.q_heads, wl.kv_heads, wl.head_dim, wl.max_ctx)
+    slots, ks, vs, lens = [], [], [], []
+    for g, q in pl.live():
+        n = pl.length[g]
+        K = torch.empty((L, wl.kv_heads, n, wl.head_dim), dtype=torch.bfloat16, device="cuda")
+        V = torch.empty_like(K)
+        baton_keygen_history(K, L, wl.kv_heads, wl.head_dim, q, 0, n, 1, wl.seed, 0)
+        baton_keygen_history(V, L, wl.kv_heads, wl.head_dim, q, 0, n, 2, wl.seed, 0)
+        slots.append(g); ks.append(K); vs.append(V); lens.append(n)
+    sh.baton_insert_many(slots, ks, vs, lens)
+    del ks, vs
+    sh.baton_mask_update()
+    torch.cuda.synchronize()
+    m = sh.baton_query()
+    live = m["lens"]
+    q = torch.randn((wl.slots, wl.q_heads, wl.head_dim), device="cuda").to(torch.bfloat16)
+    out = torch.empty_like(q)
+    tau = 2 * wl.kv_heads * wl.head_dim * 2
+    nbytes = int(live.sum()) * tau + int((live > 0).sum()) * wl.q_heads * wl.head_dim * 4
+    times = []
+    for it in range(args.iters):
+        for l in range(L):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            sh.baton_decode_attention(l, q, out)
+            e1.record()
+            times.append((e0, e1))
+    torch.cuda.synchronize()
+    us = [a.elapsed_time(b) * 1e3 for a, b in times]
+    us_w = us[L:]   # drop the first pass
+    print(json.dumps({"config": args.config, "live_slots": int((live > 0).sum()),
+                      "sum_lens": int(live.sum()), "bytes_per_launch": nbytes,
+                      "us_median": float(np.median(us_w)), "us_min": float(np.min(us_w)),
+                      "GBps_median": nbytes / np.median(us_w) / 1e3}))
+
+
+if __name__ == "__main__":
+    main()

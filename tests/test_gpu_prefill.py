@@ -1,0 +1,85 @@
+"""a8 parity: baton_prefill_attention (tcgen05/TMEM/TMA kernel, through the C ABI)
+vs the oracle.  Causal prefill attention of a prompt is, for every position i,
+the decode attention of the prefix [0, i] -- O-1 applied position by position
+(P:L132 prefilled queries), so no separate oracle function is needed."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import solo_attention
+from gpu_util import ATTN_RTOL, bf16_bits, bits_to_f64, row_rel_err, require_cuda
+
+pytestmark = pytest.mark.gpu
+
+
+def _case(seed, Hq, Hkv, n, D=128, scale_k=1.0):
+    rng = np.random.default_rng(seed)
+    t = lambda a: torch.from_numpy(a.astype(np.float32)).cuda().to(torch.bfloat16)
+    Q = t(rng.uniform(-1, 1, (Hq, n, D)))
+    K = t(rng.uniform(-scale_k, scale_k, (Hkv, n, D)))
+    V = t(rng.uniform(-1, 1, (Hkv, n, D)))
+    return Q, K, V
+
+
+def _reference(Q, K, V, rows):
+    q = bits_to_f64(bf16_bits(Q))
+    k = bits_to_f64(bf16_bits(K))
+    v = bits_to_f64(bf16_bits(V))
+    return {i: solo_attention(q[:, i], k[:, :i + 1], v[:, :i + 1]) for i in rows}
+
+
+@pytest.mark.parametrize("Hq,Hkv,n", [(2, 2, 1), (2, 2, 5), (4, 4, 127), (4, 4, 128), (4, 2, 129),
+                                      (8, 1, 300), (8, 8, 700), (32, 32, 260), (64, 8, 200)])
+def test_prefill_matches_oracle(Hq, Hkv, n):
+    require_cuda()
+    from paper_2410_18701_b200.baton import baton_prefill_attention
+    Q, K, V = _case(n * 31 + Hq, Hq, Hkv, n)
+    O = torch.full_like(Q, float("nan"))
+    baton_prefill_attention(Q, K, V, O, n, Hq, Hkv, 128)
+    torch.cuda.synchronize()
+    got = bits_to_f64(bf16_bits(O))
+    assert np.isfinite(got).all()
+    rows = sorted(set([0, n - 1, n // 2] + list(np.random.default_rng(n).integers(0, n, 24))))
+    ref = _reference(Q, K, V, rows)
+    worst = max(row_rel_err(got[:, i], ref[i]) for i in rows)
+    assert worst <= ATTN_RTOL, worst
+
+
+def test_prefill_first_row_is_first_value():
+    """Row 0 attends only to key 0: o = v_0 (up to bf16 of P = 1 exactly)."""
+    require_cuda()
+    from paper_2410_18701_b200.baton import baton_prefill_attention
+    Q, K, V = _case(5, 4, 4, 200)
+    O = torch.empty_like(Q)
+    baton_prefill_attention(Q, K, V, O, 200, 4, 4, 128)
+    torch.cuda.synchronize()
+    assert np.array_equal(bf16_bits(O)[:, 0], bf16_bits(V)[:, 0])
+
+
+def test_prefill_last_row_equals_decode_attention():
+    """The last prefill row is the decode attention of the full prompt (a3)."""
+    require_cuda()
+    from paper_2410_18701_b200.baton import (baton_prefill_attention, baton_decode_attention,
+                                             make_shape, baton_decode_workspace_bytes)
+    n, H = 400, 8
+    Q, K, V = _case(6, H, H, n, scale_k=4.0)
+    O = torch.empty_like(Q)
+    baton_prefill_attention(Q, K, V, O, n, H, H, 128)
+    S_cap = 512
+    kc = torch.zeros((1, H, S_cap, 128), dtype=torch.bfloat16, device="cuda")
+    vc = torch.zeros_like(kc)
+    kc[0, :, :n] = K
+    vc[0, :, :n] = V
+    shape = make_shape(1, 1, H, H, 128, S_cap)
+    ws = torch.zeros(baton_decode_workspace_bytes(shape), dtype=torch.uint8, device="cuda")
+    od = torch.empty((1, H, 128), dtype=torch.bfloat16, device="cuda")
+    lens = torch.tensor([n], dtype=torch.int32, device="cuda")
+    pad = torch.zeros(1, dtype=torch.int32, device="cuda")
+    baton_decode_attention(Q[:, n - 1][None].contiguous(), kc, vc, None, lens, pad, od, shape,
+                           1 / math.sqrt(128), ws)
+    torch.cuda.synchronize()
+    a = bits_to_f64(bf16_bits(O[:, n - 1]))
+    b = bits_to_f64(bf16_bits(od[0]))
+    assert row_rel_err(a, b) <= ATTN_RTOL
