@@ -176,6 +176,7 @@ int baton_decode_attention(const void *q, const void *k, const void *v, const ui
     a.pad = pad_start;
     a.out = out;
     a.tickets = static_cast<int32_t *>(workspace);
+    a.counters = a.tickets + (size_t)shape->slots * shape->q_heads;
     a.partial = reinterpret_cast<float *>(static_cast<uint8_t *>(workspace) + ticket_region(shape));
     a.slots = shape->slots;
     a.q_heads = shape->q_heads;
@@ -187,20 +188,41 @@ int baton_decode_attention(const void *q, const void *k, const void *v, const ui
     return cuda_status(launch_decode_attention(a, as_stream(stream)));
 }
 
+namespace {
+DecodeArgs layer_args(baton_state *st, int layer, const void *q, const void *k_new, const void *v_new,
+                      void *out) {
+    const baton_shape &s = st->sh;
+    DecodeArgs a;
+    a.q = q;
+    a.k = layer_ptr(st->cfg.k_cache, st, layer);
+    a.v = layer_ptr(st->cfg.v_cache, st, layer);
+    a.k_new = k_new;
+    a.v_new = v_new;
+    a.mask = st->cfg.mask;
+    a.lens = st->d_lens;
+    a.pad = st->d_pad;
+    a.out = out;
+    a.tickets = st->tickets;
+    a.counters = st->tickets + (size_t)s.slots * s.q_heads;
+    a.partial = st->partial;
+    a.slots = s.slots;
+    a.q_heads = s.q_heads;
+    a.kv_heads = s.kv_heads;
+    a.head_dim = s.head_dim;
+    a.max_ctx = s.max_ctx;
+    a.max_chunks = st->max_chunks;
+    a.scale = 1.0f / sqrtf((float)s.head_dim);
+    return a;
+}
+}  // namespace
+
 int baton_decode_layer(baton_state *st, int layer, const void *q, const void *k_new,
                        const void *v_new, void *out, void *stream) {
     if (!st || !q || !out || layer < 0 || layer >= st->sh.layers) return BATON_E_INVALID;
     if ((k_new == nullptr) != (v_new == nullptr)) return BATON_E_INVALID;
-    if (k_new) {
-        int r = baton_append_kv(st, layer, k_new, v_new, stream);
-        if (r) return r;
-    }
-    const baton_shape &s = st->sh;
-    return baton_decode_attention(q, layer_ptr(st->cfg.k_cache, st, layer),
-                                  layer_ptr(st->cfg.v_cache, st, layer), st->cfg.mask, st->d_lens,
-                                  st->d_pad, out, &s, 1.0f / sqrtf((float)s.head_dim),
-                                  reinterpret_cast<uint8_t *>(st->tickets),
-                                  baton_decode_workspace_bytes(&s), stream);
+    // a2 fused into a3: one launch streams the cache and embeds the new token
+    return cuda_status(launch_decode_attention(layer_args(st, layer, q, k_new, v_new, out),
+                                               as_stream(stream)));
 }
 
 // ---------------------------------------------------------------- a4

@@ -80,6 +80,14 @@ BATON_DEV float ex2(float x) {
     return y;
 }
 
+// gpu-scope acquire-release fetch-add: publishes (cumulatively) everything this
+// thread has observed, e.g. partials other threads wrote before an mbarrier it waited on
+BATON_DEV int atom_add_acq_rel_gpu(int32_t *p, int v) {
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
 // named barrier among `nthreads` threads (ids >= 1; 0 is __syncthreads)
 BATON_DEV void named_bar_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");

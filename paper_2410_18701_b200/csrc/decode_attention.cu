@@ -24,6 +24,7 @@
 //     (b, h) (atomic ticket) merges the chunk partials in ascending chunk order.
 #include "common.cuh"
 #include "kernels.h"
+#include "sched.cuh"
 
 namespace baton {
 namespace {
@@ -33,14 +34,13 @@ constexpr int ROWS_PER_WARP = 16;
 constexpr int TILE = CWARPS * ROWS_PER_WARP;   // 64 keys per stage
 constexpr int STAGES = 3;
 constexpr int THREADS = (CWARPS + 1) * 32;
-constexpr int TILES_PER_CHUNK = CHUNK / TILE;
 
-constexpr int F_FIRST = 1, F_LAST = 2, F_END = 4;
+constexpr int F_FIRST = 1, F_LAST = 2, F_END = 4, F_WRITE = 8;
 
 __device__ __forceinline__ int ceil_div_dev(int L) { return (L + CHUNK - 1) / CHUNK; }
 
 struct StageDesc {
-    int32_t b, h, c, nrows, flags, moff, nchunks, pad_;
+    int32_t b, h, c, nrows, flags, moff, nchunks, wrow;
 };
 
 template <int D>
@@ -54,6 +54,9 @@ struct __align__(16) Stage {
 
 struct Params {
     const __nv_bfloat16 *q, *k, *v;
+    const __nv_bfloat16 *k_new, *v_new;      // fused append (nullable)
+    __nv_bfloat16 *k_w, *v_w;                // cache base for the append write-back
+    int32_t *counters;                       // dynamic work counter (workspace)
     const uint8_t *mask;
     const int32_t *lens, *pad;
     __nv_bfloat16 *out;
@@ -67,12 +70,10 @@ template <int D>
 struct Smem {
     Stage<D> st[STAGES];
     uint64_t full[STAGES], empty[STAGES];
-    int32_t prefix[MAX_SLOTS + 1];
-    int32_t lens[MAX_SLOTS];
-    int32_t pad[MAX_SLOTS];
-    float red_o[CWARPS][D];
-    float red_m[CWARPS], red_l[CWARPS];
-    int32_t last_flag;
+    WorkSched ws;
+    float red_o[2][CWARPS][D];
+    float red_m[2][CWARPS], red_l[2][CWARPS];
+    uint64_t part_bar;
 };
 
 template <int D>
@@ -93,6 +94,7 @@ __global__ void __launch_bounds__(THREADS, 2) decode_attention_kernel(const Para
             mbar_init(&sm.full[s], 1);
             mbar_init(&sm.empty[s], CWARPS);
         }
+        mbar_init(&sm.part_bar, CWARPS * 32);
         fence_mbar_init();
     }
     // Empty slots produce a zero output row (C6).
@@ -106,42 +108,20 @@ __global__ void __launch_bounds__(THREADS, 2) decode_attention_kernel(const Para
 
     if (warp == CWARPS) {
         // ============================ producer warp ============================
-        // Item enumeration: items per slot = nchunks(b) * Hq, prefix-summed.
-        int running = 0;
-        for (int b0 = 0; b0 < p.B; b0 += 32) {
-            int b = b0 + lane;
-            int L = 0, P = 0;
-            if (b < p.B) {
-                L = p.lens[b];
-                P = p.pad[b];
-                sm.lens[b] = L;
-                sm.pad[b] = P;
-            }
-            int n = (L > 0 ? ceil_div_dev(L) : 0) * p.Hq;
-            int incl = n;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                int t = __shfl_up_sync(FULL_MASK, incl, o);
-                if (lane >= o) incl += t;
-            }
-            if (b < p.B) sm.prefix[b] = running + incl - n;
-            running += __shfl_sync(FULL_MASK, incl, 31);
-        }
-        if (lane == 0) sm.prefix[p.B] = running;
-        __syncwarp();
+        sched_build(sm.ws, p.lens, p.pad, p.B, p.Hq, lane);
         if (lane != 0) return;
-        const int total = running;
+        const int total = sched_total(sm.ws, p.Hq);
         const uint64_t pol = policy_evict_first();
         int stage = 0;
         uint32_t phase = 0;
         int b = 0;
-        for (int w = blockIdx.x; w < total; w += gridDim.x) {
-            while (sm.prefix[b + 1] <= w) ++b;
-            const int L = sm.lens[b];
+        int w = sched_next(p.counters);
+        while (w < total) {
+            const int w_next = sched_next(p.counters);   // prefetch: latency hidden by this item
+            int c, h;
+            sched_item(sm.ws, w, p.Hq, b, c, h);
+            const int L = sm.ws.lens[b];
             const int nch = ceil_div_dev(L);
-            const int rem = w - sm.prefix[b];
-            const int c = rem / p.Hq;
-            const int h = rem - c * p.Hq;
             const int g = h * p.Hkv / p.Hq;
             const int r0 = c * CHUNK;
             const int rows = min(CHUNK, L - r0);
@@ -149,8 +129,12 @@ __global__ void __launch_bounds__(THREADS, 2) decode_attention_kernel(const Para
             const __nv_bfloat16 *kb = p.k + head_off;
             const __nv_bfloat16 *vb = p.v + head_off;
             const int ntiles = (rows + TILE - 1) / TILE;
+            // fused append (a2): the item holding row L-1 takes the new token's k/v
+            // from k_new/v_new; the first q head of the kv group writes it to the cache
+            const bool app = p.k_new != nullptr && c == nch - 1;
             for (int t = 0; t < ntiles; ++t) {
                 const int nr = min(TILE, rows - t * TILE);
+                const bool app_tile = app && t == ntiles - 1;
                 mbar_wait(&sm.empty[stage], phase ^ 1);
                 Stage<D> &st = sm.st[stage];
                 uint32_t bytes = 2u * nr * D * 2;
@@ -160,7 +144,7 @@ __global__ void __launch_bounds__(THREADS, 2) decode_attention_kernel(const Para
                 if (p.mask) {
                     // aligned superset of the tile's mask bytes (row start is 16-B aligned)
                     const size_t row0 = (size_t)b * p.max_ctx;
-                    const size_t j0 = row0 + sm.pad[b] + r0 + t * TILE;
+                    const size_t j0 = row0 + sm.ws.pad[b] + r0 + t * TILE;
                     const size_t a0 = j0 & ~(size_t)15;
                     const size_t row_end = row0 + p.max_ctx;
                     size_t need = (j0 + nr - a0 + 15) & ~(size_t)15;
@@ -175,12 +159,22 @@ __global__ void __launch_bounds__(THREADS, 2) decode_attention_kernel(const Para
                 st.desc.h = h;
                 st.desc.c = c;
                 st.desc.nrows = nr;
-                st.desc.flags = (t == 0 ? F_FIRST : 0) | (t == ntiles - 1 ? F_LAST : 0);
+                st.desc.flags = (t == 0 ? F_FIRST : 0) | (t == ntiles - 1 ? F_LAST : 0) |
+                                (app_tile && h * p.Hkv % p.Hq == 0 ? F_WRITE : 0);
                 st.desc.moff = moff;
                 st.desc.nchunks = nch;
+                st.desc.wrow = L - 1;
                 mbar_arrive_expect_tx(&sm.full[stage], bytes);
-                bulk_g2s_evict_first(st.k, kb + (size_t)t * TILE * D, nr * D * 2, &sm.full[stage], pol);
-                bulk_g2s_evict_first(st.v, vb + (size_t)t * TILE * D, nr * D * 2, &sm.full[stage], pol);
+                const int ncache = app_tile ? nr - 1 : nr;
+                if (ncache > 0) {
+                    bulk_g2s_evict_first(st.k, kb + (size_t)t * TILE * D, ncache * D * 2, &sm.full[stage], pol);
+                    bulk_g2s_evict_first(st.v, vb + (size_t)t * TILE * D, ncache * D * 2, &sm.full[stage], pol);
+                }
+                if (app_tile) {
+                    const size_t nb = ((size_t)b * p.Hkv + g) * D;
+                    bulk_g2s(st.k + (nr - 1) * D, p.k_new + nb, D * 2, &sm.full[stage]);
+                    bulk_g2s(st.v + (nr - 1) * D, p.v_new + nb, D * 2, &sm.full[stage]);
+                }
                 if (mbytes) bulk_g2s(st.mask, msrc, mbytes, &sm.full[stage]);
                 if (t == 0) bulk_g2s(st.q, p.q + (size_t)(b * p.Hq + h) * D, D * 2, &sm.full[stage]);
                 if (++stage == STAGES) {
@@ -188,7 +182,9 @@ __global__ void __launch_bounds__(THREADS, 2) decode_attention_kernel(const Para
                     phase ^= 1;
                 }
             }
+            w = w_next;
         }
+        sched_done(p.counters);
         mbar_wait(&sm.empty[stage], phase ^ 1);
         sm.st[stage].desc.flags = F_END;
         mbar_arrive(&sm.full[stage]);
@@ -206,6 +202,8 @@ __global__ void __launch_bounds__(THREADS, 2) decode_attention_kernel(const Para
 
     int stage = 0;
     uint32_t phase = 0;
+    int rb = 0;                  // merge buffer of the current item
+    uint32_t part_phase = 0;     // parity of part_bar (tracked by warp 0)
     while (true) {
         mbar_wait(&sm.full[stage], phase);
         Stage<D> &st = sm.st[stage];
@@ -225,6 +223,14 @@ __global__ void __launch_bounds__(THREADS, 2) decode_attention_kernel(const Para
             for (int i = 0; i < 8; ++i) o[i] = 0.f;
         }
         const int base = warp * ROWS_PER_WARP;
+        if ((d.flags & F_WRITE) && warp == (d.nrows - 1) / ROWS_PER_WARP && lane < D / 8) {
+            // a2: the new token's k/v (already staged in smem) into cache row lens-1
+            const size_t dst = (((size_t)d.b * p.Hkv + d.h * p.Hkv / p.Hq) * p.max_ctx + d.wrow) * D;
+            reinterpret_cast<uint4 *>(p.k_w + dst)[lane] =
+                reinterpret_cast<const uint4 *>(st.k + (d.nrows - 1) * D)[lane];
+            reinterpret_cast<uint4 *>(p.v_w + dst)[lane] =
+                reinterpret_cast<const uint4 *>(st.v + (d.nrows - 1) * D)[lane];
+        }
         if (base < d.nrows) {
             // ---- scores: partial dots over this lane's 8 dims, NL rows
             float part[NL];
@@ -298,7 +304,8 @@ __global__ void __launch_bounds__(THREADS, 2) decode_attention_kernel(const Para
         }
 
         if (d.flags & F_LAST) {
-            // ---- merge the four warp states of this item
+            // ---- merge the four warp states of this item (double-buffered smem:
+            // a warp can start the next item while others still read this one)
             float lsum = l;
 #pragma unroll
             for (int o2 = 16; o2 > 0; o2 >>= 1) lsum += __shfl_xor_sync(FULL_MASK, lsum, o2);
@@ -309,26 +316,26 @@ __global__ void __launch_bounds__(THREADS, 2) decode_attention_kernel(const Para
                 for (int i = 0; i < 8; ++i) o[i] += __shfl_xor_sync(FULL_MASK, o[i], mk);
             if (lane < LPR) {
 #pragma unroll
-                for (int i = 0; i < 8; ++i) sm.red_o[warp][s * 8 + i] = o[i];
+                for (int i = 0; i < 8; ++i) sm.red_o[rb][warp][s * 8 + i] = o[i];
             }
             if (lane == 0) {
-                sm.red_m[warp] = m;
-                sm.red_l[warp] = lsum;
+                sm.red_m[rb][warp] = m;
+                sm.red_l[rb][warp] = lsum;
             }
             named_bar_sync(1, CWARPS * 32);
             const int t = threadIdx.x;
             float M = -INFINITY;
 #pragma unroll
-            for (int w2 = 0; w2 < CWARPS; ++w2) M = fmaxf(M, sm.red_m[w2]);
+            for (int w2 = 0; w2 < CWARPS; ++w2) M = fmaxf(M, sm.red_m[rb][w2]);
             const size_t bh = (size_t)d.b * p.Hq + d.h;
             if (t < D) {
                 float Lt = 0.f, Ot = 0.f;
 #pragma unroll
                 for (int w2 = 0; w2 < CWARPS; ++w2) {
-                    const float mw = sm.red_m[w2];
+                    const float mw = sm.red_m[rb][w2];
                     const float f = (mw == -INFINITY) ? 0.f : ex2(mw - M);
-                    Lt = fmaf(f, sm.red_l[w2], Lt);
-                    Ot = fmaf(f, sm.red_o[w2][t], Ot);
+                    Lt = fmaf(f, sm.red_l[rb][w2], Lt);
+                    Ot = fmaf(f, sm.red_o[rb][w2][t], Ot);
                 }
                 if (d.nchunks == 1) {
                     p.out[bh * D + t] = __float2bfloat16_rn(Lt > 0.f ? Ot / Lt : 0.f);
@@ -339,35 +346,45 @@ __global__ void __launch_bounds__(THREADS, 2) decode_attention_kernel(const Para
                         pp[D] = M;
                         pp[D + 1] = Lt;
                     }
-                    __threadfence();
                 }
             }
+            rb ^= 1;
             if (d.nchunks > 1) {
-                named_bar_sync(1, CWARPS * 32);
-                if (t == 0) {
-                    const int old = atomicAdd(&p.tickets[bh], 1);
-                    sm.last_flag = (old == d.nchunks - 1);
-                }
-                named_bar_sync(1, CWARPS * 32);
-                if (sm.last_flag) {
-                    __threadfence();
-                    if (t < D) {
+                // publish the partial: every thread arrives (release, non-blocking);
+                // warp 0 alone waits, then one gpu-scope acq_rel ticket.  The CTA that
+                // draws the last ticket merges the chunks in ascending chunk order.
+                mbar_arrive(&sm.part_bar);
+                if (warp == 0) {
+                    mbar_wait(&sm.part_bar, part_phase);
+                    part_phase ^= 1;
+                    int last = 0;
+                    if (lane == 0) last = atom_add_acq_rel_gpu(&p.tickets[bh], 1) == d.nchunks - 1;
+                    __syncwarp();
+                    last = __shfl_sync(FULL_MASK, last, 0);
+                    if (last) {
                         const float *pp = p.partial + bh * p.max_chunks * (D + 2);
                         float Mc = -INFINITY;
                         for (int c = 0; c < d.nchunks; ++c) Mc = fmaxf(Mc, __ldcg(pp + c * (D + 2) + D));
-                        float Lc = 0.f, Oc = 0.f;
+                        constexpr int NJ = (D + 31) / 32;
+                        float Lc = 0.f, Oc[NJ];
+#pragma unroll
+                        for (int j = 0; j < NJ; ++j) Oc[j] = 0.f;
                         for (int c = 0; c < d.nchunks; ++c) {
                             const float mc = __ldcg(pp + c * (D + 2) + D);
                             const float f = (mc == -INFINITY) ? 0.f : ex2(mc - Mc);
                             Lc = fmaf(f, __ldcg(pp + c * (D + 2) + D + 1), Lc);
-                            Oc = fmaf(f, __ldcg(pp + c * (D + 2) + t), Oc);
+#pragma unroll
+                            for (int j = 0; j < NJ; ++j)
+                                if (j * 32 + lane < D) Oc[j] = fmaf(f, __ldcg(pp + c * (D + 2) + j * 32 + lane), Oc[j]);
                         }
-                        p.out[bh * D + t] = __float2bfloat16_rn(Lc > 0.f ? Oc / Lc : 0.f);
+                        const float inv = Lc > 0.f ? 1.f / Lc : 0.f;
+#pragma unroll
+                        for (int j = 0; j < NJ; ++j)
+                            if (j * 32 + lane < D) p.out[bh * D + j * 32 + lane] = __float2bfloat16_rn(Oc[j] * inv);
+                        if (lane == 0) p.tickets[bh] = 0;
                     }
-                    if (t == 0) p.tickets[bh] = 0;
                 }
             }
-            named_bar_sync(1, CWARPS * 32);
         }
     }
 }
@@ -392,6 +409,11 @@ cudaError_t launch_d(const DecodeArgs &a, cudaStream_t s) {
     p.q = static_cast<const __nv_bfloat16 *>(a.q);
     p.k = static_cast<const __nv_bfloat16 *>(a.k);
     p.v = static_cast<const __nv_bfloat16 *>(a.v);
+    p.k_new = static_cast<const __nv_bfloat16 *>(a.k_new);
+    p.v_new = static_cast<const __nv_bfloat16 *>(a.v_new);
+    p.k_w = static_cast<__nv_bfloat16 *>(const_cast<void *>(a.k));
+    p.v_w = static_cast<__nv_bfloat16 *>(const_cast<void *>(a.v));
+    p.counters = a.counters;
     p.mask = a.mask;
     p.lens = a.lens;
     p.pad = a.pad;
@@ -413,10 +435,13 @@ cudaError_t launch_d(const DecodeArgs &a, cudaStream_t s) {
 size_t decode_partial_bytes(int slots, int q_heads, int head_dim, int max_ctx) {
     return (size_t)slots * q_heads * ceil_div(max_ctx, CHUNK) * (head_dim + 2) * sizeof(float);
 }
-size_t decode_ticket_bytes(int slots, int q_heads) { return (size_t)slots * q_heads * sizeof(int32_t); }
+size_t decode_ticket_bytes(int slots, int q_heads) {
+    return (size_t)slots * q_heads * sizeof(int32_t) + 2 * sizeof(int32_t);   // + work counters
+}
 bool decode_supported_head_dim(int d) { return d == 16 || d == 32 || d == 64 || d == 128; }
 
 cudaError_t launch_decode_attention(const DecodeArgs &a, cudaStream_t s) {
+    if (gqa_supported(a.q_heads, a.kv_heads, a.head_dim)) return launch_decode_gqa(a, s);
     switch (a.head_dim) {
         case 16: return launch_d<16>(a, s);
         case 32: return launch_d<32>(a, s);

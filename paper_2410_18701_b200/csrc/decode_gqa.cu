@@ -1,0 +1,455 @@
+// decode_gqa.cu -- a3 for grouped-query attention (configs[3]: 64 q heads / 8 kv
+// heads): the group of q heads that share a kv head forms a real dense tile, so
+// the dot products and the P.V product run on the tensor cores (mma.sync
+// m16n8k16 bf16 -> fp32), while K/V are still streamed from HBM exactly once.
+//
+//   work item = (slot b, kv head g, 256-key chunk c); GS = q_heads/kv_heads = 8
+//   producer warp: 32 lanes copy each 64-key K/V tile with 16-B cp.async into a
+//     128-B-swizzled shared layout (16-B chunk c of row r of half h at
+//     h*TILE*128 + r*128 + ((c ^ r) & 7)*16) so that every ldmatrix below is
+//     bank-conflict free; completion via cp.async.mbarrier.arrive.noinc.  Only
+//     rows [0, lens) are copied (placeholders are never read).
+//   consumer warps (16 keys each): S[16 x 16keys] = Q[16(8 real heads) x 128] K^T
+//     (16 MMAs), masked online softmax per head row (quad shuffles), P kept in
+//     registers as the A fragment of O[16 x 128] += P V (16 MMAs, V via
+//     ldmatrix.trans).
+//   epilogue: 4 warp states merged in smem; single chunk -> bf16 out, else split-K
+//     partials + last-CTA merge (same workspace layout as decode_attention.cu).
+#include "common.cuh"
+#include "kernels.h"
+#include "sched.cuh"
+
+namespace baton {
+namespace {
+
+constexpr int D = 128;
+constexpr int GS = 8;                       // q heads per kv head
+constexpr int CW = 4;                       // consumer warps
+constexpr int KPW = 16;                     // keys per warp per tile
+constexpr int TILE = CW * KPW;              // 64
+constexpr int STAGES = 4;
+constexpr int THREADS = (CW + 1) * 32;
+constexpr int HALF = TILE * 128;            // bytes of one 64-dim half of a tile (8 KB)
+constexpr int F_FIRST = 1, F_LAST = 2, F_END = 4, F_WRITE = 8;
+
+struct Desc {
+    int32_t b, g, c, nrows, flags, moff, nchunks, wrow;
+};
+
+struct __align__(128) Stage {
+    uint8_t k[2 * HALF];
+    uint8_t v[2 * HALF];
+    __nv_bfloat16 q[GS * D];
+    uint8_t mask[TILE + 16];
+    Desc desc;
+};
+
+struct Smem {
+    Stage st[STAGES];
+    uint64_t full[STAGES], empty[STAGES];
+    WorkSched ws;
+    float red_o[CW][GS][D];
+    float red_m[CW][GS], red_l[CW][GS];
+    int32_t last_flag;
+};
+
+struct Params {
+    const __nv_bfloat16 *q, *k, *v;
+    const __nv_bfloat16 *k_new, *v_new;      // fused append (nullable)
+    __nv_bfloat16 *k_w, *v_w;
+    int32_t *counters;
+    const uint8_t *mask;
+    const int32_t *lens, *pad;
+    __nv_bfloat16 *out;
+    float *partial;
+    int32_t *tickets;
+    int B, Hq, Hkv, max_ctx, max_chunks;
+    float scale_log2;
+};
+
+BATON_DEV uint32_t swz(int row, int chunk) {   // byte offset of 16-B chunk (0..15) of a row
+    return (uint32_t)((chunk >> 3) * HALF + row * 128 + (((chunk & 7) ^ (row & 7)) << 4));
+}
+BATON_DEV void cp_async16(uint32_t dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+BATON_DEV void cp_async_arrive_noinc(uint64_t *bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+BATON_DEV void ldsm_x4(uint32_t addr, uint32_t &r0, uint32_t &r1, uint32_t &r2, uint32_t &r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+BATON_DEV void ldsm_x4_t(uint32_t addr, uint32_t &r0, uint32_t &r1, uint32_t &r2, uint32_t &r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+BATON_DEV void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                        uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+BATON_DEV uint32_t pack_bf16(float lo, float hi) {
+    __nv_bfloat162 b = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t *>(&b);
+}
+
+__global__ void __launch_bounds__(THREADS, 1) decode_gqa_kernel(const Params p) {
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    Smem &sm = *reinterpret_cast<Smem *>(smem_raw);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            // 32 noinc arrivals (one per producer lane, fired when its cp.asyncs land)
+            // + 1 plain release-arrival by lane 0 after it wrote the descriptor
+            mbar_init(&sm.full[s], 33);
+            mbar_init(&sm.empty[s], CW);
+        }
+        fence_mbar_init();
+    }
+    for (int b = blockIdx.x; b < p.B; b += gridDim.x) {
+        if (p.lens[b] <= 0) {
+            uint4 *o = reinterpret_cast<uint4 *>(p.out + (size_t)b * p.Hq * D);
+            for (int i = threadIdx.x; i < p.Hq * D / 8; i += THREADS) o[i] = make_uint4(0, 0, 0, 0);
+        }
+    }
+    __syncthreads();
+
+    if (warp == CW) {
+        // ============================ producer warp ============================
+        sched_build(sm.ws, p.lens, p.pad, p.B, p.Hkv, lane);
+        const int total = sched_total(sm.ws, p.Hkv);
+        int stage = 0;
+        uint32_t phase = 0;
+        int b = 0;
+        int w = 0;
+        if (lane == 0) w = sched_next(p.counters);
+        w = __shfl_sync(FULL_MASK, w, 0);
+        while (w < total) {
+            int w_next = 0;
+            if (lane == 0) w_next = sched_next(p.counters);   // latency hidden by this item
+            int c, g;
+            sched_item(sm.ws, w, p.Hkv, b, c, g);
+            const int L = sm.ws.lens[b];
+            const int nch = (L + CHUNK - 1) / CHUNK;
+            const int r0 = c * CHUNK;
+            const int rows = min(CHUNK, L - r0);
+            const size_t head_off = ((size_t)(b * p.Hkv + g) * p.max_ctx + r0) * D;
+            const uint8_t *kb = reinterpret_cast<const uint8_t *>(p.k + head_off);
+            const uint8_t *vb = reinterpret_cast<const uint8_t *>(p.v + head_off);
+            const int ntiles = (rows + TILE - 1) / TILE;
+            const bool app = p.k_new != nullptr && c == nch - 1;   // fused append (a2)
+            for (int t = 0; t < ntiles; ++t) {
+                const int nr = min(TILE, rows - t * TILE);
+                const bool app_tile = app && t == ntiles - 1;
+                mbar_wait(&sm.empty[stage], phase ^ 1);
+                Stage &st = sm.st[stage];
+                const uint32_t ks = smem_u32(st.k), vs = smem_u32(st.v);
+                const uint8_t *kt = kb + (size_t)t * TILE * D * 2;
+                const uint8_t *vt = vb + (size_t)t * TILE * D * 2;
+                const uint8_t *kn = reinterpret_cast<const uint8_t *>(p.k_new + ((size_t)b * p.Hkv + g) * D);
+                const uint8_t *vn = reinterpret_cast<const uint8_t *>(p.v_new + ((size_t)b * p.Hkv + g) * D);
+                // 16 chunks per row; lane handles chunk (lane & 15) of rows (lane >> 4) + 2i
+                const int ch = lane & 15;
+                for (int r = lane >> 4; r < nr; r += 2) {
+                    const bool nw = app_tile && r == nr - 1;
+                    cp_async16(ks + swz(r, ch), (nw ? kn : kt + r * 256) + ch * 16);
+                    cp_async16(vs + swz(r, ch), (nw ? vn : vt + r * 256) + ch * 16);
+                }
+                if (t == 0) {   // the group's 8 query rows (contiguous 2 KB)
+                    const uint8_t *qs = reinterpret_cast<const uint8_t *>(p.q + ((size_t)b * p.Hq + g * GS) * D);
+                    for (int i = lane; i < GS * D / 8; i += 32) cp_async16(smem_u32(st.q) + i * 16, qs + i * 16);
+                }
+                int moff = 0;
+                if (p.mask) {
+                    const size_t row0 = (size_t)b * p.max_ctx;
+                    const size_t j0 = row0 + sm.ws.pad[b] + r0 + t * TILE;
+                    const size_t a0 = j0 & ~(size_t)15;
+                    size_t need = (j0 + nr - a0 + 15) & ~(size_t)15;
+                    if (a0 + need > row0 + p.max_ctx) need = row0 + p.max_ctx - a0;
+                    moff = (int)(j0 - a0);
+                    if (lane * 16 < (int)need) cp_async16(smem_u32(st.mask) + lane * 16, p.mask + a0 + lane * 16);
+                }
+                if (lane == 0) {
+                    st.desc.b = b;
+                    st.desc.g = g;
+                    st.desc.c = c;
+                    st.desc.nrows = nr;
+                    st.desc.flags = (t == 0 ? F_FIRST : 0) | (t == ntiles - 1 ? F_LAST : 0) |
+                                    (app_tile ? F_WRITE : 0);
+                    st.desc.moff = moff;
+                    st.desc.nchunks = nch;
+                    st.desc.wrow = L - 1;
+                }
+                __syncwarp();
+                cp_async_arrive_noinc(&sm.full[stage]);
+                if (lane == 0) mbar_arrive(&sm.full[stage]);
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            w = __shfl_sync(FULL_MASK, w_next, 0);
+        }
+        if (lane == 0) sched_done(p.counters);
+        mbar_wait(&sm.empty[stage], phase ^ 1);
+        if (lane == 0) sm.st[stage].desc.flags = F_END;
+        __syncwarp();
+        mbar_arrive(&sm.full[stage]);   // 32 + 1 plain arrivals complete the phase
+        if (lane == 0) mbar_arrive(&sm.full[stage]);
+        return;
+    }
+
+    // ============================ consumer warps ============================
+    const int qr = lane >> 2;            // fragment row (head) / B column
+    const int qc = (lane & 3) * 2;       // fragment column pair
+    uint32_t qa[8][2];                   // Q A-fragments (rows 0-7 real): a0 / a2 per k-step
+    float o[16][4];                      // O accumulator: 16 n-tiles of 8 dims (rows qr, qr+8)
+    float m = -INFINITY, l = 0.f;        // softmax state of head row qr
+    int stage = 0;
+    uint32_t phase = 0;
+    while (true) {
+        mbar_wait(&sm.full[stage], phase);
+        Stage &st = sm.st[stage];
+        const Desc d = st.desc;
+        if (d.flags & F_END) break;
+        if (d.flags & F_FIRST) {
+            const uint32_t *qw = reinterpret_cast<const uint32_t *>(st.q + qr * D);
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+                qa[ks][0] = qw[(ks * 16 + qc) / 2];
+                qa[ks][1] = qw[(ks * 16 + 8 + qc) / 2];
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+            m = -INFINITY;
+            l = 0.f;
+        }
+        const int base = warp * KPW;
+        if ((d.flags & F_WRITE) && warp == (d.nrows - 1) / KPW && lane < 16) {
+            // a2: the new token's k/v (staged in smem) into cache row lens-1
+            const size_t dst = (((size_t)d.b * p.Hkv + d.g) * p.max_ctx + d.wrow) * D;
+            reinterpret_cast<uint4 *>(p.k_w + dst)[lane] =
+                *reinterpret_cast<const uint4 *>(st.k + swz(d.nrows - 1, lane));
+            reinterpret_cast<uint4 *>(p.v_w + dst)[lane] =
+                *reinterpret_cast<const uint4 *>(st.v + swz(d.nrows - 1, lane));
+        }
+        if (base < d.nrows) {
+            const uint32_t ks_ = smem_u32(st.k), vs_ = smem_u32(st.v);
+            // ---- S = Q K^T for the warp's 16 keys (two n-tiles of 8 keys)
+            float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+            {
+                const int i = lane >> 3, r = lane & 7;
+                const int key = base + (i >> 1) * 8 + r;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    uint32_t b0, b1, b2, b3;
+                    ldsm_x4(ks_ + swz(key, 2 * kk + (i & 1)), b0, b1, b2, b3);
+                    mma16816(s[0], qa[kk][0], 0u, qa[kk][1], 0u, b0, b1);
+                    mma16816(s[1], qa[kk][0], 0u, qa[kk][1], 0u, b2, b3);
+                }
+            }
+            // ---- mask + online softmax on head row qr (values s[nt][0..1])
+            bool any_invalid = false;
+            float mx = -INFINITY;
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int kt = base + nt * 8 + qc + e;
+                    bool ok = kt < d.nrows;
+                    if (p.mask) ok = ok && st.mask[d.moff + (ok ? kt : 0)] != 0;
+                    any_invalid |= !ok;
+                    const float x = ok ? s[nt][e] * p.scale_log2 : -INFINITY;
+                    s[nt][e] = x;
+                    mx = fmaxf(mx, x);
+                }
+            mx = fmaxf(mx, __shfl_xor_sync(FULL_MASK, mx, 1));
+            mx = fmaxf(mx, __shfl_xor_sync(FULL_MASK, mx, 2));
+            const float m_new = fmaxf(m, mx);
+            const float ref = (m_new == -INFINITY) ? 0.f : m_new;
+            const float alpha = ex2(m - ref);
+            float pr[2][2];
+            float ps = 0.f;
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    // P.V multiplies bf16(p): sum the same rounded weights
+                    const float pe = __bfloat162float(__float2bfloat16_rn(ex2(s[nt][e] - ref)));
+                    pr[nt][e] = pe;
+                    ps += pe;
+                }
+            l = l * alpha + ps;
+            m = m_new;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                o[i][0] *= alpha;
+                o[i][1] *= alpha;
+            }
+            // masked / out-of-range keys: their V rows may hold anything -> zero them
+            if (__any_sync(FULL_MASK, any_invalid)) {
+                for (int kr = 0; kr < KPW; ++kr) {
+                    const int kt = base + kr;
+                    bool ok = kt < d.nrows;
+                    if (p.mask) ok = ok && st.mask[d.moff + (ok ? kt : 0)] != 0;
+                    if (!ok && lane < 16) *reinterpret_cast<uint4 *>(st.v + swz(kt, lane)) = make_uint4(0, 0, 0, 0);
+                }
+                __syncwarp();
+            }
+            const uint32_t pa0 = pack_bf16(pr[0][0], pr[0][1]);
+            const uint32_t pa2 = pack_bf16(pr[1][0], pr[1][1]);
+            // ---- O += P V : B fragments of V via ldmatrix.trans
+            {
+                const int i = lane >> 3, r = lane & 7;
+                const int key = base + (i & 1) * 8 + r;
+#pragma unroll
+                for (int dn = 0; dn < 8; ++dn) {
+                    uint32_t b0, b1, b2, b3;
+                    ldsm_x4_t(vs_ + swz(key, 2 * dn + (i >> 1)), b0, b1, b2, b3);
+                    mma16816(o[2 * dn], pa0, 0u, pa2, 0u, b0, b1);
+                    mma16816(o[2 * dn + 1], pa0, 0u, pa2, 0u, b2, b3);
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[stage]);
+        if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+        }
+
+        if (d.flags & F_LAST) {
+            float lsum = l;
+            lsum += __shfl_xor_sync(FULL_MASK, lsum, 1);
+            lsum += __shfl_xor_sync(FULL_MASK, lsum, 2);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                sm.red_o[warp][qr][i * 8 + qc] = o[i][0];
+                sm.red_o[warp][qr][i * 8 + qc + 1] = o[i][1];
+            }
+            if ((lane & 3) == 0) {
+                sm.red_m[warp][qr] = m;
+                sm.red_l[warp][qr] = lsum;
+            }
+            named_bar_sync(1, CW * 32);
+            const int t = threadIdx.x;          // 128 threads: head = t >> 4, dims 8*(t&15)..+8
+            const int hh = t >> 4, d0 = (t & 15) * 8;
+            float M = -INFINITY;
+#pragma unroll
+            for (int w2 = 0; w2 < CW; ++w2) M = fmaxf(M, sm.red_m[w2][hh]);
+            float Lt = 0.f, Ot[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int w2 = 0; w2 < CW; ++w2) {
+                const float mw = sm.red_m[w2][hh];
+                const float f = (mw == -INFINITY) ? 0.f : ex2(mw - M);
+                Lt = fmaf(f, sm.red_l[w2][hh], Lt);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) Ot[j] = fmaf(f, sm.red_o[w2][hh][d0 + j], Ot[j]);
+            }
+            const int h = d.g * GS + hh;
+            const size_t bh = (size_t)d.b * p.Hq + h;
+            if (d.nchunks == 1) {
+                const float inv = Lt > 0.f ? 1.f / Lt : 0.f;
+                uint4 w4;
+                w4.x = pack_bf16(Ot[0] * inv, Ot[1] * inv);
+                w4.y = pack_bf16(Ot[2] * inv, Ot[3] * inv);
+                w4.z = pack_bf16(Ot[4] * inv, Ot[5] * inv);
+                w4.w = pack_bf16(Ot[6] * inv, Ot[7] * inv);
+                *reinterpret_cast<uint4 *>(p.out + bh * D + d0) = w4;
+            } else {
+                float *pp = p.partial + (bh * p.max_chunks + d.c) * (D + 2);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) pp[d0 + j] = Ot[j];
+                if ((t & 15) == 0) {
+                    pp[D] = M;
+                    pp[D + 1] = Lt;
+                }
+                // bar.sync orders every thread's partial before thread 0's gpu-scope
+                // acq_rel ticket (cumulative release); no per-thread membar needed
+                named_bar_sync(1, CW * 32);
+                const size_t tk = (size_t)d.b * p.Hq + d.g * GS;   // one ticket per (b, g)
+                if (t == 0) {
+                    const int old = atom_add_acq_rel_gpu(&p.tickets[tk], 1);
+                    sm.last_flag = (old == d.nchunks - 1);
+                }
+                named_bar_sync(1, CW * 32);
+                if (sm.last_flag) {
+                    const float *pb = p.partial + bh * p.max_chunks * (D + 2);
+                    float Mc = -INFINITY;
+                    for (int c = 0; c < d.nchunks; ++c) Mc = fmaxf(Mc, __ldcg(pb + c * (D + 2) + D));
+                    float Lc = 0.f, Oc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                    for (int c = 0; c < d.nchunks; ++c) {
+                        const float mc = __ldcg(pb + c * (D + 2) + D);
+                        const float f = (mc == -INFINITY) ? 0.f : ex2(mc - Mc);
+                        Lc = fmaf(f, __ldcg(pb + c * (D + 2) + D + 1), Lc);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) Oc[j] = fmaf(f, __ldcg(pb + c * (D + 2) + d0 + j), Oc[j]);
+                    }
+                    const float inv = Lc > 0.f ? 1.f / Lc : 0.f;
+                    uint4 w4;
+                    w4.x = pack_bf16(Oc[0] * inv, Oc[1] * inv);
+                    w4.y = pack_bf16(Oc[2] * inv, Oc[3] * inv);
+                    w4.z = pack_bf16(Oc[4] * inv, Oc[5] * inv);
+                    w4.w = pack_bf16(Oc[6] * inv, Oc[7] * inv);
+                    *reinterpret_cast<uint4 *>(p.out + bh * D + d0) = w4;
+                    if (t == 0) p.tickets[tk] = 0;
+                }
+            }
+            named_bar_sync(1, CW * 32);
+        }
+    }
+}
+
+}  // namespace
+
+bool gqa_supported(int q_heads, int kv_heads, int head_dim) {
+    return head_dim == D && kv_heads > 0 && q_heads == GS * kv_heads;
+}
+
+cudaError_t launch_decode_gqa(const DecodeArgs &a, cudaStream_t s) {
+    static int num_sms = 0;
+    if (!num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const size_t smem = sizeof(Smem);
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(decode_gqa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    Params p;
+    p.q = static_cast<const __nv_bfloat16 *>(a.q);
+    p.k = static_cast<const __nv_bfloat16 *>(a.k);
+    p.v = static_cast<const __nv_bfloat16 *>(a.v);
+    p.k_new = static_cast<const __nv_bfloat16 *>(a.k_new);
+    p.v_new = static_cast<const __nv_bfloat16 *>(a.v_new);
+    p.k_w = static_cast<__nv_bfloat16 *>(const_cast<void *>(a.k));
+    p.v_w = static_cast<__nv_bfloat16 *>(const_cast<void *>(a.v));
+    p.counters = a.counters;
+    p.mask = a.mask;
+    p.lens = a.lens;
+    p.pad = a.pad;
+    p.out = static_cast<__nv_bfloat16 *>(a.out);
+    p.partial = a.partial;
+    p.tickets = a.tickets;
+    p.B = a.slots;
+    p.Hq = a.q_heads;
+    p.Hkv = a.kv_heads;
+    p.max_ctx = a.max_ctx;
+    p.max_chunks = a.max_chunks;
+    p.scale_log2 = a.scale * 1.4426950408889634f;
+    decode_gqa_kernel<<<num_sms, THREADS, smem, s>>>(p);
+    return cudaGetLastError();
+}
+
+}  // namespace baton

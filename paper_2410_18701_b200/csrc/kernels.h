@@ -17,11 +17,13 @@ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
 // ------------------------------------------------------------ decode attention
 struct DecodeArgs {
     const void *q, *k, *v;
+    const void *k_new = nullptr, *v_new = nullptr;   // fused append (a2) when non-null
+    int32_t *counters = nullptr;                      // 2 ints after the tickets
     const uint8_t *mask;            // nullable
     const int32_t *lens, *pad;
     void *out;
     float *partial;                 // [slots][q_heads][max_chunks][head_dim + 2]
-    int32_t *tickets;               // [slots][q_heads], zero between calls
+    int32_t *tickets;               // [slots][q_heads] (+2 work counters), zero between calls
     int slots, q_heads, kv_heads, head_dim, max_ctx, max_chunks;
     float scale;
 };
@@ -29,6 +31,9 @@ size_t decode_partial_bytes(int slots, int q_heads, int head_dim, int max_ctx);
 size_t decode_ticket_bytes(int slots, int q_heads);
 bool decode_supported_head_dim(int head_dim);
 cudaError_t launch_decode_attention(const DecodeArgs &a, cudaStream_t s);
+// GQA groups of 8 q heads per kv head (head_dim 128): tensor-core variant
+bool gqa_supported(int q_heads, int kv_heads, int head_dim);
+cudaError_t launch_decode_gqa(const DecodeArgs &a, cudaStream_t s);
 
 // ------------------------------------------------------------ metadata / mask
 cudaError_t launch_mask_update(uint8_t *mask, int32_t *S, int32_t *lens, int slots, int max_ctx,

@@ -260,7 +260,8 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
             if (j > 0) {
                 mbar_wait(&sm.o_done, (j - 1) & 1);   // PV_{j-1} done: O stable, P buffer free
                 tc_fence_after();
-                if (alpha != 1.f) {
+                // warp-uniform: tcgen05.ld/st are .sync.aligned (all 32 lanes converged)
+                if (__any_sync(FULL_MASK, alpha != 1.f)) {
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
                         uint32_t r[32];

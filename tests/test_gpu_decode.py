@@ -169,3 +169,44 @@ def test_invalid_arguments():
     with pytest.raises(BatonError):
         baton_decode_attention(st["q"], st["k"], st["v"], st["mask"], st["lens"], st["pad"],
                                st["q"].clone(), st["shape"], 0.25, st["ws"][:8])
+
+
+GQA_CASES = [
+    # tensor-core GQA path (8 q heads per kv head, head_dim 128)
+    (3, 8, 1, 128, 512, [1, 200, 512]),
+    (6, 16, 2, 128, 1024, [64, 65, 256, 257, 1000, 0]),
+    (4, 64, 8, 128, 4096, [4096, 2049, 300, 17]),
+]
+
+
+@pytest.mark.parametrize("case", range(len(GQA_CASES)))
+def test_gqa_matches_oracle(case):
+    require_cuda()
+    B, Hq, Hkv, D, S_cap, lens = GQA_CASES[case]
+    st = _state(200 + case, B, Hq, Hkv, D, S_cap, lens)
+    got = bits_to_f64(bf16_bits(_run(st)))
+    assert np.isfinite(got).all()
+    assert row_rel_err(got, _reference(st)) <= ATTN_RTOL
+
+
+def test_gqa_holes_and_peaky():
+    require_cuda()
+    st = _state(210, 5, 16, 2, 128, 2048, [1800, 3, 900, 257, 640], holes=0.25, scale_k=6.0)
+    got = bits_to_f64(bf16_bits(_run(st)))
+    assert np.isfinite(got).all()
+    assert row_rel_err(got, _reference(st)) <= ATTN_RTOL
+
+
+def test_gqa_batch_invariance_and_single_key():
+    require_cuda()
+    st1 = _state(211, 3, 16, 2, 128, 2048, [1500, 1, 600])
+    o1 = bf16_bits(_run(st1))
+    vb = bf16_bits(st1["v"])
+    for h in range(16):
+        assert np.array_equal(o1[1, h], vb[1, h // 8, 0])     # one live key: o = v exactly
+    st2 = _state(212, 4, 16, 2, 128, 2048, [20, 1500, 2048, 7])
+    for name in ("q", "k", "v"):
+        st2[name][1] = st1[name][0]
+    torch.cuda.synchronize()
+    o2 = bf16_bits(_run(st2))
+    assert np.array_equal(o1[0], o2[1])
