@@ -143,6 +143,7 @@ def window_plan(planner, n_iters, rank):
 
 # ------------------------------------------------------------------ the CUDA arm
 def run_baton(args, rank, world, local_rank):
+    import gc
     import torch
     import torch.distributed as dist
     from paper_2410_18701_b200.engine import Engine
@@ -157,15 +158,16 @@ def run_baton(args, rank, world, local_rank):
     K_steps, W = args.steps, args.warmup
     n_iters = W + K_steps
 
-    def make_engine(token_source, prefill_source):
+    def make_engine(token_source, prefill_source, use_graph):
         eng = Engine(wl, rank=rank, world=world, device=dev, group=group,
-                     token_source=token_source, prefill_source=prefill_source)
+                     token_source=token_source, prefill_source=prefill_source,
+                     use_graph=use_graph)
         fast_forward(eng.planner, args.t0)
         return eng
 
     # ---- warm start: materialise the t0 state through the ABI (insert every live
-    # query with its current history: S = max lens, pad = S - lens, exactly the
-    # state after the last release)
+    # query with its current keyed history: S = max lens, pad = S - lens, exactly
+    # the state after the last release)
     def warm_start(eng):
         pl = eng.planner
         slots, ks, vs, lens = [], [], [], []
@@ -184,7 +186,12 @@ def run_baton(args, rank, world, local_rank):
         eng.shard.baton_insert_many(slots, ks, vs, lens)
         torch.cuda.synchronize()
 
-    # ---- inputs for the window, resident in HBM before timing
+    def release(eng):
+        del eng
+        gc.collect()
+        torch.cuda.empty_cache()
+
+    # ---- inputs of the window, resident in HBM before any timing
     probe = Planner(wl, world)
     fast_forward(probe, args.t0)
     decodes, fresh = window_plan(probe, n_iters, rank)
@@ -209,9 +216,7 @@ def run_baton(args, rank, world, local_rank):
         baton_keygen_history(Vp, L, Hkv, D, q, 0, n, 2, wl.seed, wl.scales[2])
         pref[q] = (Kp, Vp)
     torch.cuda.synchronize()
-
     t_base = args.t0
-    state = {"i": 0}
 
     def token_dev(t, dec):
         i = t - t_base
@@ -220,65 +225,84 @@ def run_baton(args, rank, world, local_rank):
     def prefill_dev(qid, n):
         return pref[qid]
 
-    # ---------------------------------------------------------------- device-resident run
-    eng = make_engine(token_dev, prefill_dev)
+    def timed_window(eng, per_iter=None):
+        for _ in range(W):
+            eng.iteration()
+            if per_iter:
+                per_iter(eng, warm=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        st = []
+        for _ in range(K_steps):
+            st.append(eng.iteration())
+            if per_iter:
+                per_iter(eng, warm=False)
+        e1.record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        return e0.elapsed_time(e1), st
+
+    # ================= pass 1: `value` -- graph-replayed decode, inputs in HBM
+    eng = make_engine(token_dev, prefill_dev, use_graph=True)
     warm_start(eng)
-    # the window starts with the decode of iteration t0 (the planner was fast-forwarded)
-    stream = torch.cuda.current_stream()
-
-    # per-launch timing of the dominant kernel (decode attention) via events
-    attn_events = []
-    orig_layer = eng.shard.baton_decode_layer
-
-    def timed_layer(layer, q, out, k_new=None, v_new=None, stream=None):
-        eng.shard.baton_append_kv(layer, k_new, v_new)
-        if state.get("timing"):
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record()
-            eng.shard.baton_decode_attention(layer, q, out)
-            e1.record()
-            attn_events.append((e0, e1))
-        else:
-            eng.shard.baton_decode_attention(layer, q, out)
-        return out
-
-    eng.shard.baton_decode_layer = timed_layer
-
-    stats_w = [eng.iteration() for _ in range(W)]
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
     clocks = ClockSampler(local_rank)
     clocks.start()
-    time.sleep(0.5)          # let the sampler start before the timed region
-    state["timing"] = True
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
+    time.sleep(0.3)
     clocks.mark("t_start")
-    ev0.record()
-    stats = [eng.iteration() for _ in range(K_steps)]
-    ev1.record()
-    torch.cuda.synchronize()
+    ms, stats = timed_window(eng)
     clocks.mark("t_end")
-    state["timing"] = False
-    if world > 1:
-        dist.barrier()
     clk = clocks.stop()
-    ms = ev0.elapsed_time(ev1)
-    attn_ms = [a.elapsed_time(b) for a, b in attn_events]
+    release(eng)
 
     tokens = sum(s.decoded for s in stats)
-    live_rows = sum(s.live_rows for s in stats)   # per layer, summed over iterations
+    live_rows = sum(s.live_rows for s in stats)   # sum of lens over decoding slots
     splice_rows = sum(s.insert_rows + s.extract_rows + s.compact_rows for s in stats)
-    n_launch = sum(1 + 2 * L + (1 if s.removed or s.released else 0) + s.stored
-                   + (2 if s.stored else 0) + (2 if s.inserted else 0) for s in stats)
+    # our kernels per step: mask update + one fused append/attention per layer (+ the
+    # splice: remove/release, the batched KV copy + mask splice of inserts)
+    n_launch = sum(1 + L + (1 if (s.removed or s.released) else 0) + s.stored
+                   + (2 if s.inserted else 0) for s in stats)
     tau = 2 * Hkv * D * 2       # K+V bytes per token per layer
-    attn_bytes_total = L * (live_rows * tau + sum(s.decoded for s in stats) * Hq * D * 2 * 2)
-    attn_time_s = sum(attn_ms) / 1e3
-    attn_launches = len(attn_ms)
+    attn_bytes_total = L * (live_rows * tau + tokens * Hq * D * 2 * 2)
 
-    # ---------------------------------------------------------------- e2e run (host buffers)
+    # ================= pass 2: roofline -- same window, eager, events per attention launch
+    attn_ms = []
+    eng = make_engine(token_dev, prefill_dev, use_graph=False)
+    warm_start(eng)
+    sh = eng.shard
+    orig = sh.baton_decode_layer
+    timing = {"on": False}
+
+    def timed_layer(layer, q, out, k_new=None, v_new=None, stream=None):
+        if not timing["on"]:
+            return orig(layer, q, out, k_new, v_new)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        orig(layer, q, out, k_new, v_new)
+        b.record()
+        attn_ms.append((a, b))
+        return out
+
+    sh.baton_decode_layer = timed_layer
+    for _ in range(W):
+        eng.iteration()
+    torch.cuda.synchronize()
+    timing["on"] = True
+    for _ in range(K_steps):      # the same K iterations as pass 1 (deterministic window)
+        eng.iteration()
+    torch.cuda.synchronize()
+    attn = [a.elapsed_time(b) for a, b in attn_ms]
+    sh.baton_decode_layer = orig
+    del sh, orig, timed_layer
+    release(eng)
+    attn_time_s = sum(attn) / 1e3
+    attn_launches = len(attn)
+
+    # ================= pass 3: e2e -- host buffers, H2D/D2H inside the timed region
     e2e = None
     if not args.no_e2e:
         q_h = q_all.cpu().pin_memory()
@@ -287,6 +311,8 @@ def run_baton(args, rank, world, local_rank):
         pref_h = {q: (a.cpu().pin_memory(), b.cpu().pin_memory()) for q, (a, b) in pref.items()}
         del q_all, k_all, v_all
         pref.clear()
+        gc.collect()
+        torch.cuda.empty_cache()
         qd = torch.empty((L, B, Hq, D), dtype=torch.bfloat16, device=dev)
         kd = torch.empty((L, B, Hkv, D), dtype=torch.bfloat16, device=dev)
         vd = torch.empty_like(kd)
@@ -306,15 +332,19 @@ def run_baton(args, rank, world, local_rank):
             counters["h2d"] += (a.numel() + b.numel()) * 2
             return a.to(dev, non_blocking=True), b.to(dev, non_blocking=True)
 
-        del eng, timed_layer, orig_layer
-        import gc
-        gc.collect()
-        torch.cuda.empty_cache()
-        eng2 = make_engine(token_host, prefill_host)
-        warm_start(eng2)
+        def fetch_result(eng2, warm):
+            res_h.copy_(eng2.out[L - 1], non_blocking=True)   # the step's result to the host
+            if not warm:
+                counters["d2h"] += res_h.numel() * 2
+
+        eng = make_engine(token_host, prefill_host, use_graph=True)
+        warm_start(eng)
+        counters["h2d"] = 0
+        ms2, st2 = None, None
+        # warm-up iterations also move bytes; count only the timed ones
         for _ in range(W):
-            eng2.iteration()
-            res_h.copy_(eng2.out[L - 1], non_blocking=True)
+            eng.iteration()
+            fetch_result(eng, True)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -324,18 +354,16 @@ def run_baton(args, rank, world, local_rank):
         e0.record()
         st2 = []
         for _ in range(K_steps):
-            st2.append(eng2.iteration())
-            res_h.copy_(eng2.out[L - 1], non_blocking=True)   # the step's result to the host
-            counters["d2h"] += res_h.numel() * 2
+            st2.append(eng.iteration())
+            fetch_result(eng, False)
         e1.record()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         ms2 = e0.elapsed_time(e1)
-        tok2 = sum(s.decoded for s in st2)
-        e2e = {"ms": ms2, "tokens": tok2, "h2d": counters["h2d"] / K_steps,
+        e2e = {"ms": ms2, "tokens": sum(s.decoded for s in st2), "h2d": counters["h2d"] / K_steps,
                "d2h": counters["d2h"] / K_steps}
-        del eng2
+        release(eng)
 
     return dict(ms=ms, tokens=tokens, attn_bytes=attn_bytes_total, attn_time_s=attn_time_s,
                 attn_launches=attn_launches, splice_rows=splice_rows, tau=tau, L=L,

@@ -137,6 +137,18 @@ int  baton_decode_attention(const void *q, const void *k, const void *v, const u
 int  baton_decode_layer(baton_state *st, int layer, const void *q, const void *k_new,
                         const void *v_new, void *out, void *stream);
 
+/* One whole decode iteration of the shard: a1 (baton_mask_update), then for every
+ * layer l the fused a2+a3 (baton_decode_layer with k_new/v_new).
+ *   q, out     : device bf16 [layers][slots][q_heads][head_dim]
+ *   k_new,v_new: device bf16 [layers][slots][kv_heads][head_dim]
+ * The launch sequence is captured once into a CUDA graph (kernels chained by
+ * programmatic dependent launch) and replayed; it is re-captured only when one
+ * of the four pointers changes, so keep them fixed (staging buffers).  All
+ * kernels read the device copies of S/lens/pad, so the replay needs no host
+ * sync.  Errors: BATON_E_INVALID, BATON_E_CAPACITY (S+1 > max_ctx). */
+int  baton_decode_step(baton_state *st, const void *q, const void *k_new, const void *v_new,
+                       void *out, void *stream);
+
 /* ---------------------------------------------------------------- KV splice
  * a4 -- P:L105 "set all the values of the query^2 part of the current
  * attention_mask tensor to 0", then P:L123-124 resource releasing: the

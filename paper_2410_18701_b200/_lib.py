@@ -64,6 +64,7 @@ _SIGS = {
     "baton_decode_attention": (_I, [_P, _P, _P, _P, _P, _P, _P, ctypes.POINTER(baton_shape),
                                     ctypes.c_float, _P, ctypes.c_size_t, _P]),
     "baton_decode_layer": (_I, [_P, _I, _P, _P, _P, _P, _P]),
+    "baton_decode_step": (_I, [_P, _P, _P, _P, _P, _P]),
     "baton_remove": (_I, [_P, _I32P, _I, _I32P, _P]),
     "baton_insert": (_I, [_P, _I, _P, _P, _I, _P]),
     "baton_insert_many": (_I, [_P, _I, _I32P, ctypes.POINTER(_P), ctypes.POINTER(_P), _I32P, _P]),

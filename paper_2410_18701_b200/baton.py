@@ -150,6 +150,12 @@ class BatonShard:
                                      _stream(stream)), "baton_decode_layer")
         return out
 
+    def baton_decode_step(self, q, k_new, v_new, out, stream=None):
+        """Whole decode iteration (a1 + fused a2/a3 for every layer), graph-replayed."""
+        check(lib.baton_decode_step(self._h, _ptr(q), _ptr(k_new), _ptr(v_new), _ptr(out),
+                                    _stream(stream)), "baton_decode_step")
+        return out
+
     def baton_decode_attention(self, layer, q, out, scale=None, stream=None, use_mask=True):
         ws = baton_decode_workspace_bytes(self.shape)
         off = self.workspace.numel() - ws

@@ -28,6 +28,14 @@ struct baton_state {
     float *partial = nullptr;
     int max_chunks = 0;
     size_t layer_elems = 0;   // elements of one layer of the K (or V) cache
+    // baton_decode_step: the captured decode iteration, keyed by its I/O pointers
+    cudaStream_t cap_stream = nullptr;
+    cudaGraphExec_t step_exec = nullptr;
+    const void *step_io[4] = {nullptr, nullptr, nullptr, nullptr};
+    ~baton_state() {
+        if (step_exec) cudaGraphExecDestroy(step_exec);
+        if (cap_stream) cudaStreamDestroy(cap_stream);
+    }
 };
 
 namespace {
@@ -223,6 +231,56 @@ int baton_decode_layer(baton_state *st, int layer, const void *q, const void *k_
     // a2 fused into a3: one launch streams the cache and embeds the new token
     return cuda_status(launch_decode_attention(layer_args(st, layer, q, k_new, v_new, out),
                                                as_stream(stream)));
+}
+
+int baton_decode_step(baton_state *st, const void *q, const void *k_new, const void *v_new,
+                      void *out, void *stream) {
+    if (!st || !q || !k_new || !v_new || !out) return BATON_E_INVALID;
+    if (st->S + 1 > st->sh.max_ctx) return BATON_E_CAPACITY;
+    const baton_shape &s = st->sh;
+    const size_t qstride = (size_t)s.slots * s.q_heads * s.head_dim;
+    const size_t kstride = (size_t)s.slots * s.kv_heads * s.head_dim;
+    const void *io[4] = {q, k_new, v_new, out};
+    if (!st->step_exec || std::memcmp(io, st->step_io, sizeof(io)) != 0) {
+        // (re)capture: mask update + every layer's fused append/attention, chained
+        // with programmatic dependent launch; the graph reads only device state
+        if (st->step_exec) {
+            cudaGraphExecDestroy(st->step_exec);
+            st->step_exec = nullptr;
+        }
+        cudaError_t e = cudaSuccess;
+        if (!st->cap_stream) e = cudaStreamCreateWithFlags(&st->cap_stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) return cuda_status(e);
+        DecodeArgs probe = layer_args(st, 0, q, k_new, v_new, out);
+        probe.dry = true;   // kernel attributes must be set outside the capture
+        if ((e = launch_decode_attention(probe, st->cap_stream)) != cudaSuccess) return cuda_status(e);
+        if ((e = cudaStreamBeginCapture(st->cap_stream, cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
+            return cuda_status(e);
+        e = launch_mask_update(st->cfg.mask, st->d_S, st->d_lens, s.slots, s.max_ctx, st->cap_stream);
+        for (int l = 0; l < s.layers && e == cudaSuccess; ++l) {
+            const __nv_bfloat16 *ql = static_cast<const __nv_bfloat16 *>(q) + l * qstride;
+            const __nv_bfloat16 *kl = static_cast<const __nv_bfloat16 *>(k_new) + l * kstride;
+            const __nv_bfloat16 *vl = static_cast<const __nv_bfloat16 *>(v_new) + l * kstride;
+            __nv_bfloat16 *ol = static_cast<__nv_bfloat16 *>(out) + l * qstride;
+            e = launch_decode_attention(layer_args(st, l, ql, kl, vl, ol), st->cap_stream);
+        }
+        cudaGraph_t g = nullptr;
+        const cudaError_t e2 = cudaStreamEndCapture(st->cap_stream, &g);
+        if (e == cudaSuccess) e = e2;
+        if (e == cudaSuccess) e = cudaGraphInstantiate(&st->step_exec, g, 0);
+        if (g) cudaGraphDestroy(g);
+        if (e != cudaSuccess) {
+            st->step_exec = nullptr;
+            return cuda_status(e);
+        }
+        std::memcpy(st->step_io, io, sizeof(io));
+    }
+    int r = cuda_status(cudaGraphLaunch(st->step_exec, as_stream(stream)));
+    if (r) return r;
+    st->S += 1;   // host mirror of a1
+    for (int b = 0; b < s.slots; ++b)
+        if (st->occ[b]) st->lens[b] += 1;
+    return BATON_OK;
 }
 
 // ---------------------------------------------------------------- a4

@@ -5,6 +5,8 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
+#include <utility>
+
 #define BATON_DEV __device__ __forceinline__
 
 namespace baton {
@@ -88,6 +90,12 @@ BATON_DEV int atom_add_acq_rel_gpu(int32_t *p, int v) {
     return old;
 }
 
+// Programmatic dependent launch: a kernel launched with the PDL attribute may be
+// scheduled while its predecessor drains; it must wait before touching anything
+// the predecessor writes.  Both are no-ops without the attribute.
+BATON_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+BATON_DEV void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // named barrier among `nthreads` threads (ids >= 1; 0 is __syncthreads)
 BATON_DEV void named_bar_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -104,6 +112,25 @@ BATON_DEV uint4 ld_shared_v4(const void *p) {
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                  : "r"(smem_u32(p)));
     return r;
+}
+
+// Launch with programmatic stream serialization (PDL): the kernel may start while
+// its predecessor on the stream drains; it calls griddep_wait() before reading
+// the predecessor's results.  Also valid inside stream capture (graph edges).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t s, Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 }  // namespace baton

@@ -97,6 +97,10 @@ __global__ void __launch_bounds__(THREADS, 2) decode_attention_kernel(const Para
         mbar_init(&sm.part_bar, CWARPS * 32);
         fence_mbar_init();
     }
+    // PDL: everything above overlapped the previous kernel's tail; from here on we
+    // read lens/pad/mask/cache written by earlier kernels.
+    griddep_wait();
+    griddep_launch_dependents();
     // Empty slots produce a zero output row (C6).
     for (int b = blockIdx.x; b < p.B; b += gridDim.x) {
         if (p.lens[b] <= 0) {
@@ -405,6 +409,7 @@ cudaError_t launch_d(const DecodeArgs &a, cudaStream_t s) {
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
+    if (a.dry) return cudaSuccess;
     Params p;
     p.q = static_cast<const __nv_bfloat16 *>(a.q);
     p.k = static_cast<const __nv_bfloat16 *>(a.k);
@@ -426,8 +431,7 @@ cudaError_t launch_d(const DecodeArgs &a, cudaStream_t s) {
     p.max_ctx = a.max_ctx;
     p.max_chunks = a.max_chunks;
     p.scale_log2 = a.scale * 1.4426950408889634f;
-    decode_attention_kernel<D><<<2 * num_sms, THREADS, smem, s>>>(p);
-    return cudaGetLastError();
+    return launch_pdl(decode_attention_kernel<D>, dim3(2 * num_sms), dim3(THREADS), smem, s, p);
 }
 
 }  // namespace

@@ -113,6 +113,8 @@ __global__ void __launch_bounds__(THREADS, 1) decode_gqa_kernel(const Params p) 
         }
         fence_mbar_init();
     }
+    griddep_wait();                 // PDL (see decode_attention.cu)
+    griddep_launch_dependents();
     for (int b = blockIdx.x; b < p.B; b += gridDim.x) {
         if (p.lens[b] <= 0) {
             uint4 *o = reinterpret_cast<uint4 *>(p.out + (size_t)b * p.Hq * D);
@@ -427,6 +429,7 @@ cudaError_t launch_decode_gqa(const DecodeArgs &a, cudaStream_t s) {
         if (e != cudaSuccess) return e;
         attr = true;
     }
+    if (a.dry) return cudaSuccess;
     Params p;
     p.q = static_cast<const __nv_bfloat16 *>(a.q);
     p.k = static_cast<const __nv_bfloat16 *>(a.k);
@@ -448,8 +451,7 @@ cudaError_t launch_decode_gqa(const DecodeArgs &a, cudaStream_t s) {
     p.max_ctx = a.max_ctx;
     p.max_chunks = a.max_chunks;
     p.scale_log2 = a.scale * 1.4426950408889634f;
-    decode_gqa_kernel<<<num_sms, THREADS, smem, s>>>(p);
-    return cudaGetLastError();
+    return launch_pdl(decode_gqa_kernel, dim3(num_sms), dim3(THREADS), smem, s, p);
 }
 
 }  // namespace baton

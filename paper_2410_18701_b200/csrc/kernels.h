@@ -19,6 +19,7 @@ struct DecodeArgs {
     const void *q, *k, *v;
     const void *k_new = nullptr, *v_new = nullptr;   // fused append (a2) when non-null
     int32_t *counters = nullptr;                      // 2 ints after the tickets
+    bool dry = false;                                 // only set kernel attributes (pre-capture)
     const uint8_t *mask;            // nullable
     const int32_t *lens, *pad;
     void *out;

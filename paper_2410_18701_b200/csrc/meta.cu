@@ -16,6 +16,8 @@ namespace {
 // a1 -- P:L96 "add a column with the value of all 1" (0 for empty rows, C6)
 __global__ void mask_update_kernel(uint8_t *__restrict__ mask, int32_t *__restrict__ S,
                                    int32_t *__restrict__ lens, int slots, int max_ctx) {
+    griddep_wait();
+    griddep_launch_dependents();
     const int s_old = *S;
     for (int b = threadIdx.x; b < slots; b += blockDim.x) {
         const int L = lens[b];
@@ -129,8 +131,7 @@ __global__ void mask_move_kernel(const __grid_constant__ MaskMoveParams p) {
 
 cudaError_t launch_mask_update(uint8_t *mask, int32_t *S, int32_t *lens, int slots, int max_ctx,
                                cudaStream_t s) {
-    mask_update_kernel<<<1, 256, 0, s>>>(mask, S, lens, slots, max_ctx);
-    return cudaGetLastError();
+    return launch_pdl(mask_update_kernel, dim3(1), dim3(256), 0, s, mask, S, lens, slots, max_ctx);
 }
 
 cudaError_t launch_append_kv(void *k_layer, void *v_layer, const void *k_new, const void *v_new,

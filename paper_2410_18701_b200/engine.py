@@ -43,7 +43,7 @@ class StepStats:
 
 class Engine:
     def __init__(self, wl, rank=0, world=1, device=None, group=None, keep_outputs=False,
-                 keep_layers=None, token_source=None, prefill_source=None):
+                 keep_layers=None, token_source=None, prefill_source=None, use_graph=True):
         self.wl = wl
         self.rank = rank
         self.world = world
@@ -69,7 +69,7 @@ class Engine:
         self.outputs: Dict[Tuple[int, int], np.ndarray] = {}
         self.token_source = token_source
         self.prefill_source = prefill_source
-        self.flag_buf = None
+        self.use_graph = use_graph
         self.last_decisions = None
 
     # ---------------------------------------------------------------- inputs (harness)
@@ -118,9 +118,16 @@ class Engine:
         else:
             q, k, v = self._gen_tokens(dec)
         sh = self.shard
-        sh.baton_mask_update()
-        for l in range(self.wl.layers):
-            sh.baton_decode_layer(l, q[l], self.out[l], k[l], v[l])
+        if self.use_graph:
+            # one graph replay: mask update + every layer's fused append/attention
+            for src, dst in ((q, self.q), (k, self.k_new), (v, self.v_new)):
+                if src.data_ptr() != dst.data_ptr():
+                    dst.copy_(src, non_blocking=True)
+            sh.baton_decode_step(self.q, self.k_new, self.v_new, self.out)
+        else:
+            sh.baton_mask_update()
+            for l in range(self.wl.layers):
+                sh.baton_decode_layer(l, q[l], self.out[l], k[l], v[l])
         if self.keep_outputs and dec:
             layers = self.keep_layers if self.keep_layers is not None else range(self.wl.layers)
             o = self.out[list(layers)].float().cpu().numpy()

@@ -48,9 +48,9 @@ def _check_state(eng, sim):
         assert np.array_equal(bf16_bits(Vd), _f64_to_bf16_bits(Vo)), f"V slot {b}"
 
 
-def _replay(wl, check_every=1):
+def _replay(wl, check_every=1, use_graph=True):
     from paper_2410_18701_b200.engine import Engine
-    eng = Engine(wl, keep_outputs=True)
+    eng = Engine(wl, keep_outputs=True, use_graph=use_graph)
     sim = Simulator(wl, kv=True, keep_outputs=True, fill=np.nan)
     n = 0
     while True:
@@ -129,3 +129,23 @@ def test_extract_insert_round_trip_bitwise():
     sh.baton_insert(0, K2, V2, 300)
     Kd, Vd = sh.live_kv(0)
     assert torch.equal(Kd, K) and torch.equal(Vd, V)
+
+
+def test_graph_step_equals_eager_layers_bitwise():
+    """baton_decode_step (captured graph, PDL-chained) == per-layer eager launches."""
+    require_cuda()
+    from paper_2410_18701_b200.engine import Engine
+    wl = random_stream(17)
+    a = Engine(wl, keep_outputs=True, use_graph=True)
+    b = Engine(wl, keep_outputs=True, use_graph=False)
+    while not a.done():
+        a.iteration()
+        b.iteration()
+    assert b.done() and a.outputs.keys() == b.outputs.keys()
+    for k in a.outputs:
+        assert np.array_equal(a.outputs[k], b.outputs[k])
+
+
+def test_w1_replay_eager_layers():
+    require_cuda()
+    _replay(w1_workload(), use_graph=False)
