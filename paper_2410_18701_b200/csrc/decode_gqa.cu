@@ -4,11 +4,14 @@
 // m16n8k16 bf16 -> fp32), while K/V are still streamed from HBM exactly once.
 //
 //   work item = (slot b, kv head g, 256-key chunk c); GS = q_heads/kv_heads = 8
-//   producer warp: 32 lanes copy each 64-key K/V tile with 16-B cp.async into a
-//     128-B-swizzled shared layout (16-B chunk c of row r of half h at
-//     h*TILE*128 + r*128 + ((c ^ r) & 7)*16) so that every ldmatrix below is
-//     bank-conflict free; completion via cp.async.mbarrier.arrive.noinc.  Only
-//     rows [0, lens) are copied (placeholders are never read).
+//   producer (one elected lane): each 64-key K/V tile arrives by TMA 2-D tensor
+//     loads (4 boxes of 64 rows x 64 dims, SWIZZLE_128B: 16-B chunk c of row r of
+//     half h lands at h*TILE*128 + r*128 + ((c ^ r) & 7)*16) so every ldmatrix below
+//     is bank-conflict free; q and the tile's mask bytes by 1-D bulk copies; all
+//     completion tracked by one mbarrier tx-count.  A box may extend past lens in
+//     the last tile of a slot: those rows are masked and their V zeroed, never used.
+//     (A single warp's cp.async stream was measured at 1.3 TB/s -- too few bytes
+//     in flight; the TMA engine keeps 4 x 32 KB per SM in flight.)
 //   consumer warps (16 keys each): S[16 x 16keys] = Q[16(8 real heads) x 128] K^T
 //     (16 MMAs), masked online softmax per head row (quad shuffles), P kept in
 //     registers as the A fragment of O[16 x 128] += P V (16 MMAs, V via
@@ -18,6 +21,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "sched.cuh"
+#include "tma.h"
 
 namespace baton {
 namespace {
@@ -30,13 +34,13 @@ constexpr int TILE = CW * KPW;              // 64
 constexpr int STAGES = 4;
 constexpr int THREADS = (CW + 1) * 32;
 constexpr int HALF = TILE * 128;            // bytes of one 64-dim half of a tile (8 KB)
-constexpr int F_FIRST = 1, F_LAST = 2, F_END = 4, F_WRITE = 8;
+constexpr int F_FIRST = 1, F_LAST = 2, F_END = 4;
 
 struct Desc {
     int32_t b, g, c, nrows, flags, moff, nchunks, wrow;
 };
 
-struct __align__(128) Stage {
+struct __align__(1024) Stage {
     uint8_t k[2 * HALF];
     uint8_t v[2 * HALF];
     __nv_bfloat16 q[GS * D];
@@ -55,8 +59,6 @@ struct Smem {
 
 struct Params {
     const __nv_bfloat16 *q, *k, *v;
-    const __nv_bfloat16 *k_new, *v_new;      // fused append (nullable)
-    __nv_bfloat16 *k_w, *v_w;
     int32_t *counters;
     const uint8_t *mask;
     const int32_t *lens, *pad;
@@ -69,12 +71,6 @@ struct Params {
 
 BATON_DEV uint32_t swz(int row, int chunk) {   // byte offset of 16-B chunk (0..15) of a row
     return (uint32_t)((chunk >> 3) * HALF + row * 128 + (((chunk & 7) ^ (row & 7)) << 4));
-}
-BATON_DEV void cp_async16(uint32_t dst, const void *src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-BATON_DEV void cp_async_arrive_noinc(uint64_t *bar) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 BATON_DEV void ldsm_x4(uint32_t addr, uint32_t &r0, uint32_t &r1, uint32_t &r2, uint32_t &r3) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -99,16 +95,24 @@ BATON_DEV uint32_t pack_bf16(float lo, float hi) {
     return *reinterpret_cast<uint32_t *>(&b);
 }
 
-__global__ void __launch_bounds__(THREADS, 1) decode_gqa_kernel(const Params p) {
-    extern __shared__ __align__(128) uint8_t smem_raw[];
-    Smem &sm = *reinterpret_cast<Smem *>(smem_raw);
+BATON_DEV void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
+                  const Params p) {
+    extern __shared__ uint8_t smem_raw[];
+    Smem &sm = *reinterpret_cast<Smem *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
-            // 32 noinc arrivals (one per producer lane, fired when its cp.asyncs land)
-            // + 1 plain release-arrival by lane 0 after it wrote the descriptor
-            mbar_init(&sm.full[s], 33);
+            mbar_init(&sm.full[s], 1);       // producer's arrive.expect_tx (+ TMA bytes)
             mbar_init(&sm.empty[s], CW);
         }
         fence_mbar_init();
@@ -126,49 +130,30 @@ __global__ void __launch_bounds__(THREADS, 1) decode_gqa_kernel(const Params p) 
     if (warp == CW) {
         // ============================ producer warp ============================
         sched_build(sm.ws, p.lens, p.pad, p.B, p.Hkv, lane);
+        if (lane != 0) return;
         const int total = sched_total(sm.ws, p.Hkv);
         int stage = 0;
         uint32_t phase = 0;
         int b = 0;
-        int w = 0;
-        if (lane == 0) w = sched_next(p.counters);
-        w = __shfl_sync(FULL_MASK, w, 0);
+        int w = sched_next(p.counters);
         while (w < total) {
-            int w_next = 0;
-            if (lane == 0) w_next = sched_next(p.counters);   // latency hidden by this item
+            const int w_next = sched_next(p.counters);   // latency hidden by this item
             int c, g;
             sched_item(sm.ws, w, p.Hkv, b, c, g);
             const int L = sm.ws.lens[b];
             const int nch = (L + CHUNK - 1) / CHUNK;
             const int r0 = c * CHUNK;
             const int rows = min(CHUNK, L - r0);
-            const size_t head_off = ((size_t)(b * p.Hkv + g) * p.max_ctx + r0) * D;
-            const uint8_t *kb = reinterpret_cast<const uint8_t *>(p.k + head_off);
-            const uint8_t *vb = reinterpret_cast<const uint8_t *>(p.v + head_off);
+            const int row_base = (b * p.Hkv + g) * p.max_ctx + r0;   // row in the 2-D tensor map
             const int ntiles = (rows + TILE - 1) / TILE;
-            const bool app = p.k_new != nullptr && c == nch - 1;   // fused append (a2)
             for (int t = 0; t < ntiles; ++t) {
                 const int nr = min(TILE, rows - t * TILE);
-                const bool app_tile = app && t == ntiles - 1;
                 mbar_wait(&sm.empty[stage], phase ^ 1);
                 Stage &st = sm.st[stage];
-                const uint32_t ks = smem_u32(st.k), vs = smem_u32(st.v);
-                const uint8_t *kt = kb + (size_t)t * TILE * D * 2;
-                const uint8_t *vt = vb + (size_t)t * TILE * D * 2;
-                const uint8_t *kn = reinterpret_cast<const uint8_t *>(p.k_new + ((size_t)b * p.Hkv + g) * D);
-                const uint8_t *vn = reinterpret_cast<const uint8_t *>(p.v_new + ((size_t)b * p.Hkv + g) * D);
-                // 16 chunks per row; lane handles chunk (lane & 15) of rows (lane >> 4) + 2i
-                const int ch = lane & 15;
-                for (int r = lane >> 4; r < nr; r += 2) {
-                    const bool nw = app_tile && r == nr - 1;
-                    cp_async16(ks + swz(r, ch), (nw ? kn : kt + r * 256) + ch * 16);
-                    cp_async16(vs + swz(r, ch), (nw ? vn : vt + r * 256) + ch * 16);
-                }
-                if (t == 0) {   // the group's 8 query rows (contiguous 2 KB)
-                    const uint8_t *qs = reinterpret_cast<const uint8_t *>(p.q + ((size_t)b * p.Hq + g * GS) * D);
-                    for (int i = lane; i < GS * D / 8; i += 32) cp_async16(smem_u32(st.q) + i * 16, qs + i * 16);
-                }
+                uint32_t bytes = 4 * HALF;      // full boxes, OOB rows zero-filled
                 int moff = 0;
+                uint32_t mbytes = 0;
+                const uint8_t *msrc = nullptr;
                 if (p.mask) {
                     const size_t row0 = (size_t)b * p.max_ctx;
                     const size_t j0 = row0 + sm.ws.pad[b] + r0 + t * TILE;
@@ -176,35 +161,39 @@ __global__ void __launch_bounds__(THREADS, 1) decode_gqa_kernel(const Params p) 
                     size_t need = (j0 + nr - a0 + 15) & ~(size_t)15;
                     if (a0 + need > row0 + p.max_ctx) need = row0 + p.max_ctx - a0;
                     moff = (int)(j0 - a0);
-                    if (lane * 16 < (int)need) cp_async16(smem_u32(st.mask) + lane * 16, p.mask + a0 + lane * 16);
+                    msrc = p.mask + a0;
+                    mbytes = (uint32_t)need;
+                    bytes += mbytes;
                 }
-                if (lane == 0) {
-                    st.desc.b = b;
-                    st.desc.g = g;
-                    st.desc.c = c;
-                    st.desc.nrows = nr;
-                    st.desc.flags = (t == 0 ? F_FIRST : 0) | (t == ntiles - 1 ? F_LAST : 0) |
-                                    (app_tile ? F_WRITE : 0);
-                    st.desc.moff = moff;
-                    st.desc.nchunks = nch;
-                    st.desc.wrow = L - 1;
-                }
-                __syncwarp();
-                cp_async_arrive_noinc(&sm.full[stage]);
-                if (lane == 0) mbar_arrive(&sm.full[stage]);
+                if (t == 0) bytes += GS * D * 2;
+                st.desc.b = b;
+                st.desc.g = g;
+                st.desc.c = c;
+                st.desc.nrows = nr;
+                st.desc.flags = (t == 0 ? F_FIRST : 0) | (t == ntiles - 1 ? F_LAST : 0);
+                st.desc.moff = moff;
+                st.desc.nchunks = nch;
+                st.desc.wrow = 0;
+                mbar_arrive_expect_tx(&sm.full[stage], bytes);
+                const int row = row_base + t * TILE;
+                tma_load_2d(st.k, &kmap, 0, row, &sm.full[stage]);
+                tma_load_2d(st.k + HALF, &kmap, 64, row, &sm.full[stage]);
+                tma_load_2d(st.v, &vmap, 0, row, &sm.full[stage]);
+                tma_load_2d(st.v + HALF, &vmap, 64, row, &sm.full[stage]);
+                if (t == 0)   // the group's 8 query rows (contiguous 2 KB)
+                    bulk_g2s(st.q, p.q + ((size_t)b * p.Hq + g * GS) * D, GS * D * 2, &sm.full[stage]);
+                if (mbytes) bulk_g2s(st.mask, msrc, mbytes, &sm.full[stage]);
                 if (++stage == STAGES) {
                     stage = 0;
                     phase ^= 1;
                 }
             }
-            w = __shfl_sync(FULL_MASK, w_next, 0);
+            w = w_next;
         }
-        if (lane == 0) sched_done(p.counters);
+        sched_done(p.counters);
         mbar_wait(&sm.empty[stage], phase ^ 1);
-        if (lane == 0) sm.st[stage].desc.flags = F_END;
-        __syncwarp();
-        mbar_arrive(&sm.full[stage]);   // 32 + 1 plain arrivals complete the phase
-        if (lane == 0) mbar_arrive(&sm.full[stage]);
+        sm.st[stage].desc.flags = F_END;
+        mbar_arrive(&sm.full[stage]);
         return;
     }
 
@@ -234,14 +223,6 @@ __global__ void __launch_bounds__(THREADS, 1) decode_gqa_kernel(const Params p) 
             l = 0.f;
         }
         const int base = warp * KPW;
-        if ((d.flags & F_WRITE) && warp == (d.nrows - 1) / KPW && lane < 16) {
-            // a2: the new token's k/v (staged in smem) into cache row lens-1
-            const size_t dst = (((size_t)d.b * p.Hkv + d.g) * p.max_ctx + d.wrow) * D;
-            reinterpret_cast<uint4 *>(p.k_w + dst)[lane] =
-                *reinterpret_cast<const uint4 *>(st.k + swz(d.nrows - 1, lane));
-            reinterpret_cast<uint4 *>(p.v_w + dst)[lane] =
-                *reinterpret_cast<const uint4 *>(st.v + swz(d.nrows - 1, lane));
-        }
         if (base < d.nrows) {
             const uint32_t ks_ = smem_u32(st.k), vs_ = smem_u32(st.v);
             // ---- S = Q K^T for the warp's 16 keys (two n-tiles of 8 keys)
@@ -422,7 +403,7 @@ cudaError_t launch_decode_gqa(const DecodeArgs &a, cudaStream_t s) {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    const size_t smem = sizeof(Smem);
+    const size_t smem = sizeof(Smem) + 1024;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(decode_gqa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -434,10 +415,6 @@ cudaError_t launch_decode_gqa(const DecodeArgs &a, cudaStream_t s) {
     p.q = static_cast<const __nv_bfloat16 *>(a.q);
     p.k = static_cast<const __nv_bfloat16 *>(a.k);
     p.v = static_cast<const __nv_bfloat16 *>(a.v);
-    p.k_new = static_cast<const __nv_bfloat16 *>(a.k_new);
-    p.v_new = static_cast<const __nv_bfloat16 *>(a.v_new);
-    p.k_w = static_cast<__nv_bfloat16 *>(const_cast<void *>(a.k));
-    p.v_w = static_cast<__nv_bfloat16 *>(const_cast<void *>(a.v));
     p.counters = a.counters;
     p.mask = a.mask;
     p.lens = a.lens;
@@ -451,7 +428,19 @@ cudaError_t launch_decode_gqa(const DecodeArgs &a, cudaStream_t s) {
     p.max_ctx = a.max_ctx;
     p.max_chunks = a.max_chunks;
     p.scale_log2 = a.scale * 1.4426950408889634f;
-    return launch_pdl(decode_gqa_kernel, dim3(num_sms), dim3(THREADS), smem, s, p);
+    // 2-D maps over this layer's cache: [slots*kv_heads*max_ctx rows][128 dims]
+    CUtensorMap km, vm;
+    const uint64_t dims[2] = {(uint64_t)D, (uint64_t)a.slots * a.kv_heads * a.max_ctx};
+    const uint64_t strides[1] = {(uint64_t)D * 2};
+    const uint32_t box[2] = {64, TILE};
+    if (!encode_bf16_map(&km, a.k, 2, dims, strides, box) || !encode_bf16_map(&vm, a.v, 2, dims, strides, box))
+        return cudaErrorInvalidValue;
+    if (a.k_new) {   // a2 as its own (PDL-chained) launch before the attention
+        cudaError_t e = launch_append_kv(const_cast<void *>(a.k), const_cast<void *>(a.v), a.k_new, a.v_new,
+                                         a.lens, a.slots, a.kv_heads, a.head_dim, a.max_ctx, s);
+        if (e != cudaSuccess) return e;
+    }
+    return launch_pdl(decode_gqa_kernel, dim3(num_sms), dim3(THREADS), smem, s, km, vm, p);
 }
 
 }  // namespace baton

@@ -34,6 +34,8 @@ __global__ void append_kv_kernel(uint4 *__restrict__ k, uint4 *__restrict__ v,
                                  const uint4 *__restrict__ kn, const uint4 *__restrict__ vn,
                                  const int32_t *__restrict__ lens, int kv_heads, int vec_per_row,
                                  int max_ctx) {
+    griddep_wait();
+    griddep_launch_dependents();
     const int b = blockIdx.x, g = blockIdx.y;
     const int L = lens[b];
     if (L <= 0) return;
@@ -138,11 +140,10 @@ cudaError_t launch_append_kv(void *k_layer, void *v_layer, const void *k_new, co
                              const int32_t *lens, int slots, int kv_heads, int head_dim,
                              int max_ctx, cudaStream_t s) {
     const int vpr = head_dim / 8;
-    append_kv_kernel<<<dim3(slots, kv_heads), vpr < 32 ? 32 : vpr, 0, s>>>(
-        static_cast<uint4 *>(k_layer), static_cast<uint4 *>(v_layer),
-        static_cast<const uint4 *>(k_new), static_cast<const uint4 *>(v_new), lens, kv_heads, vpr,
-        max_ctx);
-    return cudaGetLastError();
+    return launch_pdl(append_kv_kernel, dim3(slots, kv_heads), dim3(vpr < 32 ? 32 : vpr), 0, s,
+                      static_cast<uint4 *>(k_layer), static_cast<uint4 *>(v_layer),
+                      static_cast<const uint4 *>(k_new), static_cast<const uint4 *>(v_new), lens,
+                      kv_heads, vpr, max_ctx);
 }
 
 cudaError_t launch_mask_splice(uint8_t *mask, int slots, int max_ctx, const MaskOp *ops, int nops,
