@@ -52,9 +52,8 @@ struct Smem {
     Stage st[STAGES];
     uint64_t full[STAGES], empty[STAGES];
     WorkSched ws;
-    float red_o[CW][GS][D];
-    float red_m[CW][GS], red_l[CW][GS];
-    int32_t last_flag;
+    float red_o[2][CW][GS][D + 8];     // +8: spread the 8 head rows over the banks
+    float red_m[2][CW][GS], red_l[2][CW][GS];
 };
 
 struct Params {
@@ -107,7 +106,9 @@ __global__ void __launch_bounds__(THREADS, 1)
 decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
                   const Params p) {
     extern __shared__ uint8_t smem_raw[];
-    Smem &sm = *reinterpret_cast<Smem *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-B alignment for the SWIZZLE_128B boxes; offsetting the __shared__ array
+    // itself keeps the shared address space visible to the compiler (LDS, not LD)
+    Smem &sm = *reinterpret_cast<Smem *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
@@ -205,6 +206,7 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
     float m = -INFINITY, l = 0.f;        // softmax state of head row qr
     int stage = 0;
     uint32_t phase = 0;
+    int rb = 0;                          // merge buffer of the current item
     while (true) {
         mbar_wait(&sm.full[stage], phase);
         Stage &st = sm.st[stage];
@@ -309,33 +311,43 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
         }
 
         if (d.flags & F_LAST) {
+            // ---- merge the 4 warp states (double-buffered smem: one barrier per item).
+            // Multi-chunk queries leave an fp32 partial; decode_combine_kernel (next in
+            // the stream, PDL) merges chunks in order -- no tickets, no waiting here.
             float lsum = l;
             lsum += __shfl_xor_sync(FULL_MASK, lsum, 1);
             lsum += __shfl_xor_sync(FULL_MASK, lsum, 2);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                sm.red_o[warp][qr][i * 8 + qc] = o[i][0];
-                sm.red_o[warp][qr][i * 8 + qc + 1] = o[i][1];
-            }
+            for (int i = 0; i < 16; ++i)
+                *reinterpret_cast<float2 *>(&sm.red_o[rb][warp][qr][i * 8 + qc]) = make_float2(o[i][0], o[i][1]);
             if ((lane & 3) == 0) {
-                sm.red_m[warp][qr] = m;
-                sm.red_l[warp][qr] = lsum;
+                sm.red_m[rb][warp][qr] = m;
+                sm.red_l[rb][warp][qr] = lsum;
             }
             named_bar_sync(1, CW * 32);
             const int t = threadIdx.x;          // 128 threads: head = t >> 4, dims 8*(t&15)..+8
             const int hh = t >> 4, d0 = (t & 15) * 8;
             float M = -INFINITY;
 #pragma unroll
-            for (int w2 = 0; w2 < CW; ++w2) M = fmaxf(M, sm.red_m[w2][hh]);
+            for (int w2 = 0; w2 < CW; ++w2) M = fmaxf(M, sm.red_m[rb][w2][hh]);
             float Lt = 0.f, Ot[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
             for (int w2 = 0; w2 < CW; ++w2) {
-                const float mw = sm.red_m[w2][hh];
+                const float mw = sm.red_m[rb][w2][hh];
                 const float f = (mw == -INFINITY) ? 0.f : ex2(mw - M);
-                Lt = fmaf(f, sm.red_l[w2][hh], Lt);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) Ot[j] = fmaf(f, sm.red_o[w2][hh][d0 + j], Ot[j]);
+                Lt = fmaf(f, sm.red_l[rb][w2][hh], Lt);
+                const float4 a4 = *reinterpret_cast<const float4 *>(&sm.red_o[rb][w2][hh][d0]);
+                const float4 b4 = *reinterpret_cast<const float4 *>(&sm.red_o[rb][w2][hh][d0 + 4]);
+                Ot[0] = fmaf(f, a4.x, Ot[0]);
+                Ot[1] = fmaf(f, a4.y, Ot[1]);
+                Ot[2] = fmaf(f, a4.z, Ot[2]);
+                Ot[3] = fmaf(f, a4.w, Ot[3]);
+                Ot[4] = fmaf(f, b4.x, Ot[4]);
+                Ot[5] = fmaf(f, b4.y, Ot[5]);
+                Ot[6] = fmaf(f, b4.z, Ot[6]);
+                Ot[7] = fmaf(f, b4.w, Ot[7]);
             }
+            rb ^= 1;
             const int h = d.g * GS + hh;
             const size_t bh = (size_t)d.b * p.Hq + h;
             if (d.nchunks == 1) {
@@ -348,46 +360,52 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
                 *reinterpret_cast<uint4 *>(p.out + bh * D + d0) = w4;
             } else {
                 float *pp = p.partial + (bh * p.max_chunks + d.c) * (D + 2);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) pp[d0 + j] = Ot[j];
+                *reinterpret_cast<float4 *>(pp + d0) = make_float4(Ot[0], Ot[1], Ot[2], Ot[3]);
+                *reinterpret_cast<float4 *>(pp + d0 + 4) = make_float4(Ot[4], Ot[5], Ot[6], Ot[7]);
                 if ((t & 15) == 0) {
                     pp[D] = M;
                     pp[D + 1] = Lt;
                 }
-                // bar.sync orders every thread's partial before thread 0's gpu-scope
-                // acq_rel ticket (cumulative release); no per-thread membar needed
-                named_bar_sync(1, CW * 32);
-                const size_t tk = (size_t)d.b * p.Hq + d.g * GS;   // one ticket per (b, g)
-                if (t == 0) {
-                    const int old = atom_add_acq_rel_gpu(&p.tickets[tk], 1);
-                    sm.last_flag = (old == d.nchunks - 1);
-                }
-                named_bar_sync(1, CW * 32);
-                if (sm.last_flag) {
-                    const float *pb = p.partial + bh * p.max_chunks * (D + 2);
-                    float Mc = -INFINITY;
-                    for (int c = 0; c < d.nchunks; ++c) Mc = fmaxf(Mc, __ldcg(pb + c * (D + 2) + D));
-                    float Lc = 0.f, Oc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-                    for (int c = 0; c < d.nchunks; ++c) {
-                        const float mc = __ldcg(pb + c * (D + 2) + D);
-                        const float f = (mc == -INFINITY) ? 0.f : ex2(mc - Mc);
-                        Lc = fmaf(f, __ldcg(pb + c * (D + 2) + D + 1), Lc);
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) Oc[j] = fmaf(f, __ldcg(pb + c * (D + 2) + d0 + j), Oc[j]);
-                    }
-                    const float inv = Lc > 0.f ? 1.f / Lc : 0.f;
-                    uint4 w4;
-                    w4.x = pack_bf16(Oc[0] * inv, Oc[1] * inv);
-                    w4.y = pack_bf16(Oc[2] * inv, Oc[3] * inv);
-                    w4.z = pack_bf16(Oc[4] * inv, Oc[5] * inv);
-                    w4.w = pack_bf16(Oc[6] * inv, Oc[7] * inv);
-                    *reinterpret_cast<uint4 *>(p.out + bh * D + d0) = w4;
-                    if (t == 0) p.tickets[tk] = 0;
-                }
             }
-            named_bar_sync(1, CW * 32);
         }
     }
+}
+
+// Split-K merge for multi-chunk queries: one warp per (slot, q head), chunks merged
+// in ascending order (batch-invariant).  Single-chunk queries were written directly.
+__global__ void __launch_bounds__(128) decode_combine_kernel(const int32_t *__restrict__ lens,
+                                                             const float *__restrict__ partial,
+                                                             __nv_bfloat16 *__restrict__ out, int B,
+                                                             int Hq, int max_chunks) {
+    griddep_wait();
+    griddep_launch_dependents();
+    const int pair = blockIdx.x * 4 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (pair >= B * Hq) return;
+    const int b = pair / Hq;
+    const int L = lens[b];
+    const int nch = (L + CHUNK - 1) / CHUNK;
+    if (nch <= 1) return;
+    const float *pp = partial + (size_t)pair * max_chunks * (D + 2);
+    float Mc = -INFINITY;
+    for (int c = 0; c < nch; ++c) Mc = fmaxf(Mc, pp[c * (D + 2) + D]);
+    float Lc = 0.f;
+    float4 Oc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c = 0; c < nch; ++c) {
+        const float mc = pp[c * (D + 2) + D];
+        const float f = (mc == -INFINITY) ? 0.f : ex2(mc - Mc);
+        Lc = fmaf(f, pp[c * (D + 2) + D + 1], Lc);
+        const float4 v = *reinterpret_cast<const float4 *>(pp + c * (D + 2) + lane * 4);
+        Oc.x = fmaf(f, v.x, Oc.x);
+        Oc.y = fmaf(f, v.y, Oc.y);
+        Oc.z = fmaf(f, v.z, Oc.z);
+        Oc.w = fmaf(f, v.w, Oc.w);
+    }
+    const float inv = Lc > 0.f ? 1.f / Lc : 0.f;
+    uint2 w;
+    w.x = pack_bf16(Oc.x * inv, Oc.y * inv);
+    w.y = pack_bf16(Oc.z * inv, Oc.w * inv);
+    *reinterpret_cast<uint2 *>(out + (size_t)pair * D + lane * 4) = w;
 }
 
 }  // namespace
@@ -440,7 +458,12 @@ cudaError_t launch_decode_gqa(const DecodeArgs &a, cudaStream_t s) {
                                          a.lens, a.slots, a.kv_heads, a.head_dim, a.max_ctx, s);
         if (e != cudaSuccess) return e;
     }
-    return launch_pdl(decode_gqa_kernel, dim3(num_sms), dim3(THREADS), smem, s, km, vm, p);
+    cudaError_t e = launch_pdl(decode_gqa_kernel, dim3(num_sms), dim3(THREADS), smem, s, km, vm, p);
+    if (e != cudaSuccess) return e;
+    const int pairs = a.slots * a.q_heads;
+    return launch_pdl(decode_combine_kernel, dim3((pairs + 3) / 4), dim3(128), 0, s, a.lens,
+                      (const float *)a.partial, static_cast<__nv_bfloat16 *>(a.out), a.slots,
+                      a.q_heads, a.max_chunks);
 }
 
 }  // namespace baton

@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1)
 prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                          const __grid_constant__ CUtensorMap tm_v, const PfParams p) {
     extern __shared__ uint8_t smem_raw[];
-    PfSmem &sm = *reinterpret_cast<PfSmem *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    PfSmem &sm = *reinterpret_cast<PfSmem *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // heavy tiles (near the diagonal end) first
     const int mt = p.n_mtiles - 1 - (int)(blockIdx.x % p.n_mtiles);

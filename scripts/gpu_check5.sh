@@ -1,0 +1,7 @@
+set -x
+cd $GRAFT_REPO_ROOT
+timeout 600 python -m pytest tests/test_gpu_decode.py -x -q --timeout 300 > gpurun_out/pytest_c.log 2>&1; echo "exit $?" >> gpurun_out/pytest_c.log
+python scripts/profile_decode.py --iters 20 --config 70b > gpurun_out/prof_decode.log 2>&1
+python scripts/profile_decode.py --iters 20 >> gpurun_out/prof_decode.log 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:decode_gqa -s 2 -c 1 -o gpurun_out/gqa_v3 -f python scripts/profile_decode.py --iters 2 --layers 2 --config 70b > gpurun_out/ncu_gqa.log 2>&1
+timeout 1200 python -m pytest tests -m gpu -q --timeout 300 > gpurun_out/pytest_gpu.log 2>&1; echo "exit $?" >> gpurun_out/pytest_gpu.log
