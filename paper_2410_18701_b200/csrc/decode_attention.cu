@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(THREADS, 2) decode_attention_kernel(const Para
                 if (d.nchunks == 1) {
                     p.out[bh * D + t] = __float2bfloat16_rn(Lt > 0.f ? Ot / Lt : 0.f);
                 } else {
-                    float *pp = p.partial + (bh * p.max_chunks + d.c) * (D + 2);
+                    float *pp = p.partial + (bh * p.max_chunks + d.c) * (D + PREC_PAD);
                     pp[t] = Ot;
                     if (t == 0) {
                         pp[D] = M;
@@ -366,20 +366,20 @@ __global__ void __launch_bounds__(THREADS, 2) decode_attention_kernel(const Para
                     __syncwarp();
                     last = __shfl_sync(FULL_MASK, last, 0);
                     if (last) {
-                        const float *pp = p.partial + bh * p.max_chunks * (D + 2);
+                        const float *pp = p.partial + bh * p.max_chunks * (D + PREC_PAD);
                         float Mc = -INFINITY;
-                        for (int c = 0; c < d.nchunks; ++c) Mc = fmaxf(Mc, __ldcg(pp + c * (D + 2) + D));
+                        for (int c = 0; c < d.nchunks; ++c) Mc = fmaxf(Mc, __ldcg(pp + c * (D + PREC_PAD) + D));
                         constexpr int NJ = (D + 31) / 32;
                         float Lc = 0.f, Oc[NJ];
 #pragma unroll
                         for (int j = 0; j < NJ; ++j) Oc[j] = 0.f;
                         for (int c = 0; c < d.nchunks; ++c) {
-                            const float mc = __ldcg(pp + c * (D + 2) + D);
+                            const float mc = __ldcg(pp + c * (D + PREC_PAD) + D);
                             const float f = (mc == -INFINITY) ? 0.f : ex2(mc - Mc);
-                            Lc = fmaf(f, __ldcg(pp + c * (D + 2) + D + 1), Lc);
+                            Lc = fmaf(f, __ldcg(pp + c * (D + PREC_PAD) + D + 1), Lc);
 #pragma unroll
                             for (int j = 0; j < NJ; ++j)
-                                if (j * 32 + lane < D) Oc[j] = fmaf(f, __ldcg(pp + c * (D + 2) + j * 32 + lane), Oc[j]);
+                                if (j * 32 + lane < D) Oc[j] = fmaf(f, __ldcg(pp + c * (D + PREC_PAD) + j * 32 + lane), Oc[j]);
                         }
                         const float inv = Lc > 0.f ? 1.f / Lc : 0.f;
 #pragma unroll
@@ -437,7 +437,7 @@ cudaError_t launch_d(const DecodeArgs &a, cudaStream_t s) {
 }  // namespace
 
 size_t decode_partial_bytes(int slots, int q_heads, int head_dim, int max_ctx) {
-    return (size_t)slots * q_heads * ceil_div(max_ctx, CHUNK) * (head_dim + 2) * sizeof(float);
+    return (size_t)slots * q_heads * ceil_div(max_ctx, CHUNK) * (head_dim + PREC_PAD) * sizeof(float);
 }
 size_t decode_ticket_bytes(int slots, int q_heads) {
     return (size_t)slots * q_heads * sizeof(int32_t) + 2 * sizeof(int32_t);   // + work counters

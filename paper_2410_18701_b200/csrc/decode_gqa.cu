@@ -52,7 +52,7 @@ struct Smem {
     Stage st[STAGES];
     uint64_t full[STAGES], empty[STAGES];
     WorkSched ws;
-    float red_o[2][CW][GS][D + 8];     // +8: spread the 8 head rows over the banks
+    alignas(16) float red_o[2][CW][GS][D + 8];     // +8: spread the 8 head rows over the banks
     float red_m[2][CW][GS], red_l[2][CW][GS];
 };
 
@@ -359,7 +359,7 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
                 w4.w = pack_bf16(Ot[6] * inv, Ot[7] * inv);
                 *reinterpret_cast<uint4 *>(p.out + bh * D + d0) = w4;
             } else {
-                float *pp = p.partial + (bh * p.max_chunks + d.c) * (D + 2);
+                float *pp = p.partial + (bh * p.max_chunks + d.c) * (D + PREC_PAD);
                 *reinterpret_cast<float4 *>(pp + d0) = make_float4(Ot[0], Ot[1], Ot[2], Ot[3]);
                 *reinterpret_cast<float4 *>(pp + d0 + 4) = make_float4(Ot[4], Ot[5], Ot[6], Ot[7]);
                 if ((t & 15) == 0) {
@@ -386,16 +386,16 @@ __global__ void __launch_bounds__(128) decode_combine_kernel(const int32_t *__re
     const int L = lens[b];
     const int nch = (L + CHUNK - 1) / CHUNK;
     if (nch <= 1) return;
-    const float *pp = partial + (size_t)pair * max_chunks * (D + 2);
+    const float *pp = partial + (size_t)pair * max_chunks * (D + PREC_PAD);
     float Mc = -INFINITY;
-    for (int c = 0; c < nch; ++c) Mc = fmaxf(Mc, pp[c * (D + 2) + D]);
+    for (int c = 0; c < nch; ++c) Mc = fmaxf(Mc, pp[c * (D + PREC_PAD) + D]);
     float Lc = 0.f;
     float4 Oc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int c = 0; c < nch; ++c) {
-        const float mc = pp[c * (D + 2) + D];
+        const float mc = pp[c * (D + PREC_PAD) + D];
         const float f = (mc == -INFINITY) ? 0.f : ex2(mc - Mc);
-        Lc = fmaf(f, pp[c * (D + 2) + D + 1], Lc);
-        const float4 v = *reinterpret_cast<const float4 *>(pp + c * (D + 2) + lane * 4);
+        Lc = fmaf(f, pp[c * (D + PREC_PAD) + D + 1], Lc);
+        const float4 v = *reinterpret_cast<const float4 *>(pp + c * (D + PREC_PAD) + lane * 4);
         Oc.x = fmaf(f, v.x, Oc.x);
         Oc.y = fmaf(f, v.y, Oc.y);
         Oc.z = fmaf(f, v.z, Oc.z);

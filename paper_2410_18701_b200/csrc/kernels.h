@@ -11,6 +11,8 @@ constexpr int CHUNK = 256;      // split-K chunk (keys), == BATON_CHUNK
 constexpr int MAX_SLOTS = 256;  // per-shard slot limit (kernel-parameter and smem arrays)
 constexpr int MAX_SPLICE_JOBS = 64;
 constexpr int MAX_MASK_OPS = 2 * MAX_SLOTS + 2;
+// split-K partial record: o[D], m, l, 2 pad floats -> 16-B aligned records (float4 I/O)
+constexpr int PREC_PAD = 4;
 
 inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
@@ -23,7 +25,7 @@ struct DecodeArgs {
     const uint8_t *mask;            // nullable
     const int32_t *lens, *pad;
     void *out;
-    float *partial;                 // [slots][q_heads][max_chunks][head_dim + 2]
+    float *partial;                 // [slots][q_heads][max_chunks][head_dim + PREC_PAD]: o, m, l, pad
     int32_t *tickets;               // [slots][q_heads] (+2 work counters), zero between calls
     int slots, q_heads, kv_heads, head_dim, max_ctx, max_chunks;
     float scale;

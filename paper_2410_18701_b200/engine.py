@@ -43,7 +43,8 @@ class StepStats:
 
 class Engine:
     def __init__(self, wl, rank=0, world=1, device=None, group=None, keep_outputs=False,
-                 keep_layers=None, token_source=None, prefill_source=None, use_graph=True):
+                 keep_layers=None, token_source=None, prefill_source=None, use_graph=True,
+                 stash_host=False):
         self.wl = wl
         self.rank = rank
         self.world = world
@@ -70,6 +71,9 @@ class Engine:
         self.token_source = token_source
         self.prefill_source = prefill_source
         self.use_graph = use_graph
+        # P:L147 "moved to the host memory": stored K/V in pinned host memory (the
+        # extract/insert copy kernels read/write it over PCIe), else an HBM stash
+        self.stash_host = stash_host
         self.last_decisions = None
 
     # ---------------------------------------------------------------- inputs (harness)
@@ -158,7 +162,13 @@ class Engine:
         vic = [(pl.local(g), q, n) for g, q, n in d.victims if pl.rank_of(g) == self.rank]
         if vic:
             for b, q, n in vic:
-                self.stash[q] = sh.baton_extract(b)
+                if self.stash_host:
+                    shape = (self.wl.layers, self.wl.kv_heads, n, self.wl.head_dim)
+                    ko = torch.empty(shape, dtype=torch.bfloat16, pin_memory=True)
+                    vo = torch.empty(shape, dtype=torch.bfloat16, pin_memory=True)
+                    self.stash[q] = sh.baton_extract(b, ko, vo)
+                else:
+                    self.stash[q] = sh.baton_extract(b)
                 stats.extract_rows += n
             stats.released += sh.baton_remove([b for b, _, _ in vic])
             stats.stored = len(vic)

@@ -1,0 +1,54 @@
+"""Measure a8 (baton_prefill_attention, tcgen05) on the configs' prompt shapes.
+
+    python scripts/bench_prefill.py [--iters N]
+
+Prints one JSON line per shape: causal FLOPs (4*H*D*sum_i (i+1), the algorithmic
+work of the masked product), CUDA-event time per launch and TFLOP/s as a fraction
+of the measured dense bf16 peak (MEASURED_PEAKS.json bf16_tflops, burst)."""
+import argparse
+import json
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2410_18701_b200.baton import baton_prefill_attention  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--iters", type=int, default=20)
+    args = ap.parse_args()
+    peak = 1657.7
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        peak = json.load(open(p))["bf16_tflops"]
+    shapes = [("7b", 32, 32, 512), ("7b", 32, 32, 1024), ("7b", 32, 32, 1800),
+              ("13b", 40, 40, 1024), ("70b", 64, 8, 3400)]
+    for name, Hq, Hkv, n in shapes:
+        D = 128
+        q = torch.randn((Hq, n, D), device="cuda").to(torch.bfloat16)
+        k = torch.randn((Hkv, n, D), device="cuda").to(torch.bfloat16)
+        v = torch.randn((Hkv, n, D), device="cuda").to(torch.bfloat16)
+        o = torch.empty_like(q)
+        for _ in range(3):
+            baton_prefill_attention(q, k, v, o, n, Hq, Hkv, D)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.iters):
+            baton_prefill_attention(q, k, v, o, n, Hq, Hkv, D)
+        e1.record()
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / args.iters
+        flops = 4.0 * Hq * D * (n * (n + 1) / 2)
+        tf = flops / us / 1e6
+        print(json.dumps({"shape": name, "q_heads": Hq, "kv_heads": Hkv, "len": n, "us": us,
+                          "causal_flop": flops, "tflops": tf, "peak_tflops": peak,
+                          "frac": tf / peak}))
+
+
+if __name__ == "__main__":
+    main()

@@ -149,3 +149,44 @@ def test_graph_step_equals_eager_layers_bitwise():
 def test_w1_replay_eager_layers():
     require_cuda()
     _replay(w1_workload(), use_graph=False)
+
+
+@pytest.mark.parametrize("seed", [3, 11])
+def test_random_stream_replay_host_stash(seed):
+    """Preempted queries stored in pinned HOST memory and re-inserted from
+    there: still bit-exact state and parity."""
+    require_cuda()
+    from paper_2410_18701_b200.engine import Engine
+    wl = random_stream(seed)
+    eng = Engine(wl, keep_outputs=True, stash_host=True)
+    sim = Simulator(wl, kv=True, keep_outputs=True, fill=np.nan)
+    stored = 0
+    while True:
+        rec = sim.iteration()
+        eng.iteration()
+        torch.cuda.synchronize()
+        stored += len(rec.preempted)
+        _check_state(eng, sim)
+        if sim.done():
+            break
+    assert stored > 0
+    for k, o in sim.outputs.items():
+        assert row_rel_err(eng.outputs[k], o) <= ATTN_RTOL
+
+
+def test_extract_to_pinned_host_and_back():
+    require_cuda()
+    from paper_2410_18701_b200.baton import BatonShard
+    sh = BatonShard(2, 3, 4, 4, 64, 256)
+    K = torch.randn((2, 4, 100, 64), device="cuda").to(torch.bfloat16)
+    V = torch.randn((2, 4, 100, 64), device="cuda").to(torch.bfloat16)
+    sh.baton_insert(1, K, V, 100)
+    kh = torch.empty((2, 4, 100, 64), dtype=torch.bfloat16, pin_memory=True)
+    vh = torch.empty_like(kh).pin_memory()
+    sh.baton_extract(1, kh, vh)
+    torch.cuda.synchronize()
+    assert torch.equal(kh, K.cpu()) and torch.equal(vh, V.cpu())
+    sh.baton_remove([1])
+    sh.baton_insert(2, kh, vh, 100)
+    Kd, Vd = sh.live_kv(2)
+    assert torch.equal(Kd, K) and torch.equal(Vd, V)
