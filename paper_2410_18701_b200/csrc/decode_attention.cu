@@ -22,6 +22,8 @@
 //     query writes its bf16 output directly, otherwise the chunk partial
 //     (m, l, o[D]) goes to the workspace and the LAST CTA to finish a
 //     (b, h) (atomic ticket) merges the chunk partials in ascending chunk order.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "sched.cuh"
@@ -29,11 +31,9 @@
 namespace baton {
 namespace {
 
-constexpr int CWARPS = 4;                 // consumer warps
 constexpr int ROWS_PER_WARP = 16;
-constexpr int TILE = CWARPS * ROWS_PER_WARP;   // 64 keys per stage
-constexpr int STAGES = 3;
-constexpr int THREADS = (CWARPS + 1) * 32;
+// Default variant: 4 consumer warps (64-key tiles), 3-stage ring, 2 CTAs per SM.
+// (CWARPS, STAGES, CTAs/SM) are template parameters so variants can be swept.
 
 constexpr int F_FIRST = 1, F_LAST = 2, F_END = 4, F_WRITE = 8;
 
@@ -43,7 +43,7 @@ struct StageDesc {
     int32_t b, h, c, nrows, flags, moff, nchunks, wrow;
 };
 
-template <int D>
+template <int D, int TILE>
 struct __align__(16) Stage {
     __nv_bfloat16 k[TILE * D];
     __nv_bfloat16 v[TILE * D];
@@ -66,9 +66,9 @@ struct Params {
     float scale_log2;
 };
 
-template <int D>
+template <int D, int CWARPS, int STAGES>
 struct Smem {
-    Stage<D> st[STAGES];
+    Stage<D, CWARPS * ROWS_PER_WARP> st[STAGES];
     uint64_t full[STAGES], empty[STAGES];
     WorkSched ws;
     float red_o[2][CWARPS][D];
@@ -76,15 +76,17 @@ struct Smem {
     uint64_t part_bar;
 };
 
-template <int D>
-__global__ void __launch_bounds__(THREADS, 2) decode_attention_kernel(const Params p) {
+template <int D, int CWARPS, int STAGES, int MINB>
+__global__ void __launch_bounds__((CWARPS + 1) * 32, MINB) decode_attention_kernel(const Params p) {
+    constexpr int TILE = CWARPS * ROWS_PER_WARP;
+    constexpr int THREADS = (CWARPS + 1) * 32;
     constexpr int LPR = D / 8;                 // lanes per key row (16 B of bf16 per lane)
     constexpr int RPL = 32 / LPR;              // rows per warp-wide load
     constexpr int NL = ROWS_PER_WARP / RPL;    // loads per lane per tile
     static_assert(NL * 2 == LPR || (LPR == 2 && NL == 1), "row mapping");
 
     extern __shared__ __align__(128) uint8_t smem_raw[];
-    Smem<D> &sm = *reinterpret_cast<Smem<D> *>(smem_raw);
+    Smem<D, CWARPS, STAGES> &sm = *reinterpret_cast<Smem<D, CWARPS, STAGES> *>(smem_raw);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -140,7 +142,7 @@ __global__ void __launch_bounds__(THREADS, 2) decode_attention_kernel(const Para
                 const int nr = min(TILE, rows - t * TILE);
                 const bool app_tile = app && t == ntiles - 1;
                 mbar_wait(&sm.empty[stage], phase ^ 1);
-                Stage<D> &st = sm.st[stage];
+                Stage<D, TILE> &st = sm.st[stage];
                 uint32_t bytes = 2u * nr * D * 2;
                 int moff = 0;
                 uint32_t mbytes = 0;
@@ -210,7 +212,7 @@ __global__ void __launch_bounds__(THREADS, 2) decode_attention_kernel(const Para
     uint32_t part_phase = 0;     // parity of part_bar (tracked by warp 0)
     while (true) {
         mbar_wait(&sm.full[stage], phase);
-        Stage<D> &st = sm.st[stage];
+        Stage<D, TILE> &st = sm.st[stage];
         const StageDesc d = st.desc;
         if (d.flags & F_END) break;
         if (d.flags & F_FIRST) {
@@ -332,21 +334,21 @@ __global__ void __launch_bounds__(THREADS, 2) decode_attention_kernel(const Para
 #pragma unroll
             for (int w2 = 0; w2 < CWARPS; ++w2) M = fmaxf(M, sm.red_m[rb][w2]);
             const size_t bh = (size_t)d.b * p.Hq + d.h;
-            if (t < D) {
+            for (int dd = t; dd < D; dd += CWARPS * 32) {
                 float Lt = 0.f, Ot = 0.f;
 #pragma unroll
                 for (int w2 = 0; w2 < CWARPS; ++w2) {
                     const float mw = sm.red_m[rb][w2];
                     const float f = (mw == -INFINITY) ? 0.f : ex2(mw - M);
                     Lt = fmaf(f, sm.red_l[rb][w2], Lt);
-                    Ot = fmaf(f, sm.red_o[rb][w2][t], Ot);
+                    Ot = fmaf(f, sm.red_o[rb][w2][dd], Ot);
                 }
                 if (d.nchunks == 1) {
-                    p.out[bh * D + t] = __float2bfloat16_rn(Lt > 0.f ? Ot / Lt : 0.f);
+                    p.out[bh * D + dd] = __float2bfloat16_rn(Lt > 0.f ? Ot / Lt : 0.f);
                 } else {
                     float *pp = p.partial + (bh * p.max_chunks + d.c) * (D + PREC_PAD);
-                    pp[t] = Ot;
-                    if (t == 0) {
+                    pp[dd] = Ot;
+                    if (dd == 0) {
                         pp[D] = M;
                         pp[D + 1] = Lt;
                     }
@@ -393,7 +395,7 @@ __global__ void __launch_bounds__(THREADS, 2) decode_attention_kernel(const Para
     }
 }
 
-template <int D>
+template <int D, int CW, int ST, int MINB>
 cudaError_t launch_d(const DecodeArgs &a, cudaStream_t s) {
     static int num_sms = 0;
     if (!num_sms) {
@@ -401,10 +403,10 @@ cudaError_t launch_d(const DecodeArgs &a, cudaStream_t s) {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    const size_t smem = sizeof(Smem<D>);
+    const size_t smem = sizeof(Smem<D, CW, ST>);
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(decode_attention_kernel<D>,
+        cudaError_t e = cudaFuncSetAttribute(decode_attention_kernel<D, CW, ST, MINB>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         attr_set = true;
@@ -431,7 +433,19 @@ cudaError_t launch_d(const DecodeArgs &a, cudaStream_t s) {
     p.max_ctx = a.max_ctx;
     p.max_chunks = a.max_chunks;
     p.scale_log2 = a.scale * 1.4426950408889634f;
-    return launch_pdl(decode_attention_kernel<D>, dim3(2 * num_sms), dim3(THREADS), smem, s, p);
+    return launch_pdl(decode_attention_kernel<D, CW, ST, MINB>, dim3(MINB * num_sms),
+                      dim3((CW + 1) * 32), smem, s, p);
+}
+
+// head_dim 128 pipeline variants (consumer warps, ring stages, CTAs per SM), chosen
+// by BATON_MHA_VARIANT for sweeps; 0 is the default.
+int mha_variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("BATON_MHA_VARIANT");
+        v = e ? atoi(e) : 0;
+    }
+    return v;
 }
 
 }  // namespace
@@ -447,10 +461,17 @@ bool decode_supported_head_dim(int d) { return d == 16 || d == 32 || d == 64 || 
 cudaError_t launch_decode_attention(const DecodeArgs &a, cudaStream_t s) {
     if (gqa_supported(a.q_heads, a.kv_heads, a.head_dim)) return launch_decode_gqa(a, s);
     switch (a.head_dim) {
-        case 16: return launch_d<16>(a, s);
-        case 32: return launch_d<32>(a, s);
-        case 64: return launch_d<64>(a, s);
-        case 128: return launch_d<128>(a, s);
+        case 16: return launch_d<16, 4, 3, 2>(a, s);
+        case 32: return launch_d<32, 4, 3, 2>(a, s);
+        case 64: return launch_d<64, 4, 3, 2>(a, s);
+        case 128:
+            switch (mha_variant()) {
+                case 1: return launch_d<128, 4, 6, 1>(a, s);
+                case 2: return launch_d<128, 8, 3, 1>(a, s);
+                case 3: return launch_d<128, 4, 2, 3>(a, s);
+                case 4: return launch_d<128, 2, 3, 3>(a, s);
+                default: return launch_d<128, 4, 3, 2>(a, s);
+            }
         default: return cudaErrorInvalidValue;
     }
 }

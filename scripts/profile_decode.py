@@ -54,21 +54,42 @@ def main():
     out = torch.empty_like(q)
     tau = 2 * wl.kv_heads * wl.head_dim * 2
     nbytes = int(live.sum()) * tau + int((live > 0).sum()) * wl.q_heads * wl.head_dim * 4
-    times = []
-    for it in range(args.iters):
+    # capture iters x L launches in a CUDA graph: GPU time only, no host launch overhead
+    g = torch.cuda.CUDAGraph()
+    s_ = torch.cuda.Stream()
+    s_.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s_):
         for l in range(L):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            sh.baton_decode_attention(l, q, out)
-            e1.record()
-            times.append((e0, e1))
+            sh.baton_decode_attention(l, q, out)   # warm (sets kernel attributes)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s_):
+            for it in range(args.iters):
+                for l in range(L):
+                    sh.baton_decode_attention(l, q, out)
     torch.cuda.synchronize()
-    us = [a.elapsed_time(b) * 1e3 for a, b in times]
-    us_w = us[L:]   # drop the first pass
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    us_graph = e0.elapsed_time(e1) * 1e3 / (args.iters * L)
+    times = []
+    for it in range(3):
+        for l in range(L):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            sh.baton_decode_attention(l, q, out)
+            b.record()
+            times.append((a, b))
+    torch.cuda.synchronize()
+    us_w = [a.elapsed_time(b) * 1e3 for a, b in times][L:]
     print(json.dumps({"config": args.config, "live_slots": int((live > 0).sum()),
                       "sum_lens": int(live.sum()), "bytes_per_launch": nbytes,
-                      "us_median": float(np.median(us_w)), "us_min": float(np.min(us_w)),
-                      "GBps_median": nbytes / np.median(us_w) / 1e3}))
+                      "us_per_launch_graph": us_graph, "GBps_graph": nbytes / us_graph / 1e3,
+                      "us_eager_median": float(np.median(us_w)),
+                      "variant": os.environ.get("BATON_MHA_VARIANT", "0")}))
 
 
 if __name__ == "__main__":
