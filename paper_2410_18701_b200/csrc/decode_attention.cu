@@ -470,6 +470,10 @@ cudaError_t launch_decode_attention(const DecodeArgs &a, cudaStream_t s) {
                 case 2: return launch_d<128, 8, 3, 1>(a, s);
                 case 3: return launch_d<128, 4, 2, 3>(a, s);
                 case 4: return launch_d<128, 2, 3, 3>(a, s);
+                case 5: return launch_d<128, 2, 2, 5>(a, s);
+                case 6: return launch_d<128, 2, 2, 4>(a, s);
+                case 7: return launch_d<128, 1, 4, 5>(a, s);
+                case 8: return launch_d<128, 3, 2, 3>(a, s);
                 default: return launch_d<128, 4, 3, 2>(a, s);
             }
         default: return cudaErrorInvalidValue;
