@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
+#include <cstdio>
 
 #include <utility>
 
@@ -45,8 +46,19 @@ BATON_DEV bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+// Watchdog: a pipeline deadlock reports the waiting barrier and traps after ~2 s
+// (turns a hung GPU into a launch error).  try_wait itself suspends in hardware,
+// so the clock is read only every 1024 unsuccessful tries.
 BATON_DEV void mbar_wait(uint64_t *bar, uint32_t parity) {
-    while (!mbar_try_wait(bar, parity)) {
+    if (mbar_try_wait(bar, parity)) return;
+    const long long t0 = clock64();
+    for (uint32_t n = 1;; ++n) {
+        if (mbar_try_wait(bar, parity)) return;
+        if ((n & 1023) == 0 && clock64() - t0 > 4000000000LL) {
+            printf("baton watchdog: block %d thread %d stuck on mbarrier smem+0x%x parity %u\n",
+                   blockIdx.x, threadIdx.x, smem_u32(bar), parity);
+            __trap();
+        }
     }
 }
 

@@ -32,8 +32,9 @@ namespace baton {
 namespace {
 
 constexpr int ROWS_PER_WARP = 16;
-// Default variant: 4 consumer warps (64-key tiles), 3-stage ring, 2 CTAs per SM.
-// (CWARPS, STAGES, CTAs/SM) are template parameters so variants can be swept.
+// (consumer warps, ring stages, CTAs per SM) are template parameters; the default
+// for head_dim 128 is (2, 2, 5): 32-key tiles, many small independent CTAs -- the
+// sweep showed resident-CTA parallelism beats deeper rings (see launch table).
 
 constexpr int F_FIRST = 1, F_LAST = 2, F_END = 4, F_WRITE = 8;
 
@@ -466,15 +467,13 @@ cudaError_t launch_decode_attention(const DecodeArgs &a, cudaStream_t s) {
         case 64: return launch_d<64, 4, 3, 2>(a, s);
         case 128:
             switch (mha_variant()) {
-                case 1: return launch_d<128, 4, 6, 1>(a, s);
-                case 2: return launch_d<128, 8, 3, 1>(a, s);
+                // measured on the cfg2 t0 state (profiles/r01_mha_sweep.md), us/launch:
+                // (4,3,2) 66.2  (4,6,1) 93.6  (8,3,1) 82.3  (4,2,3) 59.8  (2,3,3) 64.2
+                // (2,2,5) 58.7  (2,2,4) 59.2  (1,4,5) 64.6  (3,2,3) 60.8
+                case 1: return launch_d<128, 4, 3, 2>(a, s);
                 case 3: return launch_d<128, 4, 2, 3>(a, s);
-                case 4: return launch_d<128, 2, 3, 3>(a, s);
-                case 5: return launch_d<128, 2, 2, 5>(a, s);
                 case 6: return launch_d<128, 2, 2, 4>(a, s);
-                case 7: return launch_d<128, 1, 4, 5>(a, s);
-                case 8: return launch_d<128, 3, 2, 3>(a, s);
-                default: return launch_d<128, 4, 3, 2>(a, s);
+                default: return launch_d<128, 2, 2, 5>(a, s);
             }
         default: return cudaErrorInvalidValue;
     }

@@ -18,6 +18,8 @@
 //     ldmatrix.trans).
 //   epilogue: 4 warp states merged in smem; single chunk -> bf16 out, else split-K
 //     partials + last-CTA merge (same workspace layout as decode_attention.cu).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "sched.cuh"
@@ -31,7 +33,6 @@ constexpr int GS = 8;                       // q heads per kv head
 constexpr int CW = 4;                       // consumer warps
 constexpr int KPW = 16;                     // keys per warp per tile
 constexpr int TILE = CW * KPW;              // 64
-constexpr int STAGES = 4;
 constexpr int THREADS = (CW + 1) * 32;
 constexpr int HALF = TILE * 128;            // bytes of one 64-dim half of a tile (8 KB)
 constexpr int F_FIRST = 1, F_LAST = 2, F_END = 4;
@@ -48,6 +49,7 @@ struct __align__(1024) Stage {
     Desc desc;
 };
 
+template <int STAGES>
 struct Smem {
     Stage st[STAGES];
     uint64_t full[STAGES], empty[STAGES];
@@ -102,13 +104,14 @@ BATON_DEV void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1, ui
         : "memory");
 }
 
-__global__ void __launch_bounds__(THREADS, 1)
+template <int STAGES, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB)
 decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
                   const Params p) {
     extern __shared__ uint8_t smem_raw[];
     // 1024-B alignment for the SWIZZLE_128B boxes; offsetting the __shared__ array
     // itself keeps the shared address space visible to the compiler (LDS, not LD)
-    Smem &sm = *reinterpret_cast<Smem *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+    Smem<STAGES> &sm = *reinterpret_cast<Smem<STAGES> *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
@@ -414,17 +417,18 @@ bool gqa_supported(int q_heads, int kv_heads, int head_dim) {
     return head_dim == D && kv_heads > 0 && q_heads == GS * kv_heads;
 }
 
-cudaError_t launch_decode_gqa(const DecodeArgs &a, cudaStream_t s) {
+template <int STAGES, int MINB>
+cudaError_t launch_gqa_v(const DecodeArgs &a, cudaStream_t s) {
     static int num_sms = 0;
     if (!num_sms) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    const size_t smem = sizeof(Smem) + 1024;
+    const size_t smem = sizeof(Smem<STAGES>) + 1024;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(decode_gqa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(decode_gqa_kernel<STAGES, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
@@ -458,12 +462,22 @@ cudaError_t launch_decode_gqa(const DecodeArgs &a, cudaStream_t s) {
                                          a.lens, a.slots, a.kv_heads, a.head_dim, a.max_ctx, s);
         if (e != cudaSuccess) return e;
     }
-    cudaError_t e = launch_pdl(decode_gqa_kernel, dim3(num_sms), dim3(THREADS), smem, s, km, vm, p);
+    cudaError_t e = launch_pdl(decode_gqa_kernel<STAGES, MINB>, dim3(MINB * num_sms), dim3(THREADS), smem, s, km, vm, p);
     if (e != cudaSuccess) return e;
     const int pairs = a.slots * a.q_heads;
     return launch_pdl(decode_combine_kernel, dim3((pairs + 3) / 4), dim3(128), 0, s, a.lens,
                       (const float *)a.partial, static_cast<__nv_bfloat16 *>(a.out), a.slots,
                       a.q_heads, a.max_chunks);
+}
+
+cudaError_t launch_decode_gqa(const DecodeArgs &a, cudaStream_t s) {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("BATON_GQA_VARIANT");
+        v = e ? atoi(e) : 0;
+    }
+    if (v == 1) return launch_gqa_v<2, 2>(a, s);
+    return launch_gqa_v<4, 1>(a, s);
 }
 
 }  // namespace baton

@@ -322,277 +322,6 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
 }
 
 
-// =====================================================================================
-// v2: two query tiles per CTA (256 rows), ping-pong softmax warpgroups.
-//   warps 0-3: softmax of tile A (rows q0 .. q0+127), warps 4-7: tile B (+128 .. +255)
-//   warp 8: TMA producer (Q_A, Q_B once; K_j and V_j single-buffered, refilled as soon
-//           as the MMAs that read them complete)
-//   warp 9: MMA issuer, order per key tile j:
-//             PV_A(j), S_A(j+1), PV_B(j), S_B(j+1)
-//           so the tensor pipe computes one tile's MMAs while the other tile's
-//           warpgroup is in softmax.
-//   TMEM (512 columns): S_A | S_B | O_A | O_B.  P goes through smem (K-major SW128).
-//   Softmax: lazy rescaling (the exponent reference only moves when the running max
-//   grows by > 8 in log2 units; P <= 256 is exact enough in bf16) and every second
-//   exponential on the FMA pipe (degree-3 polynomial, rel. err 8.6e-5 << bf16) to
-//   relieve the MUFU pipe, as FA4 does.
-// =====================================================================================
-constexpr int P2_THREADS = 320;
-constexpr float LAZY_TH = 8.f;
-
-struct __align__(1024) PfSmem2 {
-    uint8_t q[2][TILE_BYTES];
-    uint8_t k[TILE_BYTES];
-    uint8_t v[TILE_BYTES];
-    uint8_t p[2][TILE_BYTES];
-    uint64_t q_full, k_full, k_free, v_full, v_free;
-    uint64_t s_full[2], p_full[2], o_done[2];
-    uint32_t tmem_base;
-};
-
-// 2^x on the FMA pipe: x = n + f, 2^f ~ 1 + f(c1 + f(c2 + f c3)), scaled by 2^n
-BATON_DEV float ex2_poly(float x) {
-    x = fmaxf(x, -126.f);
-    const float n = floorf(x);
-    const float f = x - n;
-    float p = fmaf(fmaf(fmaf(0.07705727f, f, 0.22765567f), f, 0.69511441f), f, 1.0f);
-    return __int_as_float(__float_as_int(p) + (static_cast<int>(n) << 23));
-}
-
-__global__ void __launch_bounds__(P2_THREADS, 1)
-prefill_attention_v2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                            const __grid_constant__ CUtensorMap tm_v, const PfParams p) {
-    extern __shared__ uint8_t smem_raw[];
-    PfSmem2 &sm = *reinterpret_cast<PfSmem2 *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n_pairs = (p.n_mtiles + 1) / 2;                  // 256-row query blocks
-    const int pr = n_pairs - 1 - (int)(blockIdx.x % n_pairs);  // heavy blocks first
-    const int h = blockIdx.x / n_pairs;
-    const int g = h * p.Hkv / p.Hq;
-    const int q0 = pr * 2 * PF_M;
-    const int mA = 2 * pr;                                     // query tile index of A
-    const bool hasB = q0 + PF_M < p.len;
-    const int nA = mA + 1;                                     // key tiles needed by A
-    const int nB = hasB ? (min(q0 + 2 * PF_M, p.len) + PF_N - 1) / PF_N : 0;
-    const int nmax = hasB ? nB : nA;
-
-    if (threadIdx.x == 0) {
-        mbar_init(&sm.q_full, 1);
-        mbar_init(&sm.k_full, 1);
-        mbar_init(&sm.k_free, 1);
-        mbar_init(&sm.v_full, 1);
-        mbar_init(&sm.v_free, 1);
-        for (int t = 0; t < 2; ++t) {
-            mbar_init(&sm.s_full[t], 1);
-            mbar_init(&sm.p_full[t], 128);
-            mbar_init(&sm.o_done[t], 1);
-        }
-        fence_mbar_init();
-    }
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                         smem_u32(&sm.tmem_base)));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = sm.tmem_base;
-
-    if (warp == 8) {
-        // ======================= TMA producer =======================
-        if (lane == 0) {
-            prefetch_tmap(&tm_q);
-            prefetch_tmap(&tm_k);
-            prefetch_tmap(&tm_v);
-            mbar_arrive_expect_tx(&sm.q_full, (hasB ? 2 : 1) * TILE_BYTES);
-            tma_load_3d(sm.q[0], &tm_q, 0, q0, h, &sm.q_full);
-            tma_load_3d(sm.q[0] + REGION, &tm_q, 64, q0, h, &sm.q_full);
-            if (hasB) {
-                tma_load_3d(sm.q[1], &tm_q, 0, q0 + PF_M, h, &sm.q_full);
-                tma_load_3d(sm.q[1] + REGION, &tm_q, 64, q0 + PF_M, h, &sm.q_full);
-            }
-            for (int j = 0; j < nmax; ++j) {
-                if (j > 0) mbar_wait(&sm.k_free, (j - 1) & 1);   // S(j-1) of both tiles done
-                mbar_arrive_expect_tx(&sm.k_full, TILE_BYTES);
-                tma_load_3d(sm.k, &tm_k, 0, j * PF_N, g, &sm.k_full);
-                tma_load_3d(sm.k + REGION, &tm_k, 64, j * PF_N, g, &sm.k_full);
-                if (j > 0) mbar_wait(&sm.v_free, (j - 1) & 1);   // PV(j-1) of both tiles done
-                mbar_arrive_expect_tx(&sm.v_full, TILE_BYTES);
-                tma_load_3d(sm.v, &tm_v, 0, j * PF_N, g, &sm.v_full);
-                tma_load_3d(sm.v + REGION, &tm_v, 64, j * PF_N, g, &sm.v_full);
-            }
-        }
-    } else if (warp == 9) {
-        // ======================= MMA issuer =======================
-        if (lane == 0) {
-            constexpr uint32_t idS = idesc_bf16(PF_M, PF_N, 0);
-            constexpr uint32_t idO = idesc_bf16(PF_M, PF_D, 1);
-            const uint32_t ka = smem_u32(sm.k), va = smem_u32(sm.v);
-            auto issue_s = [&](int t) {
-                const uint32_t qa = smem_u32(sm.q[t]);
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const uint32_t off = (k >> 2) * REGION + (k & 3) * 32;
-                    umma_f16(tmem + t * 128, smem_desc(qa + off, 16, 1024), smem_desc(ka + off, 16, 1024),
-                             idS, k > 0);
-                }
-                umma_commit(&sm.s_full[t]);
-            };
-            auto issue_pv = [&](int t, int j) {
-                const uint32_t pa = smem_u32(sm.p[t]);
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const uint32_t aoff = (k >> 2) * REGION + (k & 3) * 32;
-                    umma_f16(tmem + 256 + t * 128, smem_desc(pa + aoff, 16, 1024),
-                             smem_desc(va + k * 2048, REGION, 1024), idO, (j > 0 || k > 0));
-                }
-                umma_commit(&sm.o_done[t]);
-            };
-            mbar_wait(&sm.q_full, 0);
-            mbar_wait(&sm.k_full, 0);
-            tc_fence_after();
-            issue_s(0);
-            if (hasB) issue_s(1);
-            umma_commit(&sm.k_free);
-            for (int j = 0; j < nmax; ++j) {
-                mbar_wait(&sm.v_full, j & 1);
-                const bool nextK = j + 1 < nmax;
-                if (j < nA) {
-                    mbar_wait(&sm.p_full[0], j & 1);
-                    tc_fence_after();
-                    issue_pv(0, j);
-                }
-                if (nextK) {
-                    mbar_wait(&sm.k_full, (j + 1) & 1);
-                    tc_fence_after();
-                    if (j + 1 < nA) issue_s(0);
-                }
-                if (j < nB) {
-                    mbar_wait(&sm.p_full[1], j & 1);
-                    tc_fence_after();
-                    issue_pv(1, j);
-                }
-                umma_commit(&sm.v_free);
-                if (nextK) {
-                    if (j + 1 < nB) issue_s(1);
-                    umma_commit(&sm.k_free);
-                }
-            }
-        }
-    } else {
-        // ======================= softmax warpgroups =======================
-        const int t = warp >> 2;                     // 0 = tile A, 1 = tile B
-        const int nt = t ? nB : nA;
-        const int row = (warp & 3) * 32 + lane;      // TMEM lane
-        const int qi = q0 + t * PF_M + row;
-        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-        const uint32_t tS = tmem + t * 128 + lane_off, tO = tmem + 256 + t * 128 + lane_off;
-        float m_ref = -INFINITY, l = 0.f;
-        uint32_t pk[64];
-        for (int j = 0; j < nt; ++j) {
-            mbar_wait(&sm.s_full[t], j & 1);
-            tc_fence_after();
-            const int kbase = j * PF_N;
-            const bool diag = kbase + PF_N > q0 + t * PF_M;
-            float mx = -INFINITY;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                uint32_t r[32];
-                tmem_ld32(tS + c * 32, r);
-                tmem_wait_ld();
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    float x = __uint_as_float(r[i]) * p.scale_log2;
-                    if (diag && kbase + c * 32 + i > qi) x = -INFINITY;
-                    mx = fmaxf(mx, x);
-                }
-            }
-            // lazy reference: only move it when the max grows by more than LAZY_TH
-            float alpha = 1.f;
-            if (mx > m_ref + LAZY_TH || m_ref == -INFINITY) {
-                alpha = ex2(m_ref - mx);      // m_ref = -inf -> 0
-                m_ref = mx;
-            }
-            float rs = 0.f;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                uint32_t r[32];
-                tmem_ld32(tS + c * 32, r);
-                tmem_wait_ld();
-#pragma unroll
-                for (int i = 0; i < 32; i += 2) {
-                    const int kj = kbase + c * 32 + i;
-                    float x0 = __uint_as_float(r[i]) * p.scale_log2 - m_ref;
-                    float x1 = __uint_as_float(r[i + 1]) * p.scale_log2 - m_ref;
-                    const float e0 = (diag && kj > qi) ? 0.f : ex2(x0);
-                    const float e1 = (diag && kj + 1 > qi) ? 0.f : ex2_poly(x1);
-                    const __nv_bfloat162 b = __floats2bfloat162_rn(e0, e1);
-                    rs += __low2float(b) + __high2float(b);
-                    pk[c * 16 + i / 2] = *reinterpret_cast<const uint32_t *>(&b);
-                }
-            }
-            l = l * alpha + rs;
-            if (j > 0) {
-                mbar_wait(&sm.o_done[t], (j - 1) & 1);   // PV(j-1): O stable, P buffer free
-                tc_fence_after();
-                if (__any_sync(FULL_MASK, alpha != 1.f)) {   // warp-uniform (.sync.aligned)
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        uint32_t r[32];
-                        tmem_ld32(tO + c * 32, r);
-                        tmem_wait_ld();
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-                        tmem_st32(tO + c * 32, r);
-                    }
-                    tmem_wait_st();
-                }
-            }
-            uint8_t *pbuf = sm.p[t];
-#pragma unroll
-            for (int c = 0; c < 16; ++c) {
-                const int region = c >> 3, chunk = c & 7;
-                uint8_t *dst = pbuf + region * REGION + row * 128 + ((chunk ^ (row & 7)) << 4);
-                *reinterpret_cast<uint4 *>(dst) = make_uint4(pk[c * 4], pk[c * 4 + 1], pk[c * 4 + 2], pk[c * 4 + 3]);
-            }
-            fence_async_smem();
-            tc_fence_before();
-            mbar_arrive(&sm.p_full[t]);
-        }
-        if (nt > 0) {
-            mbar_wait(&sm.o_done[t], (nt - 1) & 1);
-            tc_fence_after();
-            const float inv = 1.f / l;
-            __nv_bfloat16 *orow = p.out + ((size_t)h * p.len + qi) * PF_D;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                uint32_t r[32];
-                tmem_ld32(tO + c * 32, r);
-                tmem_wait_ld();
-                if (qi < p.len) {
-                    uint32_t w[16];
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const __nv_bfloat162 b = __floats2bfloat162_rn(__uint_as_float(r[2 * i]) * inv,
-                                                                       __uint_as_float(r[2 * i + 1]) * inv);
-                        w[i] = *reinterpret_cast<const uint32_t *>(&b);
-                    }
-                    uint4 *o4 = reinterpret_cast<uint4 *>(orow + c * 32);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) o4[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
-                }
-            }
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 0) {
-        tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-    }
-}
-
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     if (!fn) {
@@ -636,29 +365,15 @@ cudaError_t launch_prefill_attention(const void *q, const void *k, const void *v
     p.n_mtiles = (len + PF_M - 1) / PF_M;
     p.scale_log2 = scale * 1.4426950408889634f;
     p.out = static_cast<__nv_bfloat16 *>(out);
-    static const bool use_v1 = getenv("BATON_PREFILL_V1") != nullptr;
-    if (use_v1) {
-        const size_t smem = sizeof(PfSmem) + 1024;
-        static bool attr = false;
-        if (!attr) {
-            cudaError_t e = cudaFuncSetAttribute(prefill_attention_kernel,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return e;
-            attr = true;
-        }
-        prefill_attention_kernel<<<p.n_mtiles * q_heads, PF_THREADS, smem, s>>>(mq, mk, mv, p);
-    } else {
-        const size_t smem = sizeof(PfSmem2) + 1024;
-        static bool attr2 = false;
-        if (!attr2) {
-            cudaError_t e = cudaFuncSetAttribute(prefill_attention_v2_kernel,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return e;
-            attr2 = true;
-        }
-        const int n_pairs = (p.n_mtiles + 1) / 2;
-        prefill_attention_v2_kernel<<<n_pairs * q_heads, P2_THREADS, smem, s>>>(mq, mk, mv, p);
+    const size_t smem = sizeof(PfSmem) + 1024;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(prefill_attention_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
     }
+    prefill_attention_kernel<<<p.n_mtiles * q_heads, PF_THREADS, smem, s>>>(mq, mk, mv, p);
     return cudaGetLastError();
 }
 
