@@ -478,6 +478,10 @@ def main():
         peak, peak_kind = _peaks()
         achieved = r["attn_bytes"] / r["attn_time_s"] / 1e9 if r["attn_time_s"] else 0.0
         per_launch = r["attn_bytes"] / max(1, r["attn_launches"])
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "r01_traffic.json")
+        if os.path.exists(tp):
+            traffic = json.load(open(tp))["traffic_bytes"]
         line = {
             "metric": "decode tokens/s (7B-shape Baton batch)",
             "value": tokens / (ms / 1e3),
@@ -497,11 +501,14 @@ def main():
                        "l2": "inputs larger than L2 (32 GiB KV cache, ~12 GiB read per step)",
                        "live_slots_per_step": r["live_slots"]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": traffic,
+                         "traffic_source": "profiles/r01_traffic.json (one ncu --set full launch)",
                          "kernel": "decode_attention_kernel<128>",
                          "bytes_per_launch": per_launch,
                          "peak_source": peak_kind,
-                         "avg_launch_us": 1e6 * r["attn_time_s"] / max(1, r["attn_launches"])},
+                         "avg_launch_us": 1e6 * r["attn_time_s"] / max(1, r["attn_launches"]),
+                         "timing": "eager launches bracketed by CUDA events over the same K-step window",
+                         "step_hbm_GBps": r["attn_bytes"] / (ms / 1e3) / 1e9},
             "gpu_launches": r["n_launch"],
             "clocks": r["clocks"],
         }
