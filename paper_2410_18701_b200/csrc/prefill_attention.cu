@@ -37,7 +37,7 @@ struct __align__(1024) PfSmem {
     uint8_t k[2][TILE_BYTES];
     uint8_t v[2][TILE_BYTES];
     uint8_t p[TILE_BYTES];
-    uint64_t bar_q, kv_full[2], kv_empty[2], s_full[2], s_free[2], p_full, o_done;
+    uint64_t bar_q, kv_full[2], kv_empty[2], s_full, s_free, p_full, o_done;
     uint32_t tmem_base;
 };
 
@@ -113,17 +113,6 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int b_mn_major) 
            ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-// 2^x on the FMA pipe for x <= 0 (or -inf): x = n + f, 2^f ~ 1 + f(c1 + f(c2 + f c3))
-// (least-squares fit, max rel. error 8.6e-5 << bf16's 3.9e-3), scaled by 2^n
-BATON_DEV float ex2_poly(float x) {
-    const float xc = fmaxf(x, -126.f);
-    const float n = floorf(xc);
-    const float f = xc - n;
-    const float q = fmaf(fmaf(fmaf(0.07705727f, f, 0.22765567f), f, 0.69511441f), f, 1.0f);
-    const float y = __int_as_float(__float_as_int(q) + (static_cast<int>(n) << 23));
-    return x < -126.f ? 0.f : y;   // masked (-inf) and underflow -> exactly 0
-}
-
 struct PfParams {
     int Hq, Hkv, len, n_mtiles;
     float scale_log2;
@@ -149,16 +138,14 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
             mbar_init(&sm.kv_full[s], 1);
             mbar_init(&sm.kv_empty[s], 1);
         }
-        for (int b = 0; b < 2; ++b) {
-            mbar_init(&sm.s_full[b], 1);
-            mbar_init(&sm.s_free[b], 128);
-        }
+        mbar_init(&sm.s_full, 1);
+        mbar_init(&sm.s_free, 128);
         mbar_init(&sm.p_full, 128);
         mbar_init(&sm.o_done, 1);
         fence_mbar_init();
     }
-    if (warp == 0) {   // TMEM: S double buffer in columns [0,256), O in [256,384)
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+    if (warp == 0) {   // TMEM: S in columns [0,128), O in [128,256)
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
                          smem_u32(&sm.tmem_base)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
@@ -166,7 +153,7 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = sm.tmem_base;
-    const uint32_t tO = tmem + 256;   // S(j) lives in columns (j & 1) * 128
+    const uint32_t tS = tmem, tO = tmem + 128;
 
     if (warp == 4) {
         // ======================= TMA producer =======================
@@ -193,28 +180,19 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
             constexpr uint32_t idS = idesc_bf16(PF_M, PF_N, 0);   // B = K tile, K-major
             constexpr uint32_t idO = idesc_bf16(PF_M, PF_D, 1);   // B = V tile, MN-major
             const uint32_t qa = smem_u32(sm.q), pa = smem_u32(sm.p);
-            // S(j) = Q K_j^T into TMEM buffer j&1 (K_j in ring stage j&1)
-            auto issue_s = [&](int j) {
+            mbar_wait(&sm.bar_q, 0);
+            for (int j = 0; j < n_kt; ++j) {
                 const int s = j & 1;
                 mbar_wait(&sm.kv_full[s], (j >> 1) & 1);
-                if (j >= 2) mbar_wait(&sm.s_free[s], ((j - 2) >> 1) & 1);   // S(j-2) was read
+                if (j > 0) mbar_wait(&sm.s_free, (j - 1) & 1);   // softmax has read S_{j-1}
                 tc_fence_after();
-                const uint32_t ka = smem_u32(sm.k[s]);
+                const uint32_t ka = smem_u32(sm.k[s]), va = smem_u32(sm.v[s]);
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {   // K = head_dim in steps of 16 (32 B)
                     const uint32_t off = (k >> 2) * REGION + (k & 3) * 32;
-                    umma_f16(tmem + s * 128, smem_desc(qa + off, 16, 1024), smem_desc(ka + off, 16, 1024),
-                             idS, k > 0);
+                    umma_f16(tS, smem_desc(qa + off, 16, 1024), smem_desc(ka + off, 16, 1024), idS, k > 0);
                 }
-                umma_commit(&sm.s_full[s]);
-            };
-            mbar_wait(&sm.bar_q, 0);
-            issue_s(0);
-            for (int j = 0; j < n_kt; ++j) {
-                const int s = j & 1;
-                // the next S goes to the other TMEM buffer while softmax works on S(j)
-                if (j + 1 < n_kt) issue_s(j + 1);
-                const uint32_t va = smem_u32(sm.v[s]);
+                umma_commit(&sm.s_full);
                 mbar_wait(&sm.p_full, j & 1);                   // P_j written, O rescaled
                 tc_fence_after();
 #pragma unroll
@@ -235,9 +213,7 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
         float m = -INFINITY, l = 0.f;
         uint32_t pk[64];                              // P row packed bf16x2
         for (int j = 0; j < n_kt; ++j) {
-            const int sb = j & 1;
-            const uint32_t tS = tmem + sb * 128;
-            mbar_wait(&sm.s_full[sb], (j >> 1) & 1);
+            mbar_wait(&sm.s_full, j & 1);
             tc_fence_after();
             const int kbase = j * PF_N;
             const bool diag = kbase + PF_N > q0;      // tile touches the causal diagonal
@@ -272,8 +248,7 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
                     float x1 = __uint_as_float(r[i + 1]) * p.scale_log2;
                     if (diag && kj > qi) x0 = -INFINITY;
                     if (diag && kj + 1 > qi) x1 = -INFINITY;
-                    // every second exponential on the FMA pipe (relieves the MUFU pipe)
-                    const float e0 = ex2(x0 - m_new), e1 = ex2_poly(x1 - m_new);
+                    const float e0 = ex2(x0 - m_new), e1 = ex2(x1 - m_new);
                     const __nv_bfloat162 b = __floats2bfloat162_rn(e0, e1);
                     // the PV MMA consumes bf16 P: accumulate the sum of what it multiplies
                     rs += __low2float(b) + __high2float(b);
@@ -283,7 +258,7 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
             l = l * alpha + rs;
             m = m_new;
             tc_fence_before();
-            mbar_arrive(&sm.s_free[sb]);
+            mbar_arrive(&sm.s_free);
             if (j > 0) {
                 mbar_wait(&sm.o_done, (j - 1) & 1);   // PV_{j-1} done: O stable, P buffer free
                 tc_fence_after();
@@ -342,7 +317,7 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
     __syncthreads();
     if (warp == 0) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
     }
 }
 
