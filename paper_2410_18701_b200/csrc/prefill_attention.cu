@@ -5,39 +5,43 @@
 // SDPA of query token i over keys 0..i -- the decode attention of every
 // prefix at once, a dense contraction, so it runs on the 5th-gen tensor cores.
 //
-// One CTA per (q head, 128-query tile).  Warp roles:
-//   warp 4   TMA producer: Q tile once, then K/V tiles of 128 keys into a 2-stage
-//            ring (cp.async.bulk.tensor, SWIZZLE_128B, mbarrier tx-counts)
-//   warp 5   MMA issuer (one elected thread): S = Q K^T (M=128,N=128,K=16 x8)
-//            into TMEM, then O += P V (M=128,N=128,K=16 x8) into TMEM, each
+// One CTA per (q head, 128-query tile), TWO CTAs per SM (~98 KB smem, 256 TMEM
+// columns each) so one CTA's softmax overlaps the other's MMAs.  Warp roles
+// (DESIGN.md §6.3):
+//   warp 4   TMA producer: the Q tile once (128 x 128, SWIZZLE_128B), then per
+//            64-key tile K (single buffer, refilled as soon as S(j) is done) and
+//            V (2-stage ring) -- cp.async.bulk.tensor with mbarrier tx-counts
+//   warp 5   MMA issuer (one elected thread): S = Q K^T (M=128, N=64, K=16 x8)
+//            into TMEM, then O += P V (M=128, N=128, K=16 x4) into TMEM, each
 //            completion published with tcgen05.commit -> mbarrier
 //   warps 0-3 softmax: thread = query row; tcgen05.ld of its S row, causal mask,
 //            online max/sum (exp2), P -> bf16 into the K-major SW128 smem layout
 //            the next MMA reads, O rescale in TMEM (tcgen05.ld/st), epilogue.
-#include <cstdlib>
-
 #include <cuda.h>
-#include <cudaTypedefs.h>
 
 #include "common.cuh"
 #include "kernels.h"
+#include "tma.h"
 
 namespace baton {
 namespace {
 
 constexpr int PF_M = 128;         // queries per tile (UMMA M, TMEM lanes)
-constexpr int PF_N = 128;         // keys per tile (UMMA N of S, K of PV)
+constexpr int PF_N = 64;          // keys per tile (UMMA N of S, K of PV)
 constexpr int PF_D = 128;         // head_dim
 constexpr int PF_THREADS = 192;   // 4 softmax warps + producer warp + MMA warp
-constexpr int TILE_BYTES = PF_M * PF_D * 2;     // 32 KB (two 16 KB swizzle regions)
-constexpr int REGION = TILE_BYTES / 2;           // 16 KB: 128 rows x 64 bf16
+constexpr int Q_BYTES = PF_M * PF_D * 2;        // 32 KB: two 16 KB swizzle regions (dims 0-63, 64-127)
+constexpr int Q_REGION = Q_BYTES / 2;
+constexpr int KV_BYTES = PF_N * PF_D * 2;       // 16 KB: two 8 KB regions
+constexpr int KV_REGION = KV_BYTES / 2;
+constexpr int P_BYTES = PF_M * PF_N * 2;        // 16 KB: 128 rows x 64 keys (one 128-B atom per row)
 
 struct __align__(1024) PfSmem {
-    uint8_t q[TILE_BYTES];
-    uint8_t k[2][TILE_BYTES];
-    uint8_t v[2][TILE_BYTES];
-    uint8_t p[TILE_BYTES];
-    uint64_t bar_q, kv_full[2], kv_empty[2], s_full, s_free, p_full, o_done;
+    uint8_t q[Q_BYTES];
+    uint8_t k[KV_BYTES];
+    uint8_t v[2][KV_BYTES];
+    uint8_t p[P_BYTES];
+    uint64_t bar_q, k_full, k_empty, v_full[2], v_empty[2], s_full, s_free, p_full, o_done;
     uint32_t tmem_base;
 };
 
@@ -119,7 +123,7 @@ struct PfParams {
     __nv_bfloat16 *out;
 };
 
-__global__ void __launch_bounds__(PF_THREADS, 1)
+__global__ void __launch_bounds__(PF_THREADS, 2)
 prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                          const __grid_constant__ CUtensorMap tm_v, const PfParams p) {
     extern __shared__ uint8_t smem_raw[];
@@ -134,9 +138,11 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
 
     if (threadIdx.x == 0) {
         mbar_init(&sm.bar_q, 1);
+        mbar_init(&sm.k_full, 1);
+        mbar_init(&sm.k_empty, 1);
         for (int s = 0; s < 2; ++s) {
-            mbar_init(&sm.kv_full[s], 1);
-            mbar_init(&sm.kv_empty[s], 1);
+            mbar_init(&sm.v_full[s], 1);
+            mbar_init(&sm.v_empty[s], 1);
         }
         mbar_init(&sm.s_full, 1);
         mbar_init(&sm.s_free, 128);
@@ -144,7 +150,7 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
         mbar_init(&sm.o_done, 1);
         fence_mbar_init();
     }
-    if (warp == 0) {   // TMEM: S in columns [0,128), O in [128,256)
+    if (warp == 0) {   // TMEM: S in columns [0,64), O in [128,256)
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
                          smem_u32(&sm.tmem_base)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -161,17 +167,19 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
             prefetch_tmap(&tm_q);
             prefetch_tmap(&tm_k);
             prefetch_tmap(&tm_v);
-            mbar_arrive_expect_tx(&sm.bar_q, TILE_BYTES);
+            mbar_arrive_expect_tx(&sm.bar_q, Q_BYTES);
             tma_load_3d(sm.q, &tm_q, 0, q0, h, &sm.bar_q);
-            tma_load_3d(sm.q + REGION, &tm_q, 64, q0, h, &sm.bar_q);
+            tma_load_3d(sm.q + Q_REGION, &tm_q, 64, q0, h, &sm.bar_q);
             for (int j = 0; j < n_kt; ++j) {
+                if (j > 0) mbar_wait(&sm.k_empty, (j - 1) & 1);          // S(j-1) done with K
+                mbar_arrive_expect_tx(&sm.k_full, KV_BYTES);
+                tma_load_3d(sm.k, &tm_k, 0, j * PF_N, g, &sm.k_full);
+                tma_load_3d(sm.k + KV_REGION, &tm_k, 64, j * PF_N, g, &sm.k_full);
                 const int s = j & 1;
-                if (j >= 2) mbar_wait(&sm.kv_empty[s], ((j >> 1) + 1) & 1);
-                mbar_arrive_expect_tx(&sm.kv_full[s], 2 * TILE_BYTES);
-                tma_load_3d(sm.k[s], &tm_k, 0, j * PF_N, g, &sm.kv_full[s]);
-                tma_load_3d(sm.k[s] + REGION, &tm_k, 64, j * PF_N, g, &sm.kv_full[s]);
-                tma_load_3d(sm.v[s], &tm_v, 0, j * PF_N, g, &sm.kv_full[s]);
-                tma_load_3d(sm.v[s] + REGION, &tm_v, 64, j * PF_N, g, &sm.kv_full[s]);
+                if (j >= 2) mbar_wait(&sm.v_empty[s], ((j >> 1) + 1) & 1);   // PV(j-2) done
+                mbar_arrive_expect_tx(&sm.v_full[s], KV_BYTES);
+                tma_load_3d(sm.v[s], &tm_v, 0, j * PF_N, g, &sm.v_full[s]);
+                tma_load_3d(sm.v[s] + KV_REGION, &tm_v, 64, j * PF_N, g, &sm.v_full[s]);
             }
         }
     } else if (warp == 5) {
@@ -179,30 +187,31 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
         if (lane == 0) {
             constexpr uint32_t idS = idesc_bf16(PF_M, PF_N, 0);   // B = K tile, K-major
             constexpr uint32_t idO = idesc_bf16(PF_M, PF_D, 1);   // B = V tile, MN-major
-            const uint32_t qa = smem_u32(sm.q), pa = smem_u32(sm.p);
+            const uint32_t qa = smem_u32(sm.q), pa = smem_u32(sm.p), ka = smem_u32(sm.k);
             mbar_wait(&sm.bar_q, 0);
             for (int j = 0; j < n_kt; ++j) {
                 const int s = j & 1;
-                mbar_wait(&sm.kv_full[s], (j >> 1) & 1);
-                if (j > 0) mbar_wait(&sm.s_free, (j - 1) & 1);   // softmax has read S_{j-1}
+                mbar_wait(&sm.k_full, j & 1);
+                if (j > 0) mbar_wait(&sm.s_free, (j - 1) & 1);   // softmax has read S(j-1)
                 tc_fence_after();
-                const uint32_t ka = smem_u32(sm.k[s]), va = smem_u32(sm.v[s]);
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {   // K = head_dim in steps of 16 (32 B)
-                    const uint32_t off = (k >> 2) * REGION + (k & 3) * 32;
-                    umma_f16(tS, smem_desc(qa + off, 16, 1024), smem_desc(ka + off, 16, 1024), idS, k > 0);
+                    umma_f16(tS, smem_desc(qa + (k >> 2) * Q_REGION + (k & 3) * 32, 16, 1024),
+                             smem_desc(ka + (k >> 2) * KV_REGION + (k & 3) * 32, 16, 1024), idS, k > 0);
                 }
                 umma_commit(&sm.s_full);
-                mbar_wait(&sm.p_full, j & 1);                   // P_j written, O rescaled
+                umma_commit(&sm.k_empty);
+                mbar_wait(&sm.p_full, j & 1);                   // P(j) written, O rescaled
+                mbar_wait(&sm.v_full[s], (j >> 1) & 1);
                 tc_fence_after();
+                const uint32_t va = smem_u32(sm.v[s]);
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {   // K = keys in steps of 16
-                    const uint32_t aoff = (k >> 2) * REGION + (k & 3) * 32;
-                    umma_f16(tO, smem_desc(pa + aoff, 16, 1024),
-                             smem_desc(va + k * 2048, REGION, 1024), idO, (j > 0 || k > 0));
+                for (int k = 0; k < 4; ++k) {   // K = 64 keys in steps of 16
+                    umma_f16(tO, smem_desc(pa + k * 32, 16, 1024),
+                             smem_desc(va + k * 2048, KV_REGION, 1024), idO, (j > 0 || k > 0));
                 }
                 umma_commit(&sm.o_done);
-                umma_commit(&sm.kv_empty[s]);
+                umma_commit(&sm.v_empty[s]);
             }
         }
     } else {
@@ -211,79 +220,67 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
         const int qi = q0 + row;
         const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
         float m = -INFINITY, l = 0.f;
-        uint32_t pk[64];                              // P row packed bf16x2
+        uint32_t pk[32];                              // P row (64 keys) packed bf16x2
         for (int j = 0; j < n_kt; ++j) {
             mbar_wait(&sm.s_full, j & 1);
             tc_fence_after();
             const int kbase = j * PF_N;
             const bool diag = kbase + PF_N > q0;      // tile touches the causal diagonal
-            // pass 1: row max
+            uint32_t r[2][32];
+            tmem_ld32(tS + lane_off, r[0]);
+            tmem_ld32(tS + lane_off + 32, r[1]);
+            tmem_wait_ld();
+            tc_fence_before();
+            mbar_arrive(&sm.s_free);                  // S(j) is in registers: next S may start
             float mx = -INFINITY;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                uint32_t r[32];
-                tmem_ld32(tS + lane_off + c * 32, r);
-                tmem_wait_ld();
+            for (int c = 0; c < 2; ++c)
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
-                    const int kj = kbase + c * 32 + i;
-                    float x = __uint_as_float(r[i]) * p.scale_log2;
-                    if (diag && kj > qi) x = -INFINITY;
+                    float x = __uint_as_float(r[c][i]) * p.scale_log2;
+                    if (diag && kbase + c * 32 + i > qi) x = -INFINITY;
+                    r[c][i] = __float_as_uint(x);
                     mx = fmaxf(mx, x);
                 }
-            }
             const float m_new = fmaxf(m, mx);
             const float alpha = ex2(m - m_new);
-            // pass 2: probabilities
             float rs = 0.f;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                uint32_t r[32];
-                tmem_ld32(tS + lane_off + c * 32, r);
-                tmem_wait_ld();
+            for (int c = 0; c < 2; ++c)
 #pragma unroll
                 for (int i = 0; i < 32; i += 2) {
-                    const int kj = kbase + c * 32 + i;
-                    float x0 = __uint_as_float(r[i]) * p.scale_log2;
-                    float x1 = __uint_as_float(r[i + 1]) * p.scale_log2;
-                    if (diag && kj > qi) x0 = -INFINITY;
-                    if (diag && kj + 1 > qi) x1 = -INFINITY;
-                    const float e0 = ex2(x0 - m_new), e1 = ex2(x1 - m_new);
+                    const float e0 = ex2(__uint_as_float(r[c][i]) - m_new);
+                    const float e1 = ex2(__uint_as_float(r[c][i + 1]) - m_new);
                     const __nv_bfloat162 b = __floats2bfloat162_rn(e0, e1);
                     // the PV MMA consumes bf16 P: accumulate the sum of what it multiplies
                     rs += __low2float(b) + __high2float(b);
                     pk[c * 16 + i / 2] = *reinterpret_cast<const uint32_t *>(&b);
                 }
-            }
             l = l * alpha + rs;
             m = m_new;
-            tc_fence_before();
-            mbar_arrive(&sm.s_free);
             if (j > 0) {
-                mbar_wait(&sm.o_done, (j - 1) & 1);   // PV_{j-1} done: O stable, P buffer free
+                mbar_wait(&sm.o_done, (j - 1) & 1);   // PV(j-1) done: O stable, P buffer free
                 tc_fence_after();
                 // warp-uniform: tcgen05.ld/st are .sync.aligned (all 32 lanes converged)
                 if (__any_sync(FULL_MASK, alpha != 1.f)) {
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
-                        uint32_t r[32];
-                        tmem_ld32(tO + lane_off + c * 32, r);
+                        uint32_t o[32];
+                        tmem_ld32(tO + lane_off + c * 32, o);
                         tmem_wait_ld();
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-                        tmem_st32(tO + lane_off + c * 32, r);
+                        for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+                        tmem_st32(tO + lane_off + c * 32, o);
                     }
                     tmem_wait_st();
                 }
             }
-            // P row -> smem, K-major SWIZZLE_128B: keys [64a, 64a+64) in region a,
-            // 16-B chunk c of row r at chunk position c ^ (r & 7)
+            // P row -> smem, K-major SWIZZLE_128B: 64 keys = one 128-B row, 16-B chunk c
+            // of row r at chunk position c ^ (r & 7)
 #pragma unroll
-            for (int c = 0; c < 16; ++c) {
-                const int region = c >> 3, chunk = c & 7;
-                uint8_t *dst = sm.p + region * REGION + row * 128 + ((chunk ^ (row & 7)) << 4);
-                *reinterpret_cast<uint4 *>(dst) =
-                    make_uint4(pk[c * 4], pk[c * 4 + 1], pk[c * 4 + 2], pk[c * 4 + 3]);
+            for (int c = 0; c < 8; ++c) {
+                uint8_t *dst = sm.p + row * 128 + ((c ^ (row & 7)) << 4);
+                *reinterpret_cast<uint4 *>(dst) = make_uint4(pk[c * 4], pk[c * 4 + 1], pk[c * 4 + 2], pk[c * 4 + 3]);
             }
             fence_async_smem();
             tc_fence_before();
@@ -296,15 +293,15 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
         __nv_bfloat16 *orow = p.out + ((size_t)h * p.len + qi) * PF_D;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-            uint32_t r[32];
-            tmem_ld32(tO + lane_off + c * 32, r);
+            uint32_t o[32];
+            tmem_ld32(tO + lane_off + c * 32, o);
             tmem_wait_ld();
             if (qi < p.len) {
                 uint32_t w[16];
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
-                    const __nv_bfloat162 b = __floats2bfloat162_rn(__uint_as_float(r[2 * i]) * inv,
-                                                                   __uint_as_float(r[2 * i + 1]) * inv);
+                    const __nv_bfloat162 b = __floats2bfloat162_rn(__uint_as_float(o[2 * i]) * inv,
+                                                                   __uint_as_float(o[2 * i + 1]) * inv);
                     w[i] = *reinterpret_cast<const uint32_t *>(&b);
                 }
                 uint4 *o4 = reinterpret_cast<uint4 *>(orow + c * 32);
@@ -321,30 +318,11 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
     }
 }
 
-
-PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
-        cudaDriverEntryPointQueryResult q;
-        void *ptr = nullptr;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
-    }
-    return fn;
-}
-
-bool make_map(CUtensorMap *m, const void *base, int heads, int len) {
-    auto enc = get_encode();
-    if (!enc) return false;
-    cuuint64_t dims[3] = {(cuuint64_t)PF_D, (cuuint64_t)len, (cuuint64_t)heads};
-    cuuint64_t strides[2] = {(cuuint64_t)PF_D * 2, (cuuint64_t)len * PF_D * 2};
-    cuuint32_t box[3] = {64, 128, 1};
-    cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(base), dims, strides,
-                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS;
+bool make_map(CUtensorMap *m, const void *base, int heads, int len, int box_rows) {
+    const uint64_t dims[3] = {(uint64_t)PF_D, (uint64_t)len, (uint64_t)heads};
+    const uint64_t strides[2] = {(uint64_t)PF_D * 2, (uint64_t)len * PF_D * 2};
+    const uint32_t box[3] = {64, (uint32_t)box_rows, 1};
+    return encode_bf16_map(m, base, 3, dims, strides, box);
 }
 
 }  // namespace
@@ -356,15 +334,9 @@ cudaError_t launch_prefill_attention(const void *q, const void *k, const void *v
                                      cudaStream_t s) {
     if (head_dim != PF_D || len < 1) return cudaErrorInvalidValue;
     CUtensorMap mq, mk, mv;
-    if (!make_map(&mq, q, q_heads, len) || !make_map(&mk, k, kv_heads, len) || !make_map(&mv, v, kv_heads, len))
+    if (!make_map(&mq, q, q_heads, len, PF_M) || !make_map(&mk, k, kv_heads, len, PF_N) ||
+        !make_map(&mv, v, kv_heads, len, PF_N))
         return cudaErrorInvalidValue;
-    PfParams p;
-    p.Hq = q_heads;
-    p.Hkv = kv_heads;
-    p.len = len;
-    p.n_mtiles = (len + PF_M - 1) / PF_M;
-    p.scale_log2 = scale * 1.4426950408889634f;
-    p.out = static_cast<__nv_bfloat16 *>(out);
     const size_t smem = sizeof(PfSmem) + 1024;
     static bool attr = false;
     if (!attr) {
@@ -373,6 +345,13 @@ cudaError_t launch_prefill_attention(const void *q, const void *k, const void *v
         if (e != cudaSuccess) return e;
         attr = true;
     }
+    PfParams p;
+    p.Hq = q_heads;
+    p.Hkv = kv_heads;
+    p.len = len;
+    p.n_mtiles = (len + PF_M - 1) / PF_M;
+    p.scale_log2 = scale * 1.4426950408889634f;
+    p.out = static_cast<__nv_bfloat16 *>(out);
     prefill_attention_kernel<<<p.n_mtiles * q_heads, PF_THREADS, smem, s>>>(mq, mk, mv, p);
     return cudaGetLastError();
 }
