@@ -288,6 +288,20 @@ def run_baton(args, rank, world, local_rank):
         return out
 
     sh.baton_decode_layer = timed_layer
+    # splice (a5/a6/a7) K/V copies timed the same way: bytes = read + write of the rows
+    splice_ev = []
+    orig_ins = sh.baton_insert_many
+
+    def timed_insert(slots, ks, vs, lens, stream=None):
+        if not timing["on"]:
+            return orig_ins(slots, ks, vs, lens)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        orig_ins(slots, ks, vs, lens)
+        b.record()
+        splice_ev.append((a, b, 2 * sum(lens) * L * Hkv * D * 2 * 2))
+
+    sh.baton_insert_many = timed_insert
     for _ in range(W):
         eng.iteration()
     torch.cuda.synchronize()
@@ -296,8 +310,11 @@ def run_baton(args, rank, world, local_rank):
         eng.iteration()
     torch.cuda.synchronize()
     attn = [a.elapsed_time(b) for a, b in attn_ms]
+    splice_bytes = sum(n for _, _, n in splice_ev)
+    splice_s = sum(a.elapsed_time(b) for a, b, _ in splice_ev) / 1e3
     sh.baton_decode_layer = orig
-    del sh, orig, timed_layer
+    sh.baton_insert_many = orig_ins
+    del sh, orig, timed_layer, orig_ins, timed_insert
     release(eng)
     attn_time_s = sum(attn) / 1e3
     attn_launches = len(attn)
@@ -365,7 +382,8 @@ def run_baton(args, rank, world, local_rank):
                "d2h": counters["d2h"] / K_steps}
         release(eng)
 
-    return dict(ms=ms, tokens=tokens, attn_bytes=attn_bytes_total, attn_time_s=attn_time_s,
+    return dict(splice_bytes=splice_bytes, splice_s=splice_s, splice_calls=len(splice_ev),
+                ms=ms, tokens=tokens, attn_bytes=attn_bytes_total, attn_time_s=attn_time_s,
                 attn_launches=attn_launches, splice_rows=splice_rows, tau=tau, L=L,
                 n_launch=n_launch, clocks=clk, e2e=e2e, iters=K_steps,
                 live_slots=tokens / K_steps, live_rows=live_rows)
@@ -509,6 +527,11 @@ def main():
                          "avg_launch_us": 1e6 * r["attn_time_s"] / max(1, r["attn_launches"]),
                          "timing": "eager launches bracketed by CUDA events over the same K-step window",
                          "step_hbm_GBps": r["attn_bytes"] / (ms / 1e3) / 1e9},
+            "splice": {"calls": r["splice_calls"], "bytes": r["splice_bytes"],
+                       "GBps": (r["splice_bytes"] / r["splice_s"] / 1e9) if r["splice_s"] else None,
+                       "frac": (r["splice_bytes"] / r["splice_s"] / 1e9 / peak) if r["splice_s"] else None,
+                       "what": "baton_insert_many (batched KV embed + mask splice) in the window, "
+                               "algorithmic read+write bytes / event time"},
             "gpu_launches": r["n_launch"],
             "clocks": r["clocks"],
         }
