@@ -202,11 +202,14 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
     }
 
     // ============================ consumer warps ============================
-    const int qr = lane >> 2;            // fragment row (head) / B column
-    const int qc = (lane & 3) * 2;       // fragment column pair
-    uint32_t qa[8][2];                   // Q A-fragments (rows 0-7 real): a0 / a2 per k-step
-    float o[16][4];                      // O accumulator: 16 n-tiles of 8 dims (rows qr, qr+8)
-    float m = -INFINITY, l = 0.f;        // softmax state of head row qr
+    // Transposed formulation (keys and dims as the MMA's M so no row is padding):
+    //   S^T[16 keys x 8 heads]  = K[16 x 128] . Q^T            (8 MMAs per tile)
+    //   O^T[128 dims x 8 heads] += V^T[128 x 16 keys] . P^T     (8 MMAs per tile)
+    const int r4 = lane >> 2;            // fragment row group
+    const int c2 = (lane & 3) * 2;       // fragment column pair (heads c2, c2+1 in C)
+    uint32_t qb[8][2];                   // Q^T B-fragments: head r4, dims 16k + c2 (+8)
+    float o[8][4];                       // O^T: dims 16mt + r4 (+8) x heads c2, c2+1
+    float m[2], l[2];                    // softmax state of heads c2, c2+1
     int stage = 0;
     uint32_t phase = 0;
     int rb = 0;                          // merge buffer of the current item
@@ -216,73 +219,72 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
         const Desc d = st.desc;
         if (d.flags & F_END) break;
         if (d.flags & F_FIRST) {
-            const uint32_t *qw = reinterpret_cast<const uint32_t *>(st.q + qr * D);
+            const uint32_t *qw = reinterpret_cast<const uint32_t *>(st.q + r4 * D);
 #pragma unroll
-            for (int ks = 0; ks < 8; ++ks) {
-                qa[ks][0] = qw[(ks * 16 + qc) / 2];
-                qa[ks][1] = qw[(ks * 16 + 8 + qc) / 2];
+            for (int kk = 0; kk < 8; ++kk) {
+                qb[kk][0] = qw[(kk * 16 + c2) / 2];
+                qb[kk][1] = qw[(kk * 16 + 8 + c2) / 2];
             }
 #pragma unroll
-            for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-            m = -INFINITY;
-            l = 0.f;
+            for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+            m[0] = m[1] = -INFINITY;
+            l[0] = l[1] = 0.f;
         }
         const int base = warp * KPW;
         if (base < d.nrows) {
             const uint32_t ks_ = smem_u32(st.k), vs_ = smem_u32(st.v);
-            // ---- S = Q K^T for the warp's 16 keys (two n-tiles of 8 keys)
-            float s[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+            const int i4 = lane >> 3, r8 = lane & 7;
+            // ---- S^T = K Q^T: A = 16 key rows via ldmatrix (two accumulator chains)
+            float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
             {
-                const int i = lane >> 3, r = lane & 7;
-                const int key = base + (i >> 1) * 8 + r;
+                const int key = base + (i4 & 1) * 8 + r8;
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    uint32_t b0, b1, b2, b3;
-                    ldsm_x4(ks_ + swz(key, 2 * kk + (i & 1)), b0, b1, b2, b3);
-                    mma16816(s[0], qa[kk][0], 0u, qa[kk][1], 0u, b0, b1);
-                    mma16816(s[1], qa[kk][0], 0u, qa[kk][1], 0u, b2, b3);
+                for (int kk = 0; kk < 8; kk += 2) {
+                    uint32_t a0, a1, a2, a3, e0, e1, e2, e3;
+                    ldsm_x4(ks_ + swz(key, 2 * kk + (i4 >> 1)), a0, a1, a2, a3);
+                    ldsm_x4(ks_ + swz(key, 2 * kk + 2 + (i4 >> 1)), e0, e1, e2, e3);
+                    mma16816(sa, a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
+                    mma16816(sb, e0, e1, e2, e3, qb[kk + 1][0], qb[kk + 1][1]);
                 }
             }
-            // ---- mask + online softmax on head row qr (values s[nt][0..1])
-            bool any_invalid = false;
-            float mx = -INFINITY;
+            // keys of this thread: r4 (values 0,1) and r4 + 8 (values 2,3)
+            const int k0 = base + r4, k1 = base + r4 + 8;
+            bool ok0 = k0 < d.nrows, ok1 = k1 < d.nrows;
+            if (p.mask) {
+                ok0 = ok0 && st.mask[d.moff + (ok0 ? k0 : 0)] != 0;
+                ok1 = ok1 && st.mask[d.moff + (ok1 ? k1 : 0)] != 0;
+            }
+            float x[4];
+            x[0] = ok0 ? (sa[0] + sb[0]) * p.scale_log2 : -INFINITY;
+            x[1] = ok0 ? (sa[1] + sb[1]) * p.scale_log2 : -INFINITY;
+            x[2] = ok1 ? (sa[2] + sb[2]) * p.scale_log2 : -INFINITY;
+            x[3] = ok1 ? (sa[3] + sb[3]) * p.scale_log2 : -INFINITY;
+            // per-head (column) max over the warp's 16 keys: lanes with equal lane & 3
+            float mx0 = fmaxf(x[0], x[2]), mx1 = fmaxf(x[1], x[3]);
 #pragma unroll
-            for (int nt = 0; nt < 2; ++nt)
+            for (int o2 = 4; o2 < 32; o2 <<= 1) {
+                mx0 = fmaxf(mx0, __shfl_xor_sync(FULL_MASK, mx0, o2));
+                mx1 = fmaxf(mx1, __shfl_xor_sync(FULL_MASK, mx1, o2));
+            }
+            const float mn0 = fmaxf(m[0], mx0), mn1 = fmaxf(m[1], mx1);
+            const float rf0 = (mn0 == -INFINITY) ? 0.f : mn0, rf1 = (mn1 == -INFINITY) ? 0.f : mn1;
+            const float al0 = ex2(m[0] - rf0), al1 = ex2(m[1] - rf1);
+            // P.V multiplies bf16(p): sum the same rounded weights
+            const __nv_bfloat162 p01 = __floats2bfloat162_rn(ex2(x[0] - rf0), ex2(x[1] - rf1));  // key k0
+            const __nv_bfloat162 p23 = __floats2bfloat162_rn(ex2(x[2] - rf0), ex2(x[3] - rf1));  // key k1
+            l[0] = l[0] * al0 + __low2float(p01) + __low2float(p23);
+            l[1] = l[1] * al1 + __high2float(p01) + __high2float(p23);
+            m[0] = mn0;
+            m[1] = mn1;
 #pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int kt = base + nt * 8 + qc + e;
-                    bool ok = kt < d.nrows;
-                    if (p.mask) ok = ok && st.mask[d.moff + (ok ? kt : 0)] != 0;
-                    any_invalid |= !ok;
-                    const float x = ok ? s[nt][e] * p.scale_log2 : -INFINITY;
-                    s[nt][e] = x;
-                    mx = fmaxf(mx, x);
-                }
-            mx = fmaxf(mx, __shfl_xor_sync(FULL_MASK, mx, 1));
-            mx = fmaxf(mx, __shfl_xor_sync(FULL_MASK, mx, 2));
-            const float m_new = fmaxf(m, mx);
-            const float ref = (m_new == -INFINITY) ? 0.f : m_new;
-            const float alpha = ex2(m - ref);
-            float pr[2][2];
-            float ps = 0.f;
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    // P.V multiplies bf16(p): sum the same rounded weights
-                    const float pe = __bfloat162float(__float2bfloat16_rn(ex2(s[nt][e] - ref)));
-                    pr[nt][e] = pe;
-                    ps += pe;
-                }
-            l = l * alpha + ps;
-            m = m_new;
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                o[i][0] *= alpha;
-                o[i][1] *= alpha;
+            for (int i = 0; i < 8; ++i) {
+                o[i][0] *= al0;
+                o[i][1] *= al1;
+                o[i][2] *= al0;
+                o[i][3] *= al1;
             }
             // masked / out-of-range keys: their V rows may hold anything -> zero them
-            if (__any_sync(FULL_MASK, any_invalid)) {
+            if (__any_sync(FULL_MASK, !(ok0 && ok1))) {
                 for (int kr = 0; kr < KPW; ++kr) {
                     const int kt = base + kr;
                     bool ok = kt < d.nrows;
@@ -291,18 +293,25 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
                 }
                 __syncwarp();
             }
-            const uint32_t pa0 = pack_bf16(pr[0][0], pr[0][1]);
-            const uint32_t pa2 = pack_bf16(pr[1][0], pr[1][1]);
-            // ---- O += P V : B fragments of V via ldmatrix.trans
+            // ---- P^T B-fragment: thread needs P[keys c2, c2+1 (+8)][head r4].  The
+            // value P[k][n] sits in lane (k & 7) * 4 + n / 2, half n & 1, of p01 (k < 8)
+            // or p23 (k >= 8).
+            const uint32_t w01 = *reinterpret_cast<const uint32_t *>(&p01);
+            const uint32_t w23 = *reinterpret_cast<const uint32_t *>(&p23);
+            const int srcA = c2 * 4 + (r4 >> 1), srcB = (c2 + 1) * 4 + (r4 >> 1);
+            const uint32_t sh = (r4 & 1) ? 16 : 0;
+            const uint32_t x0 = __shfl_sync(FULL_MASK, w01, srcA), x1 = __shfl_sync(FULL_MASK, w01, srcB);
+            const uint32_t y0 = __shfl_sync(FULL_MASK, w23, srcA), y1 = __shfl_sync(FULL_MASK, w23, srcB);
+            const uint32_t pb0 = ((x0 >> sh) & 0xffffu) | (((x1 >> sh) & 0xffffu) << 16);
+            const uint32_t pb1 = ((y0 >> sh) & 0xffffu) | (((y1 >> sh) & 0xffffu) << 16);
+            // ---- O^T += V^T P^T: A = V^T (16 dims x 16 keys) via ldmatrix.trans
             {
-                const int i = lane >> 3, r = lane & 7;
-                const int key = base + (i & 1) * 8 + r;
+                const int key = base + (i4 >> 1) * 8 + r8;
 #pragma unroll
-                for (int dn = 0; dn < 8; ++dn) {
-                    uint32_t b0, b1, b2, b3;
-                    ldsm_x4_t(vs_ + swz(key, 2 * dn + (i >> 1)), b0, b1, b2, b3);
-                    mma16816(o[2 * dn], pa0, 0u, pa2, 0u, b0, b1);
-                    mma16816(o[2 * dn + 1], pa0, 0u, pa2, 0u, b2, b3);
+                for (int mt = 0; mt < 8; ++mt) {
+                    uint32_t a0, a1, a2, a3;
+                    ldsm_x4_t(vs_ + swz(key, 2 * mt + (i4 & 1)), a0, a1, a2, a3);
+                    mma16816(o[mt], a0, a1, a2, a3, pb0, pb1);
                 }
             }
         }
@@ -317,15 +326,24 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
             // ---- merge the 4 warp states (double-buffered smem: one barrier per item).
             // Multi-chunk queries leave an fp32 partial; decode_combine_kernel (next in
             // the stream, PDL) merges chunks in order -- no tickets, no waiting here.
-            float lsum = l;
-            lsum += __shfl_xor_sync(FULL_MASK, lsum, 1);
-            lsum += __shfl_xor_sync(FULL_MASK, lsum, 2);
+            float ls0 = l[0], ls1 = l[1];
 #pragma unroll
-            for (int i = 0; i < 16; ++i)
-                *reinterpret_cast<float2 *>(&sm.red_o[rb][warp][qr][i * 8 + qc]) = make_float2(o[i][0], o[i][1]);
-            if ((lane & 3) == 0) {
-                sm.red_m[rb][warp][qr] = m;
-                sm.red_l[rb][warp][qr] = lsum;
+            for (int o2 = 4; o2 < 32; o2 <<= 1) {
+                ls0 += __shfl_xor_sync(FULL_MASK, ls0, o2);
+                ls1 += __shfl_xor_sync(FULL_MASK, ls1, o2);
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                sm.red_o[rb][warp][c2][16 * i + r4] = o[i][0];
+                sm.red_o[rb][warp][c2 + 1][16 * i + r4] = o[i][1];
+                sm.red_o[rb][warp][c2][16 * i + r4 + 8] = o[i][2];
+                sm.red_o[rb][warp][c2 + 1][16 * i + r4 + 8] = o[i][3];
+            }
+            if (lane < 4) {
+                sm.red_m[rb][warp][c2] = m[0];
+                sm.red_m[rb][warp][c2 + 1] = m[1];
+                sm.red_l[rb][warp][c2] = ls0;
+                sm.red_l[rb][warp][c2 + 1] = ls1;
             }
             named_bar_sync(1, CW * 32);
             const int t = threadIdx.x;          // 128 threads: head = t >> 4, dims 8*(t&15)..+8

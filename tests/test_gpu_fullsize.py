@@ -91,3 +91,17 @@ def test_13b_churn_full_size():
     require_cuda()
     wl = config_workload("13b", n_queries=200)
     _run(wl, iters=4, sample_layers=[0, 39], n_sample_tokens=2, seed=3)
+
+
+def test_stress_shard_full_size_with_preemption():
+    """One GPU's shard of configs[4] (7B shape): active slots doubling 2 -> 32 and
+    25% of live queries stored (extract to an HBM stash) and re-inserted every 16
+    iterations.  Runs from iteration 0 through the first preemption rounds."""
+    require_cuda()
+    wl = config_workload("stress", gpus=8, n_queries=400)
+    wl.slots, wl.gpus, wl.active = 32, 1, 8
+    wl.control.resize = {24: 16}          # scale up mid-window (P:L147)
+    wl.iterations = -1
+    sim = Simulator(wl)
+    assert sum(len(sim.iteration().preempted) for _ in range(50)) >= 4
+    _run(wl, iters=50, sample_layers=[0, 31], n_sample_tokens=1, seed=4)
