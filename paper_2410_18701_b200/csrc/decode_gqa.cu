@@ -30,18 +30,19 @@ namespace {
 
 constexpr int D = 128;
 constexpr int GS = 8;                       // q heads per kv head
-constexpr int CW = 4;                       // consumer warps
-constexpr int KPW = 16;                     // keys per warp per tile
-constexpr int TILE = CW * KPW;              // 64
-constexpr int THREADS = (CW + 1) * 32;
-constexpr int HALF = TILE * 128;            // bytes of one 64-dim half of a tile (8 KB)
+constexpr int KPW = 16;                     // keys per consumer warp per tile
+// CW (consumer warps), STAGES and CTAs/SM are template parameters; a tile has
+// TILE = CW * KPW keys and its two 64-dim halves are HALF = TILE * 128 bytes each.
 constexpr int F_FIRST = 1, F_LAST = 2, F_END = 4;
 
 struct Desc {
     int32_t b, g, c, nrows, flags, moff, nchunks, wrow;
 };
 
+template <int CW>
 struct __align__(1024) Stage {
+    static constexpr int TILE = CW * KPW;
+    static constexpr int HALF = TILE * 128;
     uint8_t k[2 * HALF];
     uint8_t v[2 * HALF];
     __nv_bfloat16 q[GS * D];
@@ -49,9 +50,9 @@ struct __align__(1024) Stage {
     Desc desc;
 };
 
-template <int STAGES>
+template <int CW, int STAGES>
 struct Smem {
-    Stage st[STAGES];
+    Stage<CW> st[STAGES];
     uint64_t full[STAGES], empty[STAGES];
     WorkSched ws;
     alignas(16) float red_o[2][CW][GS][D + 8];     // +8: spread the 8 head rows over the banks
@@ -70,8 +71,8 @@ struct Params {
     float scale_log2;
 };
 
-BATON_DEV uint32_t swz(int row, int chunk) {   // byte offset of 16-B chunk (0..15) of a row
-    return (uint32_t)((chunk >> 3) * HALF + row * 128 + (((chunk & 7) ^ (row & 7)) << 4));
+BATON_DEV uint32_t swz(int row, int chunk, int half) {   // byte offset of 16-B chunk (0..15) of a row
+    return (uint32_t)((chunk >> 3) * half + row * 128 + (((chunk & 7) ^ (row & 7)) << 4));
 }
 BATON_DEV void ldsm_x4(uint32_t addr, uint32_t &r0, uint32_t &r1, uint32_t &r2, uint32_t &r3) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -104,14 +105,16 @@ BATON_DEV void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1, ui
         : "memory");
 }
 
-template <int STAGES, int MINB>
-__global__ void __launch_bounds__(THREADS, MINB)
+template <int CW, int STAGES, int MINB>
+__global__ void __launch_bounds__((CW + 1) * 32, MINB)
 decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
                   const Params p) {
     extern __shared__ uint8_t smem_raw[];
     // 1024-B alignment for the SWIZZLE_128B boxes; offsetting the __shared__ array
     // itself keeps the shared address space visible to the compiler (LDS, not LD)
-    Smem<STAGES> &sm = *reinterpret_cast<Smem<STAGES> *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+    constexpr int TILE = CW * KPW, HALF = TILE * 128, THREADS = (CW + 1) * 32;
+    Smem<CW, STAGES> &sm =
+        *reinterpret_cast<Smem<CW, STAGES> *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
@@ -153,7 +156,7 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
             for (int t = 0; t < ntiles; ++t) {
                 const int nr = min(TILE, rows - t * TILE);
                 mbar_wait(&sm.empty[stage], phase ^ 1);
-                Stage &st = sm.st[stage];
+                Stage<CW> &st = sm.st[stage];
                 uint32_t bytes = 4 * HALF;      // full boxes, OOB rows zero-filled
                 int moff = 0;
                 uint32_t mbytes = 0;
@@ -215,7 +218,7 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
     int rb = 0;                          // merge buffer of the current item
     while (true) {
         mbar_wait(&sm.full[stage], phase);
-        Stage &st = sm.st[stage];
+        Stage<CW> &st = sm.st[stage];
         const Desc d = st.desc;
         if (d.flags & F_END) break;
         if (d.flags & F_FIRST) {
@@ -241,8 +244,8 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
 #pragma unroll
                 for (int kk = 0; kk < 8; kk += 2) {
                     uint32_t a0, a1, a2, a3, e0, e1, e2, e3;
-                    ldsm_x4(ks_ + swz(key, 2 * kk + (i4 >> 1)), a0, a1, a2, a3);
-                    ldsm_x4(ks_ + swz(key, 2 * kk + 2 + (i4 >> 1)), e0, e1, e2, e3);
+                    ldsm_x4(ks_ + swz(key, 2 * kk + (i4 >> 1), HALF), a0, a1, a2, a3);
+                    ldsm_x4(ks_ + swz(key, 2 * kk + 2 + (i4 >> 1), HALF), e0, e1, e2, e3);
                     mma16816(sa, a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
                     mma16816(sb, e0, e1, e2, e3, qb[kk + 1][0], qb[kk + 1][1]);
                 }
@@ -289,7 +292,7 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
                     const int kt = base + kr;
                     bool ok = kt < d.nrows;
                     if (p.mask) ok = ok && st.mask[d.moff + (ok ? kt : 0)] != 0;
-                    if (!ok && lane < 16) *reinterpret_cast<uint4 *>(st.v + swz(kt, lane)) = make_uint4(0, 0, 0, 0);
+                    if (!ok && lane < 16) *reinterpret_cast<uint4 *>(st.v + swz(kt, lane, HALF)) = make_uint4(0, 0, 0, 0);
                 }
                 __syncwarp();
             }
@@ -310,7 +313,7 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
 #pragma unroll
                 for (int mt = 0; mt < 8; ++mt) {
                     uint32_t a0, a1, a2, a3;
-                    ldsm_x4_t(vs_ + swz(key, 2 * mt + (i4 & 1)), a0, a1, a2, a3);
+                    ldsm_x4_t(vs_ + swz(key, 2 * mt + (i4 & 1), HALF), a0, a1, a2, a3);
                     mma16816(o[mt], a0, a1, a2, a3, pb0, pb1);
                 }
             }
@@ -346,8 +349,9 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
                 sm.red_l[rb][warp][c2 + 1] = ls1;
             }
             named_bar_sync(1, CW * 32);
-            const int t = threadIdx.x;          // 128 threads: head = t >> 4, dims 8*(t&15)..+8
-            const int hh = t >> 4, d0 = (t & 15) * 8;
+          // (head, 8-dim block) pairs, CW*32 threads at a time
+          for (int idx = threadIdx.x; idx < GS * (D / 8); idx += CW * 32) {
+            const int hh = idx >> 4, d0 = (idx & 15) * 8;
             float M = -INFINITY;
 #pragma unroll
             for (int w2 = 0; w2 < CW; ++w2) M = fmaxf(M, sm.red_m[rb][w2][hh]);
@@ -368,7 +372,6 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
                 Ot[6] = fmaf(f, b4.z, Ot[6]);
                 Ot[7] = fmaf(f, b4.w, Ot[7]);
             }
-            rb ^= 1;
             const int h = d.g * GS + hh;
             const size_t bh = (size_t)d.b * p.Hq + h;
             if (d.nchunks == 1) {
@@ -383,11 +386,13 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
                 float *pp = p.partial + (bh * p.max_chunks + d.c) * (D + PREC_PAD);
                 *reinterpret_cast<float4 *>(pp + d0) = make_float4(Ot[0], Ot[1], Ot[2], Ot[3]);
                 *reinterpret_cast<float4 *>(pp + d0 + 4) = make_float4(Ot[4], Ot[5], Ot[6], Ot[7]);
-                if ((t & 15) == 0) {
+                if ((idx & 15) == 0) {
                     pp[D] = M;
                     pp[D + 1] = Lt;
                 }
             }
+          }
+          rb ^= 1;
         }
     }
 }
@@ -435,18 +440,19 @@ bool gqa_supported(int q_heads, int kv_heads, int head_dim) {
     return head_dim == D && kv_heads > 0 && q_heads == GS * kv_heads;
 }
 
-template <int STAGES, int MINB>
+template <int CW, int STAGES, int MINB>
 cudaError_t launch_gqa_v(const DecodeArgs &a, cudaStream_t s) {
+    constexpr int TILE = CW * KPW, THREADS = (CW + 1) * 32;
     static int num_sms = 0;
     if (!num_sms) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    const size_t smem = sizeof(Smem<STAGES>) + 1024;
+    const size_t smem = sizeof(Smem<CW, STAGES>) + 1024;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(decode_gqa_kernel<STAGES, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(decode_gqa_kernel<CW, STAGES, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
@@ -480,7 +486,7 @@ cudaError_t launch_gqa_v(const DecodeArgs &a, cudaStream_t s) {
                                          a.lens, a.slots, a.kv_heads, a.head_dim, a.max_ctx, s);
         if (e != cudaSuccess) return e;
     }
-    cudaError_t e = launch_pdl(decode_gqa_kernel<STAGES, MINB>, dim3(MINB * num_sms), dim3(THREADS), smem, s, km, vm, p);
+    cudaError_t e = launch_pdl(decode_gqa_kernel<CW, STAGES, MINB>, dim3(MINB * num_sms), dim3(THREADS), smem, s, km, vm, p);
     if (e != cudaSuccess) return e;
     const int pairs = a.slots * a.q_heads;
     return launch_pdl(decode_combine_kernel, dim3((pairs + 3) / 4), dim3(128), 0, s, a.lens,
@@ -494,8 +500,13 @@ cudaError_t launch_decode_gqa(const DecodeArgs &a, cudaStream_t s) {
         const char *e = getenv("BATON_GQA_VARIANT");
         v = e ? atoi(e) : 0;
     }
-    if (v == 1) return launch_gqa_v<2, 2>(a, s);
-    return launch_gqa_v<4, 1>(a, s);
+    switch (v) {
+        case 1: return launch_gqa_v<4, 2, 2>(a, s);
+        case 2: return launch_gqa_v<2, 2, 3>(a, s);
+        case 3: return launch_gqa_v<2, 3, 2>(a, s);
+        case 4: return launch_gqa_v<1, 4, 4>(a, s);
+        default: return launch_gqa_v<4, 4, 1>(a, s);
+    }
 }
 
 }  // namespace baton
