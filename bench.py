@@ -330,38 +330,54 @@ def run_baton(args, rank, world, local_rank):
         pref.clear()
         gc.collect()
         torch.cuda.empty_cache()
-        qd = torch.empty((L, B, Hq, D), dtype=torch.bfloat16, device=dev)
-        kd = torch.empty((L, B, Hkv, D), dtype=torch.bfloat16, device=dev)
-        vd = torch.empty_like(kd)
+        # double-buffered device staging, filled by a copy stream one step ahead so
+        # the PCIe transfer of step i+1 overlaps the decode of step i
+        sets = [tuple(torch.empty(shp, dtype=torch.bfloat16, device=dev)
+                      for shp in ((L, B, Hq, D), (L, B, Hkv, D), (L, B, Hkv, D))) for _ in range(2)]
+        ready = [torch.cuda.Event() for _ in range(2)]
+        free = [torch.cuda.Event() for _ in range(2)]
+        copy_stream = torch.cuda.Stream()
         res_h = torch.empty((B, Hq, D), dtype=torch.bfloat16).pin_memory()
         counters = {"h2d": 0, "d2h": 0}
 
+        def h2d(i):
+            slot = i % 2
+            with torch.cuda.stream(copy_stream):
+                copy_stream.wait_event(free[slot])          # the decode that last read it
+                for dst, src in zip(sets[slot], (q_h[i], k_h[i], v_h[i])):
+                    dst.copy_(src, non_blocking=True)
+                    counters["h2d"] += src.numel() * 2
+                ready[slot].record(copy_stream)
+
         def token_host(t, dec):
-            i = t - t_base
-            qd.copy_(q_h[i], non_blocking=True)
-            kd.copy_(k_h[i], non_blocking=True)
-            vd.copy_(v_h[i], non_blocking=True)
-            counters["h2d"] += (q_h[i].numel() + k_h[i].numel() + v_h[i].numel()) * 2
-            return qd, kd, vd
+            slot = (t - t_base) % 2
+            torch.cuda.current_stream().wait_event(ready[slot])
+            return sets[slot]
 
         def prefill_host(qid, n):
             a, b = pref_h[qid]
             counters["h2d"] += (a.numel() + b.numel()) * 2
             return a.to(dev, non_blocking=True), b.to(dev, non_blocking=True)
 
-        def fetch_result(eng2, warm):
+        def step(eng2, i, warm):
+            if i + 1 < n_iters:
+                h2d(i + 1)
+            st_ = eng2.iteration()
+            free[i % 2].record()
             res_h.copy_(eng2.out[L - 1], non_blocking=True)   # the step's result to the host
             if not warm:
                 counters["d2h"] += res_h.numel() * 2
+            return st_
 
         eng = make_engine(token_host, prefill_host, use_graph=True)
+        for st_set in sets:
+            eng.register_staging(*st_set)
         warm_start(eng)
-        counters["h2d"] = 0
-        ms2, st2 = None, None
-        # warm-up iterations also move bytes; count only the timed ones
-        for _ in range(W):
-            eng.iteration()
-            fetch_result(eng, True)
+        for ev in free:
+            ev.record()
+        h2d(0)
+        for i in range(W):
+            step(eng, i, True)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -369,10 +385,7 @@ def run_baton(args, rank, world, local_rank):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        st2 = []
-        for _ in range(K_steps):
-            st2.append(eng.iteration())
-            fetch_result(eng, False)
+        st2 = [step(eng, W + i, False) for i in range(K_steps)]
         e1.record()
         torch.cuda.synchronize()
         if world > 1:

@@ -29,11 +29,16 @@ struct baton_state {
     int max_chunks = 0;
     size_t layer_elems = 0;   // elements of one layer of the K (or V) cache
     // baton_decode_step: the captured decode iteration, keyed by its I/O pointers
+    // (a few I/O pointer sets, e.g. double-buffered staging; LRU replacement)
+    static constexpr int kGraphs = 4;
     cudaStream_t cap_stream = nullptr;
-    cudaGraphExec_t step_exec = nullptr;
-    const void *step_io[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaGraphExec_t step_exec[kGraphs] = {nullptr, nullptr, nullptr, nullptr};
+    const void *step_io[kGraphs][4] = {};
+    unsigned long long step_used[kGraphs] = {0, 0, 0, 0};
+    unsigned long long step_clock = 0;
     ~baton_state() {
-        if (step_exec) cudaGraphExecDestroy(step_exec);
+        for (auto &e : step_exec)
+            if (e) cudaGraphExecDestroy(e);
         if (cap_stream) cudaStreamDestroy(cap_stream);
     }
 };
@@ -241,12 +246,18 @@ int baton_decode_step(baton_state *st, const void *q, const void *k_new, const v
     const size_t qstride = (size_t)s.slots * s.q_heads * s.head_dim;
     const size_t kstride = (size_t)s.slots * s.kv_heads * s.head_dim;
     const void *io[4] = {q, k_new, v_new, out};
-    if (!st->step_exec || std::memcmp(io, st->step_io, sizeof(io)) != 0) {
-        // (re)capture: mask update + every layer's fused append/attention, chained
-        // with programmatic dependent launch; the graph reads only device state
-        if (st->step_exec) {
-            cudaGraphExecDestroy(st->step_exec);
-            st->step_exec = nullptr;
+    int slot = -1;
+    for (int i = 0; i < baton_state::kGraphs; ++i)
+        if (st->step_exec[i] && std::memcmp(io, st->step_io[i], sizeof(io)) == 0) slot = i;
+    if (slot < 0) {
+        // capture: mask update + every layer's fused append/attention, chained with
+        // programmatic dependent launch; the graph reads only device state
+        slot = 0;
+        for (int i = 1; i < baton_state::kGraphs; ++i)
+            if (st->step_used[i] < st->step_used[slot]) slot = i;
+        if (st->step_exec[slot]) {
+            cudaGraphExecDestroy(st->step_exec[slot]);
+            st->step_exec[slot] = nullptr;
         }
         cudaError_t e = cudaSuccess;
         if (!st->cap_stream) e = cudaStreamCreateWithFlags(&st->cap_stream, cudaStreamNonBlocking);
@@ -267,15 +278,16 @@ int baton_decode_step(baton_state *st, const void *q, const void *k_new, const v
         cudaGraph_t g = nullptr;
         const cudaError_t e2 = cudaStreamEndCapture(st->cap_stream, &g);
         if (e == cudaSuccess) e = e2;
-        if (e == cudaSuccess) e = cudaGraphInstantiate(&st->step_exec, g, 0);
+        if (e == cudaSuccess) e = cudaGraphInstantiate(&st->step_exec[slot], g, 0);
         if (g) cudaGraphDestroy(g);
         if (e != cudaSuccess) {
-            st->step_exec = nullptr;
+            st->step_exec[slot] = nullptr;
             return cuda_status(e);
         }
-        std::memcpy(st->step_io, io, sizeof(io));
+        std::memcpy(st->step_io[slot], io, sizeof(io));
     }
-    int r = cuda_status(cudaGraphLaunch(st->step_exec, as_stream(stream)));
+    st->step_used[slot] = ++st->step_clock;
+    int r = cuda_status(cudaGraphLaunch(st->step_exec[slot], as_stream(stream)));
     if (r) return r;
     st->S += 1;   // host mirror of a1
     for (int b = 0; b < s.slots; ++b)
