@@ -31,6 +31,7 @@ KIND_Q, KIND_K, KIND_V = 0, 1, 2
 class StepStats:
     t: int
     decoded: int = 0
+    idle: int = 0               # decodes of already-finished queries (run-to-completion baseline)
     inserted: int = 0
     removed: int = 0
     stored: int = 0
@@ -44,13 +45,13 @@ class StepStats:
 class Engine:
     def __init__(self, wl, rank=0, world=1, device=None, group=None, keep_outputs=False,
                  keep_layers=None, token_source=None, prefill_source=None, use_graph=True,
-                 stash_host=False):
+                 stash_host=False, policy="baton"):
         self.wl = wl
         self.rank = rank
         self.world = world
         self.group = group
         self.device = torch.device(device or "cuda")
-        self.planner = Planner(wl, world)
+        self.planner = Planner(wl, world, policy=policy)
         self.B = self.planner.per_rank
         # libbaton requires max_ctx % 16 == 0 (16-B aligned mask rows for the bulk
         # copies); a larger capacity changes no result (C24 caps l_q + A anyway)
@@ -122,6 +123,7 @@ class Engine:
         pl = self.planner
         dec = [(pl.local(g), q, p) for g, q, p in pl.decode_plan() if pl.rank_of(g) == self.rank]
         stats.decoded = len(dec)
+        stats.idle = sum(1 for b, q, p in dec if p >= pl.meta[q].l_q + pl.meta[q].A)
         stats.live_rows = sum(p + 1 for _, _, p in dec)
         if self.token_source is not None:
             q, k, v = self.token_source(pl.t, dec)

@@ -39,7 +39,15 @@ class Decisions:
 
 
 class Planner:
-    def __init__(self, wl, world=1):
+    def __init__(self, wl, world=1, policy="baton"):
+        """policy "baton": relay race (remove on completion, insert at once);
+        "rtc": the paper's run-to-completion Benchmark -- a finished query
+        keeps its slot and keeps decoding (idle EOS tokens) until every query of
+        the batch has finished; only an empty batch is refilled (NEXT-4)."""
+        if policy not in ("baton", "rtc"):
+            raise ValueError(policy)
+        self.policy = policy
+        self.drained = set()                                  # rtc: finished but resident
         self.wl = wl
         self.world = world
         if wl.slots % world:
@@ -76,6 +84,10 @@ class Planner:
         """Slots that decode this iteration and the position each one handles."""
         return [(g, q, self.length[g]) for g, q in self.live()]
 
+    def idle_decodes(self, decode):
+        """Decode entries of queries that already produced all their tokens (rtc)."""
+        return sum(1 for g, q, pos in decode if pos >= self.meta[q].l_q + self.meta[q].A)
+
     def local_completion_flags(self, rank):
         """Per local slot: 1 if the query there produced its last token in the
         decode just executed (the engine all-gathers these)."""
@@ -106,6 +118,13 @@ class Planner:
                     self.done_tokens[q] >= self.meta[q].A)
                 if done:
                     d.finished.append((g, q))
+            if self.policy == "rtc":
+                self.drained.update(q for _, q in d.finished)
+                if any(q not in self.drained for _, q in self.live()):
+                    d.finished = []                           # the batch runs on
+                else:
+                    d.finished = list(self.live())
+                    self.drained.clear()
             for g, _ in d.finished:
                 self.occupant[g] = -1
                 self.length[g] = 0
@@ -174,6 +193,8 @@ class Planner:
             self.next_arrival += 1
 
     def _fill(self, d):
+        if self.policy == "rtc" and self.live():
+            return                                            # batch still running
         while self.queue:
             free = [r * self.per_rank + b for r in range(self.world) for b in range(self.active)
                     if self.occupant[r * self.per_rank + b] < 0]

@@ -1,0 +1,68 @@
+"""NEXT-4: Baton's relay race vs the paper's run-to-completion Benchmark on B200.
+
+    python scripts/policy_compare.py [--dataset d2|d1] [--batches 2,4,6,8,10]
+
+Runs the whole synthetic dataset through the same libbaton kernels under both
+policies (Planner policy "baton" vs "rtc": a finished query keeps decoding idle
+EOS tokens until its whole batch is done) and reports, per batch size,
+the completion time of the dataset (device time of all iterations) and useful
+decode tokens/s -- the B200 counterpart of Tables 2/3, with the
+paper's datasets replaced by the length mixes of P:L212 (model GEMMs excluded).
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from baton_inputs import Workload                                  # noqa: E402
+from baton_inputs.workload import _mix_queries, CLASSES_7B, CLASSES_D2  # noqa: E402
+from paper_2410_18701_b200.engine import Engine                    # noqa: E402
+
+
+def dataset(name, batch):
+    rng = np.random.default_rng(2410)
+    if name == "d2":     # 30 short/short queries, dozens to 200 words
+        qs = _mix_queries(rng, 30, 30, 0.0, CLASSES_D2, 4096, all_at_zero=True)
+    else:                # 120 queries, 1:1:2 long-in/short-out, short-in/long-out, short/short
+        qs = _mix_queries(rng, 120, 120, 0.0, CLASSES_7B, 2048, all_at_zero=True)
+    # run-to-completion grows finished queries until the batch ends: 4096 capacity
+    return Workload(name, qs, layers=32, q_heads=32, kv_heads=32, head_dim=128, slots=batch,
+                    max_ctx=4096)
+
+
+def run(name, batch, policy):
+    wl = dataset(name, batch)
+    eng = Engine(wl, policy=policy, use_graph=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    st = eng.run()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    useful = sum(s.decoded - s.idle for s in st)
+    assert useful == wl.decode_tokens()
+    return {"iterations": len(st), "ms": ms, "useful_tokens": useful,
+            "idle_tokens": sum(s.idle for s in st), "useful_tok_per_s": useful / (ms / 1e3)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--dataset", default="d2")
+    ap.add_argument("--batches", default="2,4,6,8,10")
+    args = ap.parse_args()
+    for b in [int(x) for x in args.batches.split(",")]:
+        base = run(args.dataset, b, "rtc")
+        bat = run(args.dataset, b, "baton")
+        print(json.dumps({"dataset": args.dataset, "batch": b, "benchmark_rtc": base, "baton": bat,
+                          "completion_speedup": base["ms"] / bat["ms"]}), flush=True)
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()

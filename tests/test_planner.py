@@ -65,3 +65,32 @@ def test_flags_path_equals_local_bookkeeping():
         flags = sum((b.local_completion_flags(r) for r in range(4)), []) if b.t > 0 else None
         da, db = a.plan(), b.plan(flags)
         assert da == db
+
+
+def test_run_to_completion_policy():
+    """NEXT-4 baseline: no slot is refilled before the whole batch has
+    finished; finished queries keep decoding (idle tokens) until then."""
+    from baton_inputs import Workload, Query
+    A = [10, 2, 3, 9, 2, 4, 8, 1, 2]
+    qs = [Query(i, 0, 5 + i, A[i]) for i in range(9)]
+    wl = Workload("rtc", qs, layers=1, q_heads=2, kv_heads=2, head_dim=16, slots=3, max_ctx=64)
+    pl = Planner(wl, 1, policy="rtc")
+    useful = idle = 0
+    batches = []
+    while not pl.finished_all():
+        d = pl.plan()
+        idle += pl.idle_decodes(d.decode)
+        useful += len(d.decode) - pl.idle_decodes(d.decode)
+        if d.finished:                      # the whole batch leaves at once
+            assert len(d.finished) == 3 or not pl.queue
+        if d.inserts:
+            live = sorted(q for q in pl.occupant if q >= 0)
+            assert live == sorted(i[1] for i in d.inserts)     # only into an empty batch
+            batches.append([i[1] for i in d.inserts])
+    assert batches == [[0, 1, 2], [3, 4, 5], [6, 7, 8]]
+    assert useful == sum(A)
+    assert idle == sum(max(A[j] for j in b) * len(b) - sum(A[j] for j in b) for b in batches)
+    base = Planner(wl, 1)
+    while not base.finished_all():
+        base.plan()
+    assert base.t < pl.t            # the relay race finishes the same work sooner
