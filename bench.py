@@ -137,7 +137,7 @@ def window_plan(planner, n_iters, rank):
         decodes.append(dec)
         for g, q, n, home in d.inserts:
             if p.rank_of(g) == rank and home is None:
-                inserts.append((q, n))
+                inserts.append((q, n, d.t))
     return decodes, inserts
 
 
@@ -209,7 +209,7 @@ def run_baton(args, rank, world, local_rank):
         baton_keygen_tokens(k_all[i], dq, dp, L, B, Hkv, D, 1, 0, wl.seed, wl.scales[1])
         baton_keygen_tokens(v_all[i], dq, dp, L, B, Hkv, D, 2, 0, wl.seed, wl.scales[2])
     pref = {}
-    for q, n in fresh:
+    for q, n, _ in fresh:
         Kp = torch.empty((L, Hkv, n, D), dtype=torch.bfloat16, device=dev)
         Vp = torch.empty_like(Kp)
         baton_keygen_history(Kp, L, Hkv, D, q, 0, n, 1, wl.seed, wl.scales[1])
@@ -354,14 +354,38 @@ def run_baton(args, rank, world, local_rank):
             torch.cuda.current_stream().wait_event(ready[slot])
             return sets[slot]
 
+        # prefilled K/V of the queries inserted at window step i arrive on the copy
+        # stream two steps ahead (inserts are known from the window plan)
+        ins_at = {}
+        for q, n, t_ins in fresh:
+            ins_at.setdefault(t_ins - t_base, []).append(q)
+        pref_dev = {}
+
+        def prefetch_inserts(i):
+            for q in ins_at.get(i, []):
+                a, b = pref_h[q]
+                with torch.cuda.stream(copy_stream):
+                    da, db = a.to(dev, non_blocking=True), b.to(dev, non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(copy_stream)
+                counters["h2d"] += (a.numel() + b.numel()) * 2
+                pref_dev[q] = (da, db, ev)
+
         def prefill_host(qid, n):
-            a, b = pref_h[qid]
-            counters["h2d"] += (a.numel() + b.numel()) * 2
-            return a.to(dev, non_blocking=True), b.to(dev, non_blocking=True)
+            if qid not in pref_dev:          # not prefetched (should not happen): copy now
+                a, b = pref_h[qid]
+                counters["h2d"] += (a.numel() + b.numel()) * 2
+                return a.to(dev, non_blocking=True), b.to(dev, non_blocking=True)
+            da, db, ev = pref_dev.pop(qid)
+            torch.cuda.current_stream().wait_event(ev)
+            da.record_stream(torch.cuda.current_stream())
+            db.record_stream(torch.cuda.current_stream())
+            return da, db
 
         def step(eng2, i, warm):
             if i + 1 < n_iters:
                 h2d(i + 1)
+            prefetch_inserts(i + 2)
             st_ = eng2.iteration()
             free[i % 2].record()
             res_h.copy_(eng2.out[L - 1], non_blocking=True)   # the step's result to the host
@@ -376,6 +400,8 @@ def run_baton(args, rank, world, local_rank):
         for ev in free:
             ev.record()
         h2d(0)
+        prefetch_inserts(0)
+        prefetch_inserts(1)
         for i in range(W):
             step(eng, i, True)
         if world > 1:
