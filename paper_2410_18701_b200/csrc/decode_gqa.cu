@@ -505,6 +505,7 @@ cudaError_t launch_decode_gqa(const DecodeArgs &a, cudaStream_t s) {
         case 2: return launch_gqa_v<2, 2, 3>(a, s);
         case 3: return launch_gqa_v<2, 3, 2>(a, s);
         case 4: return launch_gqa_v<1, 4, 4>(a, s);
+        case 5: return launch_gqa_v<4, 5, 1>(a, s);
         default: return launch_gqa_v<4, 4, 1>(a, s);
     }
 }
