@@ -28,6 +28,7 @@ struct baton_state {
     float *partial = nullptr;
     int max_chunks = 0;
     size_t layer_elems = 0;   // elements of one layer of the K (or V) cache
+    bool prev_decode = false; // the shard's last launch was a decode kernel (DecodeArgs::early)
     // baton_decode_step: the captured decode iteration, keyed by its I/O pointers
     // (a few I/O pointer sets, e.g. double-buffered staging; LRU replacement)
     static constexpr int kGraphs = 4;
@@ -151,6 +152,7 @@ int baton_query(const baton_state *st, int32_t *S, int32_t *pad_start, int32_t *
 
 // ---------------------------------------------------------------- a1
 int baton_mask_update(baton_state *st, void *stream) {
+    if (st) st->prev_decode = false;
     if (!st) return BATON_E_INVALID;
     if (st->S + 1 > st->sh.max_ctx) return BATON_E_CAPACITY;
     int r = cuda_status(launch_mask_update(st->cfg.mask, st->d_S, st->d_lens, st->sh.slots,
@@ -164,6 +166,7 @@ int baton_mask_update(baton_state *st, void *stream) {
 
 // ---------------------------------------------------------------- a2
 int baton_append_kv(baton_state *st, int layer, const void *k_new, const void *v_new, void *stream) {
+    if (st) st->prev_decode = false;
     if (!st || !k_new || !v_new || layer < 0 || layer >= st->sh.layers) return BATON_E_INVALID;
     return cuda_status(launch_append_kv(layer_ptr(st->cfg.k_cache, st, layer),
                                         layer_ptr(st->cfg.v_cache, st, layer), k_new, v_new,
@@ -203,7 +206,7 @@ int baton_decode_attention(const void *q, const void *k, const void *v, const ui
 
 namespace {
 DecodeArgs layer_args(baton_state *st, int layer, const void *q, const void *k_new, const void *v_new,
-                      void *out) {
+                      void *out, bool early) {
     const baton_shape &s = st->sh;
     DecodeArgs a;
     a.q = q;
@@ -225,6 +228,7 @@ DecodeArgs layer_args(baton_state *st, int layer, const void *q, const void *k_n
     a.max_ctx = s.max_ctx;
     a.max_chunks = st->max_chunks;
     a.scale = 1.0f / sqrtf((float)s.head_dim);
+    a.early = early;
     return a;
 }
 }  // namespace
@@ -234,12 +238,15 @@ int baton_decode_layer(baton_state *st, int layer, const void *q, const void *k_
     if (!st || !q || !out || layer < 0 || layer >= st->sh.layers) return BATON_E_INVALID;
     if ((k_new == nullptr) != (v_new == nullptr)) return BATON_E_INVALID;
     // a2 fused into a3: one launch streams the cache and embeds the new token
-    return cuda_status(launch_decode_attention(layer_args(st, layer, q, k_new, v_new, out),
-                                               as_stream(stream)));
+    const int r = cuda_status(launch_decode_attention(
+        layer_args(st, layer, q, k_new, v_new, out, st->prev_decode), as_stream(stream)));
+    st->prev_decode = r == BATON_OK;
+    return r;
 }
 
 int baton_decode_step(baton_state *st, const void *q, const void *k_new, const void *v_new,
                       void *out, void *stream) {
+    if (st) st->prev_decode = false;
     if (!st || !q || !k_new || !v_new || !out) return BATON_E_INVALID;
     if (st->S + 1 > st->sh.max_ctx) return BATON_E_CAPACITY;
     const baton_shape &s = st->sh;
@@ -262,7 +269,7 @@ int baton_decode_step(baton_state *st, const void *q, const void *k_new, const v
         cudaError_t e = cudaSuccess;
         if (!st->cap_stream) e = cudaStreamCreateWithFlags(&st->cap_stream, cudaStreamNonBlocking);
         if (e != cudaSuccess) return cuda_status(e);
-        DecodeArgs probe = layer_args(st, 0, q, k_new, v_new, out);
+        DecodeArgs probe = layer_args(st, 0, q, k_new, v_new, out, false);
         probe.dry = true;   // kernel attributes must be set outside the capture
         if ((e = launch_decode_attention(probe, st->cap_stream)) != cudaSuccess) return cuda_status(e);
         if ((e = cudaStreamBeginCapture(st->cap_stream, cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
@@ -273,7 +280,8 @@ int baton_decode_step(baton_state *st, const void *q, const void *k_new, const v
             const __nv_bfloat16 *kl = static_cast<const __nv_bfloat16 *>(k_new) + l * kstride;
             const __nv_bfloat16 *vl = static_cast<const __nv_bfloat16 *>(v_new) + l * kstride;
             __nv_bfloat16 *ol = static_cast<__nv_bfloat16 *>(out) + l * qstride;
-            e = launch_decode_attention(layer_args(st, l, ql, kl, vl, ol), st->cap_stream);
+            // layer 0 follows the mask update (writes lens): no early prefetch
+            e = launch_decode_attention(layer_args(st, l, ql, kl, vl, ol, l > 0), st->cap_stream);
         }
         cudaGraph_t g = nullptr;
         const cudaError_t e2 = cudaStreamEndCapture(st->cap_stream, &g);
@@ -297,6 +305,7 @@ int baton_decode_step(baton_state *st, const void *q, const void *k_new, const v
 
 // ---------------------------------------------------------------- a4
 int baton_remove(baton_state *st, const int32_t *slots, int n, int32_t *released, void *stream) {
+    if (st) st->prev_decode = false;
     if (!st || n < 0 || (n > 0 && !slots)) return BATON_E_INVALID;
     const int B = st->sh.slots;
     std::vector<char> seen(B, 0);
@@ -332,6 +341,7 @@ int baton_remove(baton_state *st, const int32_t *slots, int n, int32_t *released
 // ---------------------------------------------------------------- a5
 int baton_insert_many(baton_state *st, int n, const int32_t *slots, const void *const *k_pref,
                       const void *const *v_pref, const int32_t *lens, void *stream) {
+    if (st) st->prev_decode = false;
     if (!st || n < 0) return BATON_E_INVALID;
     if (n == 0) return BATON_OK;
     if (!slots || !k_pref || !v_pref || !lens) return BATON_E_INVALID;
@@ -397,6 +407,7 @@ int baton_insert(baton_state *st, int slot, const void *k_pref, const void *v_pr
 
 // ---------------------------------------------------------------- a6
 int baton_extract(baton_state *st, int slot, void *k_out, void *v_out, void *stream) {
+    if (st) st->prev_decode = false;
     if (!st || !k_out || !v_out) return BATON_E_INVALID;
     const baton_shape &s = st->sh;
     if (slot < 0 || slot >= s.slots) return BATON_E_INVALID;
@@ -420,6 +431,7 @@ int baton_extract(baton_state *st, int slot, void *k_out, void *v_out, void *str
 
 // ---------------------------------------------------------------- a7
 int baton_compact(baton_state *st, int n_active, int32_t *old_to_new, void *stream) {
+    if (st) st->prev_decode = false;
     if (!st) return BATON_E_INVALID;
     const baton_shape &s = st->sh;
     if (n_active < 1 || n_active > s.slots) return BATON_E_INVALID;

@@ -65,6 +65,7 @@ struct Params {
     int32_t *tickets;
     int B, Hq, Hkv, max_ctx, max_chunks;
     float scale_log2;
+    bool early;                              // prefetch before griddepcontrol.wait
 };
 
 template <int D, int CWARPS, int STAGES>
@@ -100,18 +101,19 @@ __global__ void __launch_bounds__((CWARPS + 1) * 32, MINB) decode_attention_kern
         mbar_init(&sm.part_bar, CWARPS * 32);
         fence_mbar_init();
     }
-    // PDL: everything above overlapped the previous kernel's tail; from here on we
-    // read lens/pad/mask/cache written by earlier kernels.
-    griddep_wait();
-    griddep_launch_dependents();
-    // Empty slots produce a zero output row (C6).
-    for (int b = blockIdx.x; b < p.B; b += gridDim.x) {
-        if (p.lens[b] <= 0) {
-            uint4 *o = reinterpret_cast<uint4 *>(p.out + (size_t)b * p.Hq * D);
-            for (int i = threadIdx.x; i < p.Hq * D / 8; i += THREADS) o[i] = make_uint4(0, 0, 0, 0);
-        }
-    }
     __syncthreads();
+    // PDL.  Without p.early everything below reads lens/pad/mask/cache only after
+    // the previous kernel completed.  With p.early (the host saw that the previous
+    // launch was a decode kernel, which writes none of lens/pad/mask and no cache
+    // row but lens-1) the producer builds the work list and streams the first ring
+    // of K/V tiles of a statically assigned first item BEFORE the wait, overlapping
+    // the previous layer's tail; q, the appended row and every write wait for it.
+    // Every thread waits before it triggers, so when any kernel starts, all
+    // launches two or more back in the stream have completed.
+    if (!p.early) {
+        griddep_wait();
+        griddep_launch_dependents();
+    }
 
     if (warp == CWARPS) {
         // ============================ producer warp ============================
@@ -122,9 +124,21 @@ __global__ void __launch_bounds__((CWARPS + 1) * 32, MINB) decode_attention_kern
         int stage = 0;
         uint32_t phase = 0;
         int b = 0;
-        int w = sched_next(p.counters);
+        bool waited = !p.early;
+        const __nv_bfloat16 *late_q = nullptr;   // q of a tile issued before the wait
+        int late_stage = 0, issued = 0;
+        auto flush = [&]() {
+            griddep_wait();
+            griddep_launch_dependents();
+            waited = true;
+            if (late_q) bulk_g2s(sm.st[late_stage].q, late_q, D * 2, &sm.full[late_stage]);
+            late_q = nullptr;
+        };
+        // items [0, gridDim.x) are static (CTA i takes item i: no counter before the
+        // wait), the rest are handed out by the dynamic counter
+        int w = blockIdx.x;
+        int w_next = waited ? (int)gridDim.x + sched_next(p.counters) : -1;
         while (w < total) {
-            const int w_next = sched_next(p.counters);   // prefetch: latency hidden by this item
             int c, h;
             sched_item(sm.ws, w, p.Hq, b, c, h);
             const int L = sm.ws.lens[b];
@@ -142,6 +156,8 @@ __global__ void __launch_bounds__((CWARPS + 1) * 32, MINB) decode_attention_kern
             for (int t = 0; t < ntiles; ++t) {
                 const int nr = min(TILE, rows - t * TILE);
                 const bool app_tile = app && t == ntiles - 1;
+                // row L-1 may still be written by the previous (same-layer) kernel
+                if (!waited && (issued == STAGES || r0 + t * TILE + nr == L)) flush();
                 mbar_wait(&sm.empty[stage], phase ^ 1);
                 Stage<D, TILE> &st = sm.st[stage];
                 uint32_t bytes = 2u * nr * D * 2;
@@ -177,20 +193,33 @@ __global__ void __launch_bounds__((CWARPS + 1) * 32, MINB) decode_attention_kern
                     bulk_g2s_evict_first(st.k, kb + (size_t)t * TILE * D, ncache * D * 2, &sm.full[stage], pol);
                     bulk_g2s_evict_first(st.v, vb + (size_t)t * TILE * D, ncache * D * 2, &sm.full[stage], pol);
                 }
-                if (app_tile) {
+                if (app_tile) {   // (always after the wait: see the flush above)
                     const size_t nb = ((size_t)b * p.Hkv + g) * D;
                     bulk_g2s(st.k + (nr - 1) * D, p.k_new + nb, D * 2, &sm.full[stage]);
                     bulk_g2s(st.v + (nr - 1) * D, p.v_new + nb, D * 2, &sm.full[stage]);
                 }
                 if (mbytes) bulk_g2s(st.mask, msrc, mbytes, &sm.full[stage]);
-                if (t == 0) bulk_g2s(st.q, p.q + (size_t)(b * p.Hq + h) * D, D * 2, &sm.full[stage]);
+                if (t == 0) {
+                    const __nv_bfloat16 *qsrc = p.q + (size_t)(b * p.Hq + h) * D;
+                    if (waited) {
+                        bulk_g2s(st.q, qsrc, D * 2, &sm.full[stage]);
+                    } else {
+                        late_q = qsrc;
+                        late_stage = stage;
+                    }
+                }
+                ++issued;
                 if (++stage == STAGES) {
                     stage = 0;
                     phase ^= 1;
                 }
             }
+            if (!waited) flush();
+            if (w_next < 0) w_next = (int)gridDim.x + sched_next(p.counters);
             w = w_next;
+            w_next = w < total ? (int)gridDim.x + sched_next(p.counters) : total;
         }
+        if (!waited) flush();
         sched_done(p.counters);
         mbar_wait(&sm.empty[stage], phase ^ 1);
         sm.st[stage].desc.flags = F_END;
@@ -199,6 +228,17 @@ __global__ void __launch_bounds__((CWARPS + 1) * 32, MINB) decode_attention_kern
     }
 
     // ============================ consumer warps ============================
+    if (p.early) {
+        griddep_wait();
+        griddep_launch_dependents();
+    }
+    // Empty slots produce a zero output row (C6).
+    for (int b = blockIdx.x; b < p.B; b += gridDim.x) {
+        if (p.lens[b] <= 0) {
+            uint4 *o = reinterpret_cast<uint4 *>(p.out + (size_t)b * p.Hq * D);
+            for (int i = threadIdx.x; i < p.Hq * D / 8; i += CWARPS * 32) o[i] = make_uint4(0, 0, 0, 0);
+        }
+    }
     const int g = lane / LPR;        // row group within a warp-wide load
     const int s = lane % LPR;        // 16-B column chunk: dims [8s, 8s+8)
     const int my_row = (s >> 1) * RPL + g;   // row whose score this lane ends up holding
@@ -434,6 +474,7 @@ cudaError_t launch_d(const DecodeArgs &a, cudaStream_t s) {
     p.max_ctx = a.max_ctx;
     p.max_chunks = a.max_chunks;
     p.scale_log2 = a.scale * 1.4426950408889634f;
+    p.early = a.early;
     return launch_pdl(decode_attention_kernel<D, CW, ST, MINB>, dim3(MINB * num_sms),
                       dim3((CW + 1) * 32), smem, s, p);
 }

@@ -26,6 +26,19 @@
 #include "tma.h"
 
 namespace baton {
+
+// Debug timeline (off unless baton_debug_gqa_trace(1, ...) was called): per CTA,
+// [0] enter [1] work list built [2] exit [3] items [4] smid, then per item k
+// [8+4k] item w, [9+4k] first TMA issued, [10+4k] first tile ready, [11+4k] epilogue done.
+constexpr int TRACE_CTAS = 1024, TRACE_W = 64;
+__device__ int g_trace_on;
+__device__ long long g_trace[TRACE_CTAS][TRACE_W];
+BATON_DEV long long gtimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 namespace {
 
 constexpr int D = 128;
@@ -116,6 +129,14 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
     Smem<CW, STAGES> &sm =
         *reinterpret_cast<Smem<CW, STAGES> *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool trace = g_trace_on && blockIdx.x < TRACE_CTAS;
+    long long *tr = g_trace[trace ? blockIdx.x : 0];
+    if (trace && threadIdx.x == 0) {
+        tr[0] = gtimer();
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        tr[4] = smid;
+    }
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -138,6 +159,8 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
         // ============================ producer warp ============================
         sched_build(sm.ws, p.lens, p.pad, p.B, p.Hkv, lane);
         if (lane != 0) return;
+        if (trace) tr[1] = gtimer();
+        int titem = 0;
         const int total = sched_total(sm.ws, p.Hkv);
         int stage = 0;
         uint32_t phase = 0;
@@ -153,6 +176,11 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
             const int rows = min(CHUNK, L - r0);
             const int row_base = (b * p.Hkv + g) * p.max_ctx + r0;   // row in the 2-D tensor map
             const int ntiles = (rows + TILE - 1) / TILE;
+            if (trace && titem < (TRACE_W - 8) / 4) {
+                tr[8 + 4 * titem] = w;
+                tr[9 + 4 * titem] = gtimer();
+            }
+            ++titem;
             for (int t = 0; t < ntiles; ++t) {
                 const int nr = min(TILE, rows - t * TILE);
                 mbar_wait(&sm.empty[stage], phase ^ 1);
@@ -216,11 +244,14 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
     int stage = 0;
     uint32_t phase = 0;
     int rb = 0;                          // merge buffer of the current item
+    int citem = 0;
     while (true) {
         mbar_wait(&sm.full[stage], phase);
         Stage<CW> &st = sm.st[stage];
         const Desc d = st.desc;
         if (d.flags & F_END) break;
+        if (trace && threadIdx.x == 0 && (d.flags & F_FIRST) && citem < (TRACE_W - 8) / 4)
+            tr[10 + 4 * citem] = gtimer();
         if (d.flags & F_FIRST) {
             const uint32_t *qw = reinterpret_cast<const uint32_t *>(st.q + r4 * D);
 #pragma unroll
@@ -393,7 +424,13 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
             }
           }
           rb ^= 1;
+          if (trace && threadIdx.x == 0 && citem < (TRACE_W - 8) / 4) tr[11 + 4 * citem] = gtimer();
+          ++citem;
         }
+    }
+    if (trace && threadIdx.x == 0) {
+        tr[2] = gtimer();
+        tr[3] = citem;
     }
 }
 
@@ -511,3 +548,20 @@ cudaError_t launch_decode_gqa(const DecodeArgs &a, cudaStream_t s) {
 }
 
 }  // namespace baton
+
+// Debug only (not part of include/baton.h): switch the GQA timeline on/off and
+// copy it out ([TRACE_CTAS][TRACE_W] int64, see g_trace).
+extern "C" int baton_debug_gqa_trace(int on, void *host, size_t bytes) {
+    if (host) {
+        if (cudaMemcpyFromSymbol(host, baton::g_trace, bytes < sizeof(baton::g_trace) ? bytes : sizeof(baton::g_trace)) != cudaSuccess)
+            return -1;
+    }
+    if (on >= 0) {
+        if (on) {
+            static long long zero[baton::TRACE_CTAS][baton::TRACE_W];
+            cudaMemcpyToSymbol(baton::g_trace, zero, sizeof(zero));
+        }
+        if (cudaMemcpyToSymbol(baton::g_trace_on, &on, sizeof(int)) != cudaSuccess) return -1;
+    }
+    return 0;
+}

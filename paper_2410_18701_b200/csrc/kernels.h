@@ -22,6 +22,9 @@ struct DecodeArgs {
     const void *k_new = nullptr, *v_new = nullptr;   // fused append (a2) when non-null
     int32_t *counters = nullptr;                      // 2 ints after the tickets
     bool dry = false;                                 // only set kernel attributes (pre-capture)
+    // the previous launch in the stream was a decode kernel of this shard: the MHA
+    // kernel may prefetch before griddepcontrol.wait (decode_attention.cu)
+    bool early = false;
     const uint8_t *mask;            // nullable
     const int32_t *lens, *pad;
     void *out;

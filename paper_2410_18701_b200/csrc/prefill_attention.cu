@@ -189,8 +189,11 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
             constexpr uint32_t idO = idesc_bf16(PF_M, PF_D, 1);   // B = V tile, MN-major
             const uint32_t qa = smem_u32(sm.q), pa = smem_u32(sm.p), ka = smem_u32(sm.k);
             mbar_wait(&sm.bar_q, 0);
-            for (int j = 0; j < n_kt; ++j) {
-                const int s = j & 1;
+            // S(j+1) = Q K(j+1)^T is issued as soon as the softmax warps hold S(j) in
+            // registers, BEFORE waiting for P(j): the tensor pipe computes the next
+            // scores while the softmax of this tile runs, and PV(j) runs under the
+            // softmax of tile j+1.
+            auto issue_s = [&](int j) {
                 mbar_wait(&sm.k_full, j & 1);
                 if (j > 0) mbar_wait(&sm.s_free, (j - 1) & 1);   // softmax has read S(j-1)
                 tc_fence_after();
@@ -201,6 +204,11 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
                 }
                 umma_commit(&sm.s_full);
                 umma_commit(&sm.k_empty);
+            };
+            issue_s(0);
+            for (int j = 0; j < n_kt; ++j) {
+                const int s = j & 1;
+                if (j + 1 < n_kt) issue_s(j + 1);
                 mbar_wait(&sm.p_full, j & 1);                   // P(j) written, O rescaled
                 mbar_wait(&sm.v_full[s], (j >> 1) & 1);
                 tc_fence_after();

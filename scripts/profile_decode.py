@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--layers", type=int, default=4)
     ap.add_argument("--t0", type=int, default=512)
     ap.add_argument("--config", default="7b")
+    ap.add_argument("--trace", default=None, help="GQA only: write the per-CTA timeline here")
     args = ap.parse_args()
     wl = config_workload(args.config)
     if args.config == "70b":
@@ -89,7 +90,55 @@ def main():
                       "sum_lens": int(live.sum()), "bytes_per_launch": nbytes,
                       "us_per_launch_graph": us_graph, "GBps_graph": nbytes / us_graph / 1e3,
                       "us_eager_median": float(np.median(us_w)),
-                      "variant": os.environ.get("BATON_MHA_VARIANT", "0")}))
+                      "variant": os.environ.get("BATON_GQA_VARIANT" if wl.kv_heads < wl.q_heads
+                                                else "BATON_MHA_VARIANT", "0")}))
+    if args.trace:
+        trace_gqa(sh, q, out, g, args.trace)
+
+
+def trace_gqa(sh, q, out, graph, path):
+    """Per-CTA timeline of one launch (globaltimer ns) from the debug trace of
+    decode_gqa.cu: eager single launch, and the last launch of a graph replay."""
+    import ctypes
+    from paper_2410_18701_b200 import _lib
+    lib = _lib._load()
+    fn = lib.baton_debug_gqa_trace
+    fn.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t]
+    res = {}
+    for mode in ("eager", "graph"):
+        assert fn(1, None, 0) == 0
+        if mode == "eager":
+            sh.baton_decode_attention(0, q, out)
+        else:
+            graph.replay()
+        torch.cuda.synchronize()
+        buf = np.zeros((1024, 64), np.int64)
+        assert fn(0, buf.ctypes.data, buf.nbytes) == 0
+        rows = buf[buf[:, 0] > 0]
+        t0 = rows[:, 0].min()
+        ctas = []
+        for r in rows:
+            n = int(r[3])
+            items = [[int(r[8 + 4 * k]), *(int(x - t0) if x else 0 for x in r[9 + 4 * k:12 + 4 * k])]
+                     for k in range(min(n, 14))]
+            ctas.append({"smid": int(r[4]), "enter": int(r[0] - t0), "built": int(r[1] - t0),
+                         "exit": int(r[2] - t0), "items": items})
+        res[mode] = ctas
+        span = max(c["exit"] for c in ctas)
+        first_ready = [c["items"][0][2] for c in ctas if c["items"]]
+        exits = sorted(c["exit"] for c in ctas)
+        busy = [c["items"][-1][3] - c["items"][0][2] for c in ctas if c["items"]]
+        durs = [it[3] - it[2] for c in ctas for it in c["items"]]
+        print(json.dumps({"trace": mode, "ctas": len(ctas), "span_ns": span,
+                          "enter_max_ns": max(c["enter"] for c in ctas),
+                          "built_median_ns": float(np.median([c["built"] for c in ctas])),
+                          "first_ready_median_ns": float(np.median(first_ready)),
+                          "first_ready_max_ns": max(first_ready),
+                          "exit_p10_ns": exits[len(exits) // 10], "exit_median_ns": exits[len(exits) // 2],
+                          "items_per_cta": float(np.mean([len(c["items"]) for c in ctas])),
+                          "item_ns_median": float(np.median(durs)), "item_ns_max": max(durs),
+                          "busy_frac": float(np.sum(busy) / (span * len(ctas)))}))
+    json.dump(res, open(path, "w"))
 
 
 if __name__ == "__main__":

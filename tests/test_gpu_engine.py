@@ -190,3 +190,39 @@ def test_extract_to_pinned_host_and_back():
     sh.baton_insert(2, kh, vh, 100)
     Kd, Vd = sh.live_kv(2)
     assert torch.equal(Kd, K) and torch.equal(Vd, V)
+
+
+def test_early_prefetch_sees_previous_append():
+    """A decode launch that follows a decode launch prefetches K/V before
+    griddepcontrol.wait (DecodeArgs::early).  The previous launch may have just
+    written cache row lens-1 (fused append): a second, append-free launch on the
+    SAME layer must read that row, and give bit-for-bit the first launch's output
+    (which took the row from k_new/v_new)."""
+    require_cuda()
+    from paper_2410_18701_b200.baton import BatonShard
+    torch.manual_seed(0)
+    L, B, H, D, cap = 2, 24, 32, 128, 2048
+    sh = BatonShard(L, B, H, H, D, cap)
+    lens = [1 + (97 * i) % 1500 for i in range(B)]
+    ks = [torch.randn((L, H, n, D), device="cuda").to(torch.bfloat16) for n in lens]
+    vs = [torch.randn((L, H, n, D), device="cuda").to(torch.bfloat16) for n in lens]
+    sh.baton_insert_many(list(range(B)), ks, vs, lens)
+    for it in range(3):
+        sh.baton_mask_update()
+        q = torch.randn((B, H, D), device="cuda").to(torch.bfloat16)
+        kn = torch.randn((B, H, D), device="cuda").to(torch.bfloat16)
+        vn = torch.randn((B, H, D), device="cuda").to(torch.bfloat16)
+        outs = []
+        for l in range(L):
+            o1 = torch.empty_like(q)
+            sh.baton_decode_layer(l, q, o1, k_new=kn, v_new=vn)   # l > 0: early
+            o2 = torch.empty_like(q)
+            sh.baton_decode_layer(l, q, o2)                       # early, reads row lens-1
+            outs.append((o1, o2))
+        torch.cuda.synchronize()
+        for l, (o1, o2) in enumerate(outs):
+            assert torch.equal(o1, o2), (it, l)
+            ref = torch.empty_like(q)
+            sh.baton_decode_attention(l, q, ref)                  # stateless, no early
+            torch.cuda.synchronize()
+            assert torch.equal(o1, ref), (it, l)
