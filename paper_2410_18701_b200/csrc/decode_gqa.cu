@@ -16,8 +16,17 @@
 //     (16 MMAs), masked online softmax per head row (quad shuffles), P kept in
 //     registers as the A fragment of O[16 x 128] += P V (16 MMAs, V via
 //     ldmatrix.trans).
-//   epilogue: 4 warp states merged in smem; single chunk -> bf16 out, else split-K
-//     partials + last-CTA merge (same workspace layout as decode_attention.cu).
+//   fused append (a2): the tile holding row lens-1 also brings the new token's k/v
+//     (bulk copies into the stage's side buffer); the warp owning that row patches
+//     it into the swizzled tile and writes it to the cache row.
+//   epilogue: 4 warp states merged in smem; single chunk -> bf16 out, else an fp32
+//     split-K partial (same workspace layout as decode_attention.cu); no tickets,
+//     no fences: decode_combine_kernel, PDL-chained behind this launch, merges the
+//     chunks in ascending order.  The combine triggers its dependents right after
+//     its own wait, so the NEXT layer's launch (p.early) streams its first K/V ring
+//     while the combine runs.  (An in-kernel last-arriver merge was measured: the
+//     gpu-scope release/acquire and the 14-chunk merges of one warp left the grid
+//     open ~8 us after the streaming ended -- profiles/r01_gqa_fused.md.)
 #include <cstdlib>
 
 #include "common.cuh"
@@ -29,10 +38,14 @@ namespace baton {
 
 // Debug timeline (off unless baton_debug_gqa_trace(1, ...) was called): per CTA,
 // [0] enter [1] work list built [2] exit [3] items [4] smid, then per item k
-// [8+4k] item w, [9+4k] first TMA issued, [10+4k] first tile ready, [11+4k] epilogue done.
-constexpr int TRACE_CTAS = 1024, TRACE_W = 64;
+// [8+4k] item w, [9+4k] first TMA issued, [10+4k] first tile ready, [11+4k] epilogue
+// done (k < 8), [40+2t] tile t wait start, [41+2t] tile t ready (bit 62: it was
+// already complete when the wait began), t < 12.
+// Launch l writes slot l % TRACE_L (host launch counter, baked into captured graphs).
+constexpr int TRACE_L = 8, TRACE_CTAS = 256, TRACE_W = 64;
 __device__ int g_trace_on;
-__device__ long long g_trace[TRACE_CTAS][TRACE_W];
+__device__ long long g_trace[TRACE_L][TRACE_CTAS][TRACE_W];
+static int g_trace_launch = 0;
 BATON_DEV long long gtimer() {
     long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -43,37 +56,41 @@ namespace {
 
 constexpr int D = 128;
 constexpr int GS = 8;                       // q heads per kv head
-constexpr int KPW = 16;                     // keys per consumer warp per tile
-// CW (consumer warps), STAGES and CTAs/SM are template parameters; a tile has
-// TILE = CW * KPW keys and its two 64-dim halves are HALF = TILE * 128 bytes each.
-constexpr int F_FIRST = 1, F_LAST = 2, F_END = 4;
+// CW (consumer warps), KP (keys per consumer warp per tile: 16 or 32, i.e. one or
+// two independent 16-key MMA chains), STAGES and CTAs/SM are template parameters; a
+// tile has TILE = CW * KP keys and its two 64-dim halves are HALF = TILE * 128 bytes.
+constexpr int F_FIRST = 1, F_LAST = 2, F_END = 4, F_WRITE = 8;
+constexpr int QROW = D + 8;                 // q row stride in smem (272 B: rows 4 banks apart)
 
 struct Desc {
     int32_t b, g, c, nrows, flags, moff, nchunks, wrow;
 };
 
-template <int CW>
+template <int CW, int KP>
 struct __align__(1024) Stage {
-    static constexpr int TILE = CW * KPW;
+    static constexpr int TILE = CW * KP;
     static constexpr int HALF = TILE * 128;
     uint8_t k[2 * HALF];
     uint8_t v[2 * HALF];
-    __nv_bfloat16 q[GS * D];
+    __nv_bfloat16 q[GS * QROW];             // 8 head rows, padded: conflict-free fragment loads
+    __nv_bfloat16 knew[D], vnew[D];         // appended row (F_WRITE tiles)
     uint8_t mask[TILE + 16];
     Desc desc;
 };
 
-template <int CW, int STAGES>
+template <int CW, int KP, int STAGES, int RB>
 struct Smem {
-    Stage<CW> st[STAGES];
+    Stage<CW, KP> st[STAGES];
     uint64_t full[STAGES], empty[STAGES];
     WorkSched ws;
-    alignas(16) float red_o[2][CW][GS][D + 8];     // +8: spread the 8 head rows over the banks
-    float red_m[2][CW][GS], red_l[2][CW][GS];
+    alignas(16) float red_o[RB][CW][GS][D + 4];    // +4: the 8 head rows 4 banks apart
+    float red_m[RB][CW][GS], red_l[RB][CW][GS];
 };
 
 struct Params {
     const __nv_bfloat16 *q, *k, *v;
+    const __nv_bfloat16 *k_new, *v_new;     // fused append (nullable)
+    __nv_bfloat16 *k_w, *v_w;               // cache base for the append write-back
     int32_t *counters;
     const uint8_t *mask;
     const int32_t *lens, *pad;
@@ -82,6 +99,8 @@ struct Params {
     int32_t *tickets;
     int B, Hq, Hkv, max_ctx, max_chunks;
     float scale_log2;
+    bool early;                             // prefetch before griddepcontrol.wait
+    int trace_slot;                         // debug timeline slot
 };
 
 BATON_DEV uint32_t swz(int row, int chunk, int half) {   // byte offset of 16-B chunk (0..15) of a row
@@ -118,19 +137,20 @@ BATON_DEV void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1, ui
         : "memory");
 }
 
-template <int CW, int STAGES, int MINB>
+template <int CW, int KP, int STAGES, int RB, int MINB>
 __global__ void __launch_bounds__((CW + 1) * 32, MINB)
 decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
                   const Params p) {
     extern __shared__ uint8_t smem_raw[];
     // 1024-B alignment for the SWIZZLE_128B boxes; offsetting the __shared__ array
     // itself keeps the shared address space visible to the compiler (LDS, not LD)
-    constexpr int TILE = CW * KPW, HALF = TILE * 128, THREADS = (CW + 1) * 32;
-    Smem<CW, STAGES> &sm =
-        *reinterpret_cast<Smem<CW, STAGES> *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+    constexpr int TILE = CW * KP, HALF = TILE * 128, NG = KP / 16;
+    static_assert(KP % 16 == 0 && TILE <= 256, "tile shape");
+    Smem<CW, KP, STAGES, RB> &sm =
+        *reinterpret_cast<Smem<CW, KP, STAGES, RB> *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool trace = g_trace_on && blockIdx.x < TRACE_CTAS;
-    long long *tr = g_trace[trace ? blockIdx.x : 0];
+    long long *tr = g_trace[p.trace_slot][trace ? blockIdx.x : 0];
     if (trace && threadIdx.x == 0) {
         tr[0] = gtimer();
         unsigned smid;
@@ -145,15 +165,14 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
         }
         fence_mbar_init();
     }
-    griddep_wait();                 // PDL (see decode_attention.cu)
-    griddep_launch_dependents();
-    for (int b = blockIdx.x; b < p.B; b += gridDim.x) {
-        if (p.lens[b] <= 0) {
-            uint4 *o = reinterpret_cast<uint4 *>(p.out + (size_t)b * p.Hq * D);
-            for (int i = threadIdx.x; i < p.Hq * D / 8; i += THREADS) o[i] = make_uint4(0, 0, 0, 0);
-        }
-    }
     __syncthreads();
+    // PDL, as in decode_attention.cu: with p.early the producer builds the work list
+    // and issues the first ring of K/V boxes (never the tile holding row lens-1) of a
+    // statically assigned first item before the wait; q, k_new and all writes after.
+    if (!p.early) {
+        griddep_wait();
+        griddep_launch_dependents();
+    }
 
     if (warp == CW) {
         // ============================ producer warp ============================
@@ -165,9 +184,21 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
         int stage = 0;
         uint32_t phase = 0;
         int b = 0;
-        int w = sched_next(p.counters);
+        bool waited = !p.early;
+        const __nv_bfloat16 *late_q = nullptr;   // q of a tile issued before the wait
+        int late_stage = 0, issued = 0;
+        auto flush = [&]() {
+            griddep_wait();
+            griddep_launch_dependents();
+            waited = true;
+            if (late_q)
+                for (int hq = 0; hq < GS; ++hq)
+                    bulk_g2s(sm.st[late_stage].q + hq * QROW, late_q + hq * D, D * 2, &sm.full[late_stage]);
+            late_q = nullptr;
+        };
+        int w = blockIdx.x;   // static first item; the rest from the dynamic counter
+        int w_next = waited ? (int)gridDim.x + sched_next(p.counters) : -1;
         while (w < total) {
-            const int w_next = sched_next(p.counters);   // latency hidden by this item
             int c, g;
             sched_item(sm.ws, w, p.Hkv, b, c, g);
             const int L = sm.ws.lens[b];
@@ -176,15 +207,19 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
             const int rows = min(CHUNK, L - r0);
             const int row_base = (b * p.Hkv + g) * p.max_ctx + r0;   // row in the 2-D tensor map
             const int ntiles = (rows + TILE - 1) / TILE;
-            if (trace && titem < (TRACE_W - 8) / 4) {
+            const bool app = p.k_new != nullptr && c == nch - 1;
+            if (trace && titem < 8) {
                 tr[8 + 4 * titem] = w;
                 tr[9 + 4 * titem] = gtimer();
             }
             ++titem;
             for (int t = 0; t < ntiles; ++t) {
                 const int nr = min(TILE, rows - t * TILE);
+                const bool app_tile = app && t == ntiles - 1;
+                // row L-1 may still be written by the previous (same-layer) kernel
+                if (!waited && (issued == STAGES || r0 + t * TILE + nr == L)) flush();
                 mbar_wait(&sm.empty[stage], phase ^ 1);
-                Stage<CW> &st = sm.st[stage];
+                Stage<CW, KP> &st = sm.st[stage];
                 uint32_t bytes = 4 * HALF;      // full boxes, OOB rows zero-filled
                 int moff = 0;
                 uint32_t mbytes = 0;
@@ -201,30 +236,49 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
                     bytes += mbytes;
                 }
                 if (t == 0) bytes += GS * D * 2;
+                if (app_tile) bytes += 2 * D * 2;
                 st.desc.b = b;
                 st.desc.g = g;
                 st.desc.c = c;
                 st.desc.nrows = nr;
-                st.desc.flags = (t == 0 ? F_FIRST : 0) | (t == ntiles - 1 ? F_LAST : 0);
+                st.desc.flags = (t == 0 ? F_FIRST : 0) | (t == ntiles - 1 ? F_LAST : 0) | (app_tile ? F_WRITE : 0);
                 st.desc.moff = moff;
                 st.desc.nchunks = nch;
-                st.desc.wrow = 0;
+                st.desc.wrow = L - 1;
                 mbar_arrive_expect_tx(&sm.full[stage], bytes);
                 const int row = row_base + t * TILE;
                 tma_load_2d(st.k, &kmap, 0, row, &sm.full[stage]);
                 tma_load_2d(st.k + HALF, &kmap, 64, row, &sm.full[stage]);
                 tma_load_2d(st.v, &vmap, 0, row, &sm.full[stage]);
                 tma_load_2d(st.v + HALF, &vmap, 64, row, &sm.full[stage]);
-                if (t == 0)   // the group's 8 query rows (contiguous 2 KB)
-                    bulk_g2s(st.q, p.q + ((size_t)b * p.Hq + g * GS) * D, GS * D * 2, &sm.full[stage]);
                 if (mbytes) bulk_g2s(st.mask, msrc, mbytes, &sm.full[stage]);
+                if (app_tile) {   // (always after the wait: see the flush above)
+                    const size_t nb = ((size_t)b * p.Hkv + g) * D;
+                    bulk_g2s(st.knew, p.k_new + nb, D * 2, &sm.full[stage]);
+                    bulk_g2s(st.vnew, p.v_new + nb, D * 2, &sm.full[stage]);
+                }
+                if (t == 0) {   // the group's 8 query rows (contiguous 2 KB)
+                    const __nv_bfloat16 *qsrc = p.q + ((size_t)b * p.Hq + g * GS) * D;
+                    if (waited) {
+                        for (int hq = 0; hq < GS; ++hq)
+                            bulk_g2s(st.q + hq * QROW, qsrc + hq * D, D * 2, &sm.full[stage]);
+                    } else {
+                        late_q = qsrc;
+                        late_stage = stage;
+                    }
+                }
+                ++issued;
                 if (++stage == STAGES) {
                     stage = 0;
                     phase ^= 1;
                 }
             }
+            if (!waited) flush();
+            if (w_next < 0) w_next = (int)gridDim.x + sched_next(p.counters);
             w = w_next;
+            w_next = w < total ? (int)gridDim.x + sched_next(p.counters) : total;
         }
+        if (!waited) flush();
         sched_done(p.counters);
         mbar_wait(&sm.empty[stage], phase ^ 1);
         sm.st[stage].desc.flags = F_END;
@@ -233,6 +287,16 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
     }
 
     // ============================ consumer warps ============================
+    if (p.early) {
+        griddep_wait();
+        griddep_launch_dependents();
+    }
+    for (int b = blockIdx.x; b < p.B; b += gridDim.x) {   // empty slots -> zero rows (C6)
+        if (p.lens[b] <= 0) {
+            uint4 *o = reinterpret_cast<uint4 *>(p.out + (size_t)b * p.Hq * D);
+            for (int i = threadIdx.x; i < p.Hq * D / 8; i += CW * 32) o[i] = make_uint4(0, 0, 0, 0);
+        }
+    }
     // Transposed formulation (keys and dims as the MMA's M so no row is padding):
     //   S^T[16 keys x 8 heads]  = K[16 x 128] . Q^T            (8 MMAs per tile)
     //   O^T[128 dims x 8 heads] += V^T[128 x 16 keys] . P^T     (8 MMAs per tile)
@@ -244,16 +308,27 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
     int stage = 0;
     uint32_t phase = 0;
     int rb = 0;                          // merge buffer of the current item
-    int citem = 0;
+    int citem = 0, ctile = 0;
     while (true) {
+        long long t_w = 0;
+        bool was_ready = false;
+        if (trace && threadIdx.x == 0) {
+            t_w = gtimer();
+            was_ready = mbar_test_wait(&sm.full[stage], phase);
+        }
         mbar_wait(&sm.full[stage], phase);
-        Stage<CW> &st = sm.st[stage];
+        Stage<CW, KP> &st = sm.st[stage];
         const Desc d = st.desc;
         if (d.flags & F_END) break;
-        if (trace && threadIdx.x == 0 && (d.flags & F_FIRST) && citem < (TRACE_W - 8) / 4)
+        if (trace && threadIdx.x == 0 && (d.flags & F_FIRST) && citem < 8)
             tr[10 + 4 * citem] = gtimer();
+        if (trace && threadIdx.x == 0 && ctile < (TRACE_W - 40) / 2) {
+            tr[40 + 2 * ctile] = t_w;
+            tr[41 + 2 * ctile] = gtimer() | (was_ready ? (1LL << 62) : 0);
+        }
+        ++ctile;
         if (d.flags & F_FIRST) {
-            const uint32_t *qw = reinterpret_cast<const uint32_t *>(st.q + r4 * D);
+            const uint32_t *qw = reinterpret_cast<const uint32_t *>(st.q + r4 * QROW);
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
                 qb[kk][0] = qw[(kk * 16 + c2) / 2];
@@ -264,37 +339,69 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
             m[0] = m[1] = -INFINITY;
             l[0] = l[1] = 0.f;
         }
-        const int base = warp * KPW;
+        const int base = warp * KP;
+        if ((d.flags & F_WRITE) && warp == (d.nrows - 1) / KP) {
+            // a2: row lens-1 of this tile is the new token: patch it into the swizzled
+            // tile (lanes 0-15 K chunks, 16-31 V chunks) and write it to the cache
+            const int rr = d.nrows - 1, ch = lane & 15;
+            const uint4 val = reinterpret_cast<const uint4 *>(lane < 16 ? st.knew : st.vnew)[ch];
+            *reinterpret_cast<uint4 *>((lane < 16 ? st.k : st.v) + swz(rr, ch, HALF)) = val;
+            const size_t dst = (((size_t)d.b * p.Hkv + d.g) * p.max_ctx + d.wrow) * D;
+            reinterpret_cast<uint4 *>((lane < 16 ? p.k_w : p.v_w) + dst)[ch] = val;
+            __syncwarp();
+        }
         if (base < d.nrows) {
             const uint32_t ks_ = smem_u32(st.k), vs_ = smem_u32(st.v);
             const int i4 = lane >> 3, r8 = lane & 7;
-            // ---- S^T = K Q^T: A = 16 key rows via ldmatrix (two accumulator chains)
-            float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
-            {
-                const int key = base + (i4 & 1) * 8 + r8;
+            // ---- S^T = K Q^T per 16-key group: A = 16 key rows via ldmatrix (two
+            // accumulator chains per group; the NG groups are independent)
+            // (branch-free over the groups so their chains interleave; rows past
+            // nrows are masked below and their V rows zeroed)
+            float x[NG][4];
+            bool okg[NG];
+            float sa[NG][4], sb[NG][4];
 #pragma unroll
-                for (int kk = 0; kk < 8; kk += 2) {
-                    uint32_t a0, a1, a2, a3, e0, e1, e2, e3;
-                    ldsm_x4(ks_ + swz(key, 2 * kk + (i4 >> 1), HALF), a0, a1, a2, a3);
-                    ldsm_x4(ks_ + swz(key, 2 * kk + 2 + (i4 >> 1), HALF), e0, e1, e2, e3);
-                    mma16816(sa, a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
-                    mma16816(sb, e0, e1, e2, e3, qb[kk + 1][0], qb[kk + 1][1]);
+            for (int j = 0; j < NG; ++j)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) sa[j][i] = sb[j][i] = 0.f;
+#pragma unroll
+            for (int kk = 0; kk < 8; kk += 2) {
+                uint32_t a[NG][4], e[NG][4];
+#pragma unroll
+                for (int j = 0; j < NG; ++j) {
+                    const int key = base + 16 * j + (i4 & 1) * 8 + r8;
+                    ldsm_x4(ks_ + swz(key, 2 * kk + (i4 >> 1), HALF), a[j][0], a[j][1], a[j][2], a[j][3]);
+                    ldsm_x4(ks_ + swz(key, 2 * kk + 2 + (i4 >> 1), HALF), e[j][0], e[j][1], e[j][2], e[j][3]);
+                }
+#pragma unroll
+                for (int j = 0; j < NG; ++j) {
+                    mma16816(sa[j], a[j][0], a[j][1], a[j][2], a[j][3], qb[kk][0], qb[kk][1]);
+                    mma16816(sb[j], e[j][0], e[j][1], e[j][2], e[j][3], qb[kk + 1][0], qb[kk + 1][1]);
                 }
             }
-            // keys of this thread: r4 (values 0,1) and r4 + 8 (values 2,3)
-            const int k0 = base + r4, k1 = base + r4 + 8;
-            bool ok0 = k0 < d.nrows, ok1 = k1 < d.nrows;
-            if (p.mask) {
-                ok0 = ok0 && st.mask[d.moff + (ok0 ? k0 : 0)] != 0;
-                ok1 = ok1 && st.mask[d.moff + (ok1 ? k1 : 0)] != 0;
+#pragma unroll
+            for (int j = 0; j < NG; ++j) {
+                const int gb = base + 16 * j;
+                // keys of this thread: gb + r4 (values 0,1) and gb + r4 + 8 (values 2,3)
+                const int k0 = gb + r4, k1 = gb + r4 + 8;
+                bool ok0 = k0 < d.nrows, ok1 = k1 < d.nrows;
+                if (p.mask) {
+                    ok0 = ok0 && st.mask[d.moff + (ok0 ? k0 : 0)] != 0;
+                    ok1 = ok1 && st.mask[d.moff + (ok1 ? k1 : 0)] != 0;
+                }
+                x[j][0] = ok0 ? (sa[j][0] + sb[j][0]) * p.scale_log2 : -INFINITY;
+                x[j][1] = ok0 ? (sa[j][1] + sb[j][1]) * p.scale_log2 : -INFINITY;
+                x[j][2] = ok1 ? (sa[j][2] + sb[j][2]) * p.scale_log2 : -INFINITY;
+                x[j][3] = ok1 ? (sa[j][3] + sb[j][3]) * p.scale_log2 : -INFINITY;
+                okg[j] = ok0 && ok1;
             }
-            float x[4];
-            x[0] = ok0 ? (sa[0] + sb[0]) * p.scale_log2 : -INFINITY;
-            x[1] = ok0 ? (sa[1] + sb[1]) * p.scale_log2 : -INFINITY;
-            x[2] = ok1 ? (sa[2] + sb[2]) * p.scale_log2 : -INFINITY;
-            x[3] = ok1 ? (sa[3] + sb[3]) * p.scale_log2 : -INFINITY;
-            // per-head (column) max over the warp's 16 keys: lanes with equal lane & 3
-            float mx0 = fmaxf(x[0], x[2]), mx1 = fmaxf(x[1], x[3]);
+            // per-head (column) max over the warp's KP keys: lanes with equal lane & 3
+            float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+            for (int j = 0; j < NG; ++j) {
+                mx0 = fmaxf(mx0, fmaxf(x[j][0], x[j][2]));
+                mx1 = fmaxf(mx1, fmaxf(x[j][1], x[j][3]));
+            }
 #pragma unroll
             for (int o2 = 4; o2 < 32; o2 <<= 1) {
                 mx0 = fmaxf(mx0, __shfl_xor_sync(FULL_MASK, mx0, o2));
@@ -304,10 +411,19 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
             const float rf0 = (mn0 == -INFINITY) ? 0.f : mn0, rf1 = (mn1 == -INFINITY) ? 0.f : mn1;
             const float al0 = ex2(m[0] - rf0), al1 = ex2(m[1] - rf1);
             // P.V multiplies bf16(p): sum the same rounded weights
-            const __nv_bfloat162 p01 = __floats2bfloat162_rn(ex2(x[0] - rf0), ex2(x[1] - rf1));  // key k0
-            const __nv_bfloat162 p23 = __floats2bfloat162_rn(ex2(x[2] - rf0), ex2(x[3] - rf1));  // key k1
-            l[0] = l[0] * al0 + __low2float(p01) + __low2float(p23);
-            l[1] = l[1] * al1 + __high2float(p01) + __high2float(p23);
+            uint32_t w01[NG], w23[NG];
+            float ls0 = 0.f, ls1 = 0.f;
+#pragma unroll
+            for (int j = 0; j < NG; ++j) {
+                const __nv_bfloat162 p01 = __floats2bfloat162_rn(ex2(x[j][0] - rf0), ex2(x[j][1] - rf1));
+                const __nv_bfloat162 p23 = __floats2bfloat162_rn(ex2(x[j][2] - rf0), ex2(x[j][3] - rf1));
+                ls0 += __low2float(p01) + __low2float(p23);
+                ls1 += __high2float(p01) + __high2float(p23);
+                w01[j] = *reinterpret_cast<const uint32_t *>(&p01);
+                w23[j] = *reinterpret_cast<const uint32_t *>(&p23);
+            }
+            l[0] = l[0] * al0 + ls0;
+            l[1] = l[1] * al1 + ls1;
             m[0] = mn0;
             m[1] = mn1;
 #pragma unroll
@@ -318,8 +434,11 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
                 o[i][3] *= al1;
             }
             // masked / out-of-range keys: their V rows may hold anything -> zero them
-            if (__any_sync(FULL_MASK, !(ok0 && ok1))) {
-                for (int kr = 0; kr < KPW; ++kr) {
+            bool bad = false;
+#pragma unroll
+            for (int j = 0; j < NG; ++j) bad = bad || !okg[j];
+            if (__any_sync(FULL_MASK, bad)) {
+                for (int kr = 0; kr < KP; ++kr) {
                     const int kt = base + kr;
                     bool ok = kt < d.nrows;
                     if (p.mask) ok = ok && st.mask[d.moff + (ok ? kt : 0)] != 0;
@@ -330,23 +449,27 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
             // ---- P^T B-fragment: thread needs P[keys c2, c2+1 (+8)][head r4].  The
             // value P[k][n] sits in lane (k & 7) * 4 + n / 2, half n & 1, of p01 (k < 8)
             // or p23 (k >= 8).
-            const uint32_t w01 = *reinterpret_cast<const uint32_t *>(&p01);
-            const uint32_t w23 = *reinterpret_cast<const uint32_t *>(&p23);
             const int srcA = c2 * 4 + (r4 >> 1), srcB = (c2 + 1) * 4 + (r4 >> 1);
             const uint32_t sh = (r4 & 1) ? 16 : 0;
-            const uint32_t x0 = __shfl_sync(FULL_MASK, w01, srcA), x1 = __shfl_sync(FULL_MASK, w01, srcB);
-            const uint32_t y0 = __shfl_sync(FULL_MASK, w23, srcA), y1 = __shfl_sync(FULL_MASK, w23, srcB);
-            const uint32_t pb0 = ((x0 >> sh) & 0xffffu) | (((x1 >> sh) & 0xffffu) << 16);
-            const uint32_t pb1 = ((y0 >> sh) & 0xffffu) | (((y1 >> sh) & 0xffffu) << 16);
-            // ---- O^T += V^T P^T: A = V^T (16 dims x 16 keys) via ldmatrix.trans
-            {
-                const int key = base + (i4 >> 1) * 8 + r8;
+            uint32_t pb0[NG], pb1[NG];
 #pragma unroll
-                for (int mt = 0; mt < 8; ++mt) {
-                    uint32_t a0, a1, a2, a3;
-                    ldsm_x4_t(vs_ + swz(key, 2 * mt + (i4 & 1), HALF), a0, a1, a2, a3);
-                    mma16816(o[mt], a0, a1, a2, a3, pb0, pb1);
+            for (int j = 0; j < NG; ++j) {
+                const uint32_t x0 = __shfl_sync(FULL_MASK, w01[j], srcA), x1 = __shfl_sync(FULL_MASK, w01[j], srcB);
+                const uint32_t y0 = __shfl_sync(FULL_MASK, w23[j], srcA), y1 = __shfl_sync(FULL_MASK, w23[j], srcB);
+                pb0[j] = ((x0 >> sh) & 0xffffu) | (((x1 >> sh) & 0xffffu) << 16);
+                pb1[j] = ((y0 >> sh) & 0xffffu) | (((y1 >> sh) & 0xffffu) << 16);
+            }
+            // ---- O^T += V^T P^T: A = V^T (16 dims x 16 keys) via ldmatrix.trans
+#pragma unroll
+            for (int mt = 0; mt < 8; ++mt) {
+                uint32_t a[NG][4];
+#pragma unroll
+                for (int j = 0; j < NG; ++j) {
+                    const int key = base + 16 * j + (i4 >> 1) * 8 + r8;
+                    ldsm_x4_t(vs_ + swz(key, 2 * mt + (i4 & 1), HALF), a[j][0], a[j][1], a[j][2], a[j][3]);
                 }
+#pragma unroll
+                for (int j = 0; j < NG; ++j) mma16816(o[mt], a[j][0], a[j][1], a[j][2], a[j][3], pb0[j], pb1[j]);
             }
         }
         __syncwarp();
@@ -357,9 +480,9 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
         }
 
         if (d.flags & F_LAST) {
-            // ---- merge the 4 warp states (double-buffered smem: one barrier per item).
-            // Multi-chunk queries leave an fp32 partial; decode_combine_kernel (next in
-            // the stream, PDL) merges chunks in order -- no tickets, no waiting here.
+            // ---- merge the CW warp states in smem (RB = 2: double-buffered, one
+            // barrier per item; RB = 1: a second barrier before the buffer is reused).
+            // Multi-chunk queries leave an fp32 partial for decode_combine_kernel.
             float ls0 = l[0], ls1 = l[1];
 #pragma unroll
             for (int o2 = 4; o2 < 32; o2 <<= 1) {
@@ -380,9 +503,10 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
                 sm.red_l[rb][warp][c2 + 1] = ls1;
             }
             named_bar_sync(1, CW * 32);
-          // (head, 8-dim block) pairs, CW*32 threads at a time
+          // (head, dims {d0..d0+3} u {d0+64..d0+67}) per thread, CW*32 threads at a
+          // time: a half-warp reads 256 contiguous bytes per float4 load
           for (int idx = threadIdx.x; idx < GS * (D / 8); idx += CW * 32) {
-            const int hh = idx >> 4, d0 = (idx & 15) * 8;
+            const int hh = idx >> 4, d0 = (idx & 15) * 4;
             float M = -INFINITY;
 #pragma unroll
             for (int w2 = 0; w2 < CW; ++w2) M = fmaxf(M, sm.red_m[rb][w2][hh]);
@@ -393,7 +517,7 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
                 const float f = (mw == -INFINITY) ? 0.f : ex2(mw - M);
                 Lt = fmaf(f, sm.red_l[rb][w2][hh], Lt);
                 const float4 a4 = *reinterpret_cast<const float4 *>(&sm.red_o[rb][w2][hh][d0]);
-                const float4 b4 = *reinterpret_cast<const float4 *>(&sm.red_o[rb][w2][hh][d0 + 4]);
+                const float4 b4 = *reinterpret_cast<const float4 *>(&sm.red_o[rb][w2][hh][d0 + 64]);
                 Ot[0] = fmaf(f, a4.x, Ot[0]);
                 Ot[1] = fmaf(f, a4.y, Ot[1]);
                 Ot[2] = fmaf(f, a4.z, Ot[2]);
@@ -407,24 +531,26 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
             const size_t bh = (size_t)d.b * p.Hq + h;
             if (d.nchunks == 1) {
                 const float inv = Lt > 0.f ? 1.f / Lt : 0.f;
-                uint4 w4;
-                w4.x = pack_bf16(Ot[0] * inv, Ot[1] * inv);
-                w4.y = pack_bf16(Ot[2] * inv, Ot[3] * inv);
-                w4.z = pack_bf16(Ot[4] * inv, Ot[5] * inv);
-                w4.w = pack_bf16(Ot[6] * inv, Ot[7] * inv);
-                *reinterpret_cast<uint4 *>(p.out + bh * D + d0) = w4;
+                uint2 w0, w1;
+                w0.x = pack_bf16(Ot[0] * inv, Ot[1] * inv);
+                w0.y = pack_bf16(Ot[2] * inv, Ot[3] * inv);
+                w1.x = pack_bf16(Ot[4] * inv, Ot[5] * inv);
+                w1.y = pack_bf16(Ot[6] * inv, Ot[7] * inv);
+                *reinterpret_cast<uint2 *>(p.out + bh * D + d0) = w0;
+                *reinterpret_cast<uint2 *>(p.out + bh * D + d0 + 64) = w1;
             } else {
                 float *pp = p.partial + (bh * p.max_chunks + d.c) * (D + PREC_PAD);
                 *reinterpret_cast<float4 *>(pp + d0) = make_float4(Ot[0], Ot[1], Ot[2], Ot[3]);
-                *reinterpret_cast<float4 *>(pp + d0 + 4) = make_float4(Ot[4], Ot[5], Ot[6], Ot[7]);
+                *reinterpret_cast<float4 *>(pp + d0 + 64) = make_float4(Ot[4], Ot[5], Ot[6], Ot[7]);
                 if ((idx & 15) == 0) {
                     pp[D] = M;
                     pp[D + 1] = Lt;
                 }
             }
           }
-          rb ^= 1;
-          if (trace && threadIdx.x == 0 && citem < (TRACE_W - 8) / 4) tr[11 + 4 * citem] = gtimer();
+          if constexpr (RB == 1) named_bar_sync(1, CW * 32);   // merge buffer free again
+          rb = (rb + 1) % RB;
+          if (trace && threadIdx.x == 0 && citem < 8) tr[11 + 4 * citem] = gtimer();
           ++citem;
         }
     }
@@ -434,41 +560,77 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
     }
 }
 
-// Split-K merge for multi-chunk queries: one warp per (slot, q head), chunks merged
-// in ascending order (batch-invariant).  Single-chunk queries were written directly.
+// Split-K merge for multi-chunk queries.  Grid = one 4-warp CTA per SM (a GQA CTA
+// keeps two warps on one SM sub-partition; more combine warps resident there would
+// block the next layer's CTA from entering until the combine drains).  A warp merges
+// two (slot, q head) pairs at a time, 16 lanes x 8 dims each; chunks in ascending
+// order, eight per round trip (online max).  Single-chunk queries were written by
+// the attention kernel.
 __global__ void __launch_bounds__(128) decode_combine_kernel(const int32_t *__restrict__ lens,
                                                              const float *__restrict__ partial,
                                                              __nv_bfloat16 *__restrict__ out, int B,
                                                              int Hq, int max_chunks) {
-    griddep_wait();
+    // Trigger at once: the next layer's launch may begin its early phase (work list,
+    // K/V ring) while this combine -- and the attention launch before it -- finish.
+    // Safe because that phase reads only lens/pad/mask and cache rows other than
+    // lens-1, which neither launch writes; everything it writes waits for us.
     griddep_launch_dependents();
-    const int pair = blockIdx.x * 4 + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (pair >= B * Hq) return;
-    const int b = pair / Hq;
-    const int L = lens[b];
-    const int nch = (L + CHUNK - 1) / CHUNK;
-    if (nch <= 1) return;
-    const float *pp = partial + (size_t)pair * max_chunks * (D + PREC_PAD);
-    float Mc = -INFINITY;
-    for (int c = 0; c < nch; ++c) Mc = fmaxf(Mc, pp[c * (D + PREC_PAD) + D]);
-    float Lc = 0.f;
-    float4 Oc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int c = 0; c < nch; ++c) {
-        const float mc = pp[c * (D + PREC_PAD) + D];
-        const float f = (mc == -INFINITY) ? 0.f : ex2(mc - Mc);
-        Lc = fmaf(f, pp[c * (D + PREC_PAD) + D + 1], Lc);
-        const float4 v = *reinterpret_cast<const float4 *>(pp + c * (D + PREC_PAD) + lane * 4);
-        Oc.x = fmaf(f, v.x, Oc.x);
-        Oc.y = fmaf(f, v.y, Oc.y);
-        Oc.z = fmaf(f, v.z, Oc.z);
-        Oc.w = fmaf(f, v.w, Oc.w);
+    const int lane = threadIdx.x & 31, hl = lane & 15;
+    int gw = blockIdx.x * 4 + (threadIdx.x >> 5);
+    const int nw = gridDim.x * 4;
+    const int npairs = B * Hq;
+    constexpr int R = D + PREC_PAD, NB = 8;
+    // lens is stable since the mask update: read the first pair's before the wait
+    int pair = gw * 2 + (lane >> 4);
+    int L = pair < npairs ? lens[pair / Hq] : 0;
+    griddep_wait();
+    for (; gw * 2 < npairs; gw += nw, pair = gw * 2 + (lane >> 4), L = pair < npairs ? lens[pair / Hq] : 0) {
+        const int nch = (L + CHUNK - 1) / CHUNK;
+        if (pair >= npairs || nch <= 1) continue;
+        const float *pp = partial + (size_t)pair * max_chunks * R + hl * 8;
+        float Mc = -INFINITY, Lc = 0.f, Oc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        for (int c0 = 0; c0 < nch; c0 += NB) {
+            float m[NB], l[NB];
+            float4 va[NB], vb[NB];
+#pragma unroll
+            for (int j = 0; j < NB; ++j) {
+                const bool ok = c0 + j < nch;
+                const float *r = pp + (ok ? c0 + j : c0) * R;
+                m[j] = ok ? __ldcg(r - hl * 8 + D) : -INFINITY;
+                l[j] = ok ? __ldcg(r - hl * 8 + D + 1) : 0.f;
+                va[j] = __ldcg(reinterpret_cast<const float4 *>(r));
+                vb[j] = __ldcg(reinterpret_cast<const float4 *>(r + 4));
+            }
+            float Mn = Mc;
+#pragma unroll
+            for (int j = 0; j < NB; ++j) Mn = fmaxf(Mn, m[j]);
+            const float al = (Mc == -INFINITY) ? 0.f : ex2(Mc - Mn);
+            Lc *= al;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) Oc[i] *= al;
+#pragma unroll
+            for (int j = 0; j < NB; ++j) {
+                const float f = (m[j] == -INFINITY) ? 0.f : ex2(m[j] - Mn);
+                Lc = fmaf(f, l[j], Lc);
+                Oc[0] = fmaf(f, va[j].x, Oc[0]);
+                Oc[1] = fmaf(f, va[j].y, Oc[1]);
+                Oc[2] = fmaf(f, va[j].z, Oc[2]);
+                Oc[3] = fmaf(f, va[j].w, Oc[3]);
+                Oc[4] = fmaf(f, vb[j].x, Oc[4]);
+                Oc[5] = fmaf(f, vb[j].y, Oc[5]);
+                Oc[6] = fmaf(f, vb[j].z, Oc[6]);
+                Oc[7] = fmaf(f, vb[j].w, Oc[7]);
+            }
+            Mc = Mn;
+        }
+        const float inv = Lc > 0.f ? 1.f / Lc : 0.f;
+        uint4 w;
+        w.x = pack_bf16(Oc[0] * inv, Oc[1] * inv);
+        w.y = pack_bf16(Oc[2] * inv, Oc[3] * inv);
+        w.z = pack_bf16(Oc[4] * inv, Oc[5] * inv);
+        w.w = pack_bf16(Oc[6] * inv, Oc[7] * inv);
+        *reinterpret_cast<uint4 *>(out + (size_t)pair * D + hl * 8) = w;
     }
-    const float inv = Lc > 0.f ? 1.f / Lc : 0.f;
-    uint2 w;
-    w.x = pack_bf16(Oc.x * inv, Oc.y * inv);
-    w.y = pack_bf16(Oc.z * inv, Oc.w * inv);
-    *reinterpret_cast<uint2 *>(out + (size_t)pair * D + lane * 4) = w;
 }
 
 }  // namespace
@@ -477,19 +639,19 @@ bool gqa_supported(int q_heads, int kv_heads, int head_dim) {
     return head_dim == D && kv_heads > 0 && q_heads == GS * kv_heads;
 }
 
-template <int CW, int STAGES, int MINB>
+template <int CW, int KP, int STAGES, int MINB, int RB = 2>
 cudaError_t launch_gqa_v(const DecodeArgs &a, cudaStream_t s) {
-    constexpr int TILE = CW * KPW, THREADS = (CW + 1) * 32;
+    constexpr int TILE = CW * KP, THREADS = (CW + 1) * 32;
     static int num_sms = 0;
     if (!num_sms) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    const size_t smem = sizeof(Smem<CW, STAGES>) + 1024;
+    const size_t smem = sizeof(Smem<CW, KP, STAGES, RB>) + 1024;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(decode_gqa_kernel<CW, STAGES, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(decode_gqa_kernel<CW, KP, STAGES, RB, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
@@ -498,6 +660,12 @@ cudaError_t launch_gqa_v(const DecodeArgs &a, cudaStream_t s) {
     p.q = static_cast<const __nv_bfloat16 *>(a.q);
     p.k = static_cast<const __nv_bfloat16 *>(a.k);
     p.v = static_cast<const __nv_bfloat16 *>(a.v);
+    p.k_new = static_cast<const __nv_bfloat16 *>(a.k_new);
+    p.v_new = static_cast<const __nv_bfloat16 *>(a.v_new);
+    p.k_w = static_cast<__nv_bfloat16 *>(const_cast<void *>(a.k));
+    p.v_w = static_cast<__nv_bfloat16 *>(const_cast<void *>(a.v));
+    p.early = a.early;
+    p.trace_slot = g_trace_launch++ % TRACE_L;
     p.counters = a.counters;
     p.mask = a.mask;
     p.lens = a.lens;
@@ -518,15 +686,9 @@ cudaError_t launch_gqa_v(const DecodeArgs &a, cudaStream_t s) {
     const uint32_t box[2] = {64, TILE};
     if (!encode_bf16_map(&km, a.k, 2, dims, strides, box) || !encode_bf16_map(&vm, a.v, 2, dims, strides, box))
         return cudaErrorInvalidValue;
-    if (a.k_new) {   // a2 as its own (PDL-chained) launch before the attention
-        cudaError_t e = launch_append_kv(const_cast<void *>(a.k), const_cast<void *>(a.v), a.k_new, a.v_new,
-                                         a.lens, a.slots, a.kv_heads, a.head_dim, a.max_ctx, s);
-        if (e != cudaSuccess) return e;
-    }
-    cudaError_t e = launch_pdl(decode_gqa_kernel<CW, STAGES, MINB>, dim3(MINB * num_sms), dim3(THREADS), smem, s, km, vm, p);
+    cudaError_t e = launch_pdl(decode_gqa_kernel<CW, KP, STAGES, RB, MINB>, dim3(MINB * num_sms), dim3(THREADS), smem, s, km, vm, p);
     if (e != cudaSuccess) return e;
-    const int pairs = a.slots * a.q_heads;
-    return launch_pdl(decode_combine_kernel, dim3((pairs + 3) / 4), dim3(128), 0, s, a.lens,
+    return launch_pdl(decode_combine_kernel, dim3(num_sms), dim3(128), 0, s, a.lens,
                       (const float *)a.partial, static_cast<__nv_bfloat16 *>(a.out), a.slots,
                       a.q_heads, a.max_chunks);
 }
@@ -537,20 +699,21 @@ cudaError_t launch_decode_gqa(const DecodeArgs &a, cudaStream_t s) {
         const char *e = getenv("BATON_GQA_VARIANT");
         v = e ? atoi(e) : 0;
     }
+    // sweep variants (profiles/r01_gqa_engine_sweep.md); 0 is the default
     switch (v) {
-        case 1: return launch_gqa_v<4, 2, 2>(a, s);
-        case 2: return launch_gqa_v<2, 2, 3>(a, s);
-        case 3: return launch_gqa_v<2, 3, 2>(a, s);
-        case 4: return launch_gqa_v<1, 4, 4>(a, s);
-        case 5: return launch_gqa_v<4, 5, 1>(a, s);
-        default: return launch_gqa_v<4, 4, 1>(a, s);
+        case 1: return launch_gqa_v<4, 16, 2, 2>(a, s);      // 2 CTAs / SM
+        case 5: return launch_gqa_v<4, 16, 5, 1>(a, s);      // deeper ring
+        case 6: return launch_gqa_v<4, 32, 2, 1>(a, s);      // 2 MMA chains / warp
+        case 9: return launch_gqa_v<8, 16, 2, 1>(a, s);      // 8 consumer warps
+        case 10: return launch_gqa_v<4, 32, 3, 1, 1>(a, s);  // 2 chains, 3 stages, 1 merge buffer
+        default: return launch_gqa_v<4, 16, 4, 1>(a, s);
     }
 }
 
 }  // namespace baton
 
 // Debug only (not part of include/baton.h): switch the GQA timeline on/off and
-// copy it out ([TRACE_CTAS][TRACE_W] int64, see g_trace).
+// copy it out ([TRACE_L][TRACE_CTAS][TRACE_W] int64, see g_trace).
 extern "C" int baton_debug_gqa_trace(int on, void *host, size_t bytes) {
     if (host) {
         if (cudaMemcpyFromSymbol(host, baton::g_trace, bytes < sizeof(baton::g_trace) ? bytes : sizeof(baton::g_trace)) != cudaSuccess)
@@ -558,7 +721,7 @@ extern "C" int baton_debug_gqa_trace(int on, void *host, size_t bytes) {
     }
     if (on >= 0) {
         if (on) {
-            static long long zero[baton::TRACE_CTAS][baton::TRACE_W];
+            static long long zero[baton::TRACE_L][baton::TRACE_CTAS][baton::TRACE_W];
             cudaMemcpyToSymbol(baton::g_trace, zero, sizeof(zero));
         }
         if (cudaMemcpyToSymbol(baton::g_trace_on, &on, sizeof(int)) != cudaSuccess) return -1;

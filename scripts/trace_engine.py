@@ -1,0 +1,89 @@
+"""Timeline of consecutive GQA decode launches inside the engine's decode-step graph
+(70B shard, as in scripts/bench_configs.py), from the debug trace of decode_gqa.cu:
+per launch (layer) the first CTA entry, the median/last time the work list was
+built, the first tile ready, and the last CTA exit, relative to the first entry.
+
+    python scripts/trace_engine.py [--out gpurun_out/engine_trace.json]"""
+import argparse
+import ctypes
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "scripts"))
+import bench_configs                                                       # noqa: E402
+from paper_2410_18701_b200 import _lib                                     # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default="gpurun_out/engine_trace.json")
+    args = ap.parse_args()
+    lib = _lib._load()
+    fn = lib.baton_debug_gqa_trace
+    fn.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t]
+    hook = {}
+    orig_run = bench_configs.Engine.iteration
+
+    def iteration(self):
+        if hook.get("arm"):
+            hook["arm"] = False
+            torch.cuda.synchronize()
+            assert fn(1, None, 0) == 0
+            r = orig_run(self)
+            torch.cuda.synchronize()
+            buf = np.zeros((8, 256, 64), np.int64)
+            assert fn(0, buf.ctypes.data, buf.nbytes) == 0
+            hook["buf"] = buf
+            return r
+        return orig_run(self)
+
+    bench_configs.Engine.iteration = iteration
+    steps, warm = 6, 3
+    count = {"n": 0}
+    inner = bench_configs.Engine.iteration
+
+    def counted(self):
+        count["n"] += 1
+        if count["n"] == steps + warm:      # the last timed iteration
+            hook["arm"] = True
+        return inner(self)
+
+    bench_configs.Engine.iteration = counted
+    res = bench_configs.run("70b", steps, warm, torch.device("cuda"))
+    buf = hook["buf"]
+    t0 = buf[:, :, 0][buf[:, :, 0] > 0].min()
+    layers = []
+    for s in range(8):
+        rows = buf[s][buf[s][:, 0] > 0]
+        if not len(rows):
+            continue
+        first_ready = [r[10] for r in rows if r[3] > 0 and r[10] > 0]
+        layers.append({"enter_min": int(rows[:, 0].min() - t0), "enter_max": int(rows[:, 0].max() - t0),
+                       "built_med": float(np.median(rows[:, 1]) - t0),
+                       "first_ready_min": int(min(first_ready) - t0) if first_ready else None,
+                       "first_ready_med": float(np.median(first_ready) - t0) if first_ready else None,
+                       "exit_med": float(np.median(rows[:, 2]) - t0), "exit_max": int(rows[:, 2].max() - t0)})
+    layers.sort(key=lambda x: x["enter_min"])
+    for x in layers:
+        print(json.dumps(x))
+    print(json.dumps({"config_run": res}))
+    raw = {}
+    for s_ in range(8):
+        rows = buf[s_][buf[s_][:, 0] > 0]
+        raw[s_] = [[int(r[4]), int(r[0] - t0), int(r[1] - t0), int(r[2] - t0),
+                    [[int(r[8 + 4 * k])] + [int(x - t0) if x else 0 for x in r[9 + 4 * k:12 + 4 * k]]
+                     for k in range(min(int(r[3]), 8))],
+                    [[int(r[40 + 2 * t] - t0), int((r[41 + 2 * t] & ((1 << 62) - 1)) - t0),
+                      int(r[41 + 2 * t] >> 62)] for t in range(12) if r[40 + 2 * t]]]
+                   for r in rows]   # smid, enter, built, exit, items (w, issued, first ready, done), tile ready times
+    json.dump({"layers": layers, "raw": raw}, open(args.out, "w"))
+
+
+if __name__ == "__main__":
+    main()

@@ -192,7 +192,8 @@ def test_extract_to_pinned_host_and_back():
     assert torch.equal(Kd, K) and torch.equal(Vd, V)
 
 
-def test_early_prefetch_sees_previous_append():
+@pytest.mark.parametrize("hq,hkv", [(32, 32), (64, 8)])
+def test_early_prefetch_sees_previous_append(hq, hkv):
     """A decode launch that follows a decode launch prefetches K/V before
     griddepcontrol.wait (DecodeArgs::early).  The previous launch may have just
     written cache row lens-1 (fused append): a second, append-free launch on the
@@ -201,17 +202,17 @@ def test_early_prefetch_sees_previous_append():
     require_cuda()
     from paper_2410_18701_b200.baton import BatonShard
     torch.manual_seed(0)
-    L, B, H, D, cap = 2, 24, 32, 128, 2048
-    sh = BatonShard(L, B, H, H, D, cap)
+    L, B, D, cap = 2, 24, 128, 2048
+    sh = BatonShard(L, B, hq, hkv, D, cap)
     lens = [1 + (97 * i) % 1500 for i in range(B)]
-    ks = [torch.randn((L, H, n, D), device="cuda").to(torch.bfloat16) for n in lens]
-    vs = [torch.randn((L, H, n, D), device="cuda").to(torch.bfloat16) for n in lens]
+    ks = [torch.randn((L, hkv, n, D), device="cuda").to(torch.bfloat16) for n in lens]
+    vs = [torch.randn((L, hkv, n, D), device="cuda").to(torch.bfloat16) for n in lens]
     sh.baton_insert_many(list(range(B)), ks, vs, lens)
     for it in range(3):
         sh.baton_mask_update()
-        q = torch.randn((B, H, D), device="cuda").to(torch.bfloat16)
-        kn = torch.randn((B, H, D), device="cuda").to(torch.bfloat16)
-        vn = torch.randn((B, H, D), device="cuda").to(torch.bfloat16)
+        q = torch.randn((B, hq, D), device="cuda").to(torch.bfloat16)
+        kn = torch.randn((B, hkv, D), device="cuda").to(torch.bfloat16)
+        vn = torch.randn((B, hkv, D), device="cuda").to(torch.bfloat16)
         outs = []
         for l in range(L):
             o1 = torch.empty_like(q)
