@@ -29,6 +29,21 @@
 #include "sched.cuh"
 
 namespace baton {
+
+// Debug timeline (off unless baton_debug_mha_trace(1, ...) was called); launch l
+// writes slot l % MT_L.  Per CTA: [0] enter [1] work list built [2] consumer exit
+// [3] items [4] smid [5] producer past the wait; per item k < 6: [8+4k] w, [9+4k]
+// first copy issued, [10+4k] first tile ready, [11+4k] epilogue done.
+constexpr int MT_L = 8, MT_CTAS = 1024, MT_W = 32;
+__device__ int g_mtrace_on;
+__device__ long long g_mtrace[MT_L][MT_CTAS][MT_W];
+static int g_mtrace_launch = 0;
+BATON_DEV long long mtimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 namespace {
 
 constexpr int ROWS_PER_WARP = 16;
@@ -66,6 +81,7 @@ struct Params {
     int B, Hq, Hkv, max_ctx, max_chunks;
     float scale_log2;
     bool early;                              // prefetch before griddepcontrol.wait
+    int trace_slot;                          // debug timeline slot
 };
 
 template <int D, int CWARPS, int STAGES>
@@ -92,6 +108,14 @@ __global__ void __launch_bounds__((CWARPS + 1) * 32, MINB) decode_attention_kern
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    const bool trace = g_mtrace_on && blockIdx.x < MT_CTAS;
+    long long *tr = g_mtrace[p.trace_slot][trace ? blockIdx.x : 0];
+    if (trace && threadIdx.x == 0) {
+        tr[0] = mtimer();
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        tr[4] = smid;
+    }
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -119,6 +143,8 @@ __global__ void __launch_bounds__((CWARPS + 1) * 32, MINB) decode_attention_kern
         // ============================ producer warp ============================
         sched_build(sm.ws, p.lens, p.pad, p.B, p.Hq, lane);
         if (lane != 0) return;
+        if (trace) tr[1] = mtimer();
+        int titem = 0;
         const int total = sched_total(sm.ws, p.Hq);
         const uint64_t pol = policy_evict_first();
         int stage = 0;
@@ -131,6 +157,7 @@ __global__ void __launch_bounds__((CWARPS + 1) * 32, MINB) decode_attention_kern
             griddep_wait();
             griddep_launch_dependents();
             waited = true;
+            if (trace) tr[5] = mtimer();
             if (late_q) bulk_g2s(sm.st[late_stage].q, late_q, D * 2, &sm.full[late_stage]);
             late_q = nullptr;
         };
@@ -153,6 +180,11 @@ __global__ void __launch_bounds__((CWARPS + 1) * 32, MINB) decode_attention_kern
             // fused append (a2): the item holding row L-1 takes the new token's k/v
             // from k_new/v_new; the first q head of the kv group writes it to the cache
             const bool app = p.k_new != nullptr && c == nch - 1;
+            if (trace && titem < 6) {
+                tr[8 + 4 * titem] = w;
+                tr[9 + 4 * titem] = mtimer();
+            }
+            ++titem;
             for (int t = 0; t < ntiles; ++t) {
                 const int nr = min(TILE, rows - t * TILE);
                 const bool app_tile = app && t == ntiles - 1;
@@ -251,11 +283,13 @@ __global__ void __launch_bounds__((CWARPS + 1) * 32, MINB) decode_attention_kern
     uint32_t phase = 0;
     int rb = 0;                  // merge buffer of the current item
     uint32_t part_phase = 0;     // parity of part_bar (tracked by warp 0)
+    int citem = 0;
     while (true) {
         mbar_wait(&sm.full[stage], phase);
         Stage<D, TILE> &st = sm.st[stage];
         const StageDesc d = st.desc;
         if (d.flags & F_END) break;
+        if (trace && threadIdx.x == 0 && (d.flags & F_FIRST) && citem < 6) tr[10 + 4 * citem] = mtimer();
         if (d.flags & F_FIRST) {
             const uint4 qv = *reinterpret_cast<const uint4 *>(st.q + s * 8);
             const uint32_t qw[4] = {qv.x, qv.y, qv.z, qv.w};
@@ -400,6 +434,8 @@ __global__ void __launch_bounds__((CWARPS + 1) * 32, MINB) decode_attention_kern
                 // publish the partial: every thread arrives (release, non-blocking);
                 // warp 0 alone waits, then one gpu-scope acq_rel ticket.  The CTA that
                 // draws the last ticket merges the chunks in ascending chunk order.
+                // (Making the last chunk's item the merger instead was measured: it
+                // waits for sibling chunks still streaming -- profiles/r01_mha_trace.md.)
                 mbar_arrive(&sm.part_bar);
                 if (warp == 0) {
                     mbar_wait(&sm.part_bar, part_phase);
@@ -409,20 +445,42 @@ __global__ void __launch_bounds__((CWARPS + 1) * 32, MINB) decode_attention_kern
                     __syncwarp();
                     last = __shfl_sync(FULL_MASK, last, 0);
                     if (last) {
-                        const float *pp = p.partial + bh * p.max_chunks * (D + PREC_PAD);
+                        // two passes (global max, weighted sums); loads 8 chunks deep so
+                        // the merge costs two L2 round trips for up to 8 chunks
+                        const float *pc = p.partial + bh * p.max_chunks * (D + PREC_PAD);
+                        const int nch = d.nchunks;
                         float Mc = -INFINITY;
-                        for (int c = 0; c < d.nchunks; ++c) Mc = fmaxf(Mc, __ldcg(pp + c * (D + PREC_PAD) + D));
+                        for (int c0 = 0; c0 < nch; c0 += 8) {
+                            float mv[8];
+#pragma unroll
+                            for (int j2 = 0; j2 < 8; ++j2)
+                                mv[j2] = c0 + j2 < nch ? __ldcg(pc + (c0 + j2) * (D + PREC_PAD) + D) : -INFINITY;
+#pragma unroll
+                            for (int j2 = 0; j2 < 8; ++j2) Mc = fmaxf(Mc, mv[j2]);
+                        }
                         constexpr int NJ = (D + 31) / 32;
                         float Lc = 0.f, Oc[NJ];
 #pragma unroll
                         for (int j = 0; j < NJ; ++j) Oc[j] = 0.f;
-                        for (int c = 0; c < d.nchunks; ++c) {
-                            const float mc = __ldcg(pp + c * (D + PREC_PAD) + D);
-                            const float f = (mc == -INFINITY) ? 0.f : ex2(mc - Mc);
-                            Lc = fmaf(f, __ldcg(pp + c * (D + PREC_PAD) + D + 1), Lc);
+                        for (int c0 = 0; c0 < nch; c0 += 8) {
+                            float fv[8], lv[8], ov[8][NJ];
 #pragma unroll
-                            for (int j = 0; j < NJ; ++j)
-                                if (j * 32 + lane < D) Oc[j] = fmaf(f, __ldcg(pp + c * (D + PREC_PAD) + j * 32 + lane), Oc[j]);
+                            for (int j2 = 0; j2 < 8; ++j2) {
+                                const bool ok = c0 + j2 < nch;
+                                const float *r = pc + (ok ? c0 + j2 : 0) * (D + PREC_PAD);
+                                fv[j2] = ok ? __ldcg(r + D) : -INFINITY;
+                                lv[j2] = ok ? __ldcg(r + D + 1) : 0.f;
+#pragma unroll
+                                for (int j = 0; j < NJ; ++j)
+                                    ov[j2][j] = (ok && j * 32 + lane < D) ? __ldcg(r + j * 32 + lane) : 0.f;
+                            }
+#pragma unroll
+                            for (int j2 = 0; j2 < 8; ++j2) {
+                                const float f = (fv[j2] == -INFINITY) ? 0.f : ex2(fv[j2] - Mc);
+                                Lc = fmaf(f, lv[j2], Lc);
+#pragma unroll
+                                for (int j = 0; j < NJ; ++j) Oc[j] = fmaf(f, ov[j2][j], Oc[j]);
+                            }
                         }
                         const float inv = Lc > 0.f ? 1.f / Lc : 0.f;
 #pragma unroll
@@ -432,7 +490,13 @@ __global__ void __launch_bounds__((CWARPS + 1) * 32, MINB) decode_attention_kern
                     }
                 }
             }
+            if (trace && threadIdx.x == 0 && citem < 6) tr[11 + 4 * citem] = mtimer();
+            ++citem;
         }
+    }
+    if (trace && threadIdx.x == 0) {
+        tr[2] = mtimer();
+        tr[3] = citem;
     }
 }
 
@@ -475,6 +539,7 @@ cudaError_t launch_d(const DecodeArgs &a, cudaStream_t s) {
     p.max_chunks = a.max_chunks;
     p.scale_log2 = a.scale * 1.4426950408889634f;
     p.early = a.early;
+    p.trace_slot = g_mtrace_launch++ % MT_L;
     return launch_pdl(decode_attention_kernel<D, CW, ST, MINB>, dim3(MINB * num_sms),
                       dim3((CW + 1) * 32), smem, s, p);
 }
@@ -521,3 +586,20 @@ cudaError_t launch_decode_attention(const DecodeArgs &a, cudaStream_t s) {
 }
 
 }  // namespace baton
+
+// Debug only (not part of include/baton.h): MHA decode timeline on/off + copy out
+// ([MT_L][MT_CTAS][MT_W] int64, see g_mtrace).
+extern "C" int baton_debug_mha_trace(int on, void *host, size_t bytes) {
+    if (host) {
+        if (cudaMemcpyFromSymbol(host, baton::g_mtrace, bytes < sizeof(baton::g_mtrace) ? bytes : sizeof(baton::g_mtrace)) != cudaSuccess)
+            return -1;
+    }
+    if (on >= 0) {
+        if (on) {
+            static long long zero[baton::MT_L][baton::MT_CTAS][baton::MT_W];
+            cudaMemcpyToSymbol(baton::g_mtrace, zero, sizeof(zero));
+        }
+        if (cudaMemcpyToSymbol(baton::g_mtrace_on, &on, sizeof(int)) != cudaSuccess) return -1;
+    }
+    return 0;
+}

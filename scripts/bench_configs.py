@@ -8,6 +8,7 @@ q/k/v and prefilled K/V in HBM, then time K graph-replayed decode iterations
 (with their splices) with CUDA events.  Prints one JSON line per config with
 decode tokens/s and the attention bytes per second of the step.
 
+  7b       configs[1] (the bench.py workload; not in the default list)
   13b      configs[2] at G=1: 40 layers x 40 heads, 64 slots, 2 inserts + 2 removes/iter
   70b      one GPU's shard of configs[3]: 80 layers, 64q/8kv (GQA), 16 slots, ctx 4096
   stress   one GPU's shard of configs[4]: 7B shape, 2 -> 32 active slots, 25% preempted
@@ -30,6 +31,8 @@ from paper_2410_18701_b200.baton import baton_keygen_tokens, baton_keygen_histor
 
 
 def shard_workload(name):
+    if name == "7b":            # configs[1], the bench.py workload (for traces / A-B runs)
+        return config_workload("7b"), 512
     if name == "13b":
         return config_workload("13b", gpus=1), 256
     if name == "70b":

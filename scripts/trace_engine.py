@@ -23,9 +23,12 @@ from paper_2410_18701_b200 import _lib                                     # noq
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="gpurun_out/engine_trace.json")
+    ap.add_argument("--config", default="70b")
     args = ap.parse_args()
     lib = _lib._load()
-    fn = lib.baton_debug_gqa_trace
+    mha = args.config != "70b"
+    fn = lib.baton_debug_mha_trace if mha else lib.baton_debug_gqa_trace
+    shape = (8, 1024, 32) if mha else (8, 256, 64)
     fn.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t]
     hook = {}
     orig_run = bench_configs.Engine.iteration
@@ -37,7 +40,7 @@ def main():
             assert fn(1, None, 0) == 0
             r = orig_run(self)
             torch.cuda.synchronize()
-            buf = np.zeros((8, 256, 64), np.int64)
+            buf = np.zeros(shape, np.int64)
             assert fn(0, buf.ctypes.data, buf.nbytes) == 0
             hook["buf"] = buf
             return r
@@ -55,7 +58,7 @@ def main():
         return inner(self)
 
     bench_configs.Engine.iteration = counted
-    res = bench_configs.run("70b", steps, warm, torch.device("cuda"))
+    res = bench_configs.run(args.config, steps, warm, torch.device("cuda"))
     buf = hook["buf"]
     t0 = buf[:, :, 0][buf[:, :, 0] > 0].min()
     layers = []
@@ -76,12 +79,16 @@ def main():
     raw = {}
     for s_ in range(8):
         rows = buf[s_][buf[s_][:, 0] > 0]
+        nk = 6 if mha else 8
         raw[s_] = [[int(r[4]), int(r[0] - t0), int(r[1] - t0), int(r[2] - t0),
                     [[int(r[8 + 4 * k])] + [int(x - t0) if x else 0 for x in r[9 + 4 * k:12 + 4 * k]]
-                     for k in range(min(int(r[3]), 8))],
+                     for k in range(min(int(r[3]), nk))],
+                    [] if mha else
                     [[int(r[40 + 2 * t] - t0), int((r[41 + 2 * t] & ((1 << 62) - 1)) - t0),
-                      int(r[41 + 2 * t] >> 62)] for t in range(12) if r[40 + 2 * t]]]
-                   for r in rows]   # smid, enter, built, exit, items (w, issued, first ready, done), tile ready times
+                      int(r[41 + 2 * t] >> 62)] for t in range(12) if r[40 + 2 * t]],
+                    int(r[5] - t0) if mha and r[5] else 0]
+                   for r in rows]   # smid, enter, built, exit, items (w, issued, first ready, done),
+        #                             tile ready times (GQA), producer past the wait (MHA)
     json.dump({"layers": layers, "raw": raw}, open(args.out, "w"))
 
 
