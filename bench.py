@@ -237,14 +237,20 @@ def run_baton(args, rank, world, local_rank):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
         st = []
+        marks = []                 # one event after every iteration: per-iteration ms
         for _ in range(K_steps):
             st.append(eng.iteration())
             if per_iter:
                 per_iter(eng, warm=False)
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            marks.append(ev)
         e1.record()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        it_ms = [a.elapsed_time(b) for a, b in zip([e0] + marks[:-1], marks)]
+        timed_window.iter_ms = it_ms
         return e0.elapsed_time(e1), st
 
     # ================= pass 1: `value` -- graph-replayed decode, inputs in HBM
@@ -255,6 +261,7 @@ def run_baton(args, rank, world, local_rank):
     time.sleep(0.3)
     clocks.mark("t_start")
     ms, stats = timed_window(eng)
+    iter_ms = list(timed_window.iter_ms)
     clocks.mark("t_end")
     clk = clocks.stop()
     release(eng)
@@ -428,6 +435,7 @@ def run_baton(args, rank, world, local_rank):
 
     return dict(splice_bytes=splice_bytes, splice_s=splice_s, splice_calls=len(splice_ev),
                 ms=ms, tokens=tokens, attn_bytes=attn_bytes_total, attn_time_s=attn_time_s,
+                iter_ms=iter_ms,
                 attn_launches=attn_launches, splice_rows=splice_rows, tau=tau, L=L,
                 n_launch=n_launch, clocks=clk, e2e=e2e, iters=K_steps,
                 live_slots=tokens / K_steps, live_rows=live_rows)
@@ -552,6 +560,7 @@ def main():
             "steps": args.steps,
             "warmup": args.warmup,
             "ms_per_step": ms / args.steps,
+            "iter_ms_p10_p50_p90": [float(x) for x in np.percentile(r["iter_ms"], [10, 50, 90])],
             "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": None,
