@@ -22,6 +22,9 @@ Operations (each cites the passage it follows):
 * ``step``     P:L96  append one mask column (1 for live rows) and one KV column,
                then masked attention for every live row (via O-1 on the
                row's live columns gathered in ascending order).
+* ``shape_step`` P:L101-113 the vector-SHAPING iteration (Baton without P&D):
+               raw queries join with their whole prompt, every row's input is
+               padded to the common width W (reading C4: mask and KV grow by W).
 * ``insert``   P:L137 vector embedding: case l_q <= S end-aligned, front S-l_q
                placeholders; case l_q > S expand every row on the LEFT by l_q-S
                (KV fill, mask 0 for existing rows, 1 for the new query).
@@ -150,6 +153,65 @@ class Shard:
             for l in range(self.L):
                 out[l, b] = solo_attention(q[l, b], self.K[l, b][:, live, :],
                                            self.V[l, b][:, live, :])
+        return out
+
+    # ------------------------------------------------------------------ P:L101-113
+    def shape_step(self, new=(), q=None, k_new=None, v_new=None):
+        """One iteration of the vector-SHAPING path (Baton without P&D, NEXT-1).
+
+        ``new`` lists (slot, qid, l_q) raw queries inserted now: their rows must be
+        empty (the finished query's row was removed: "set all the values of the
+        query^2 part of the current attention_mask tensor to 0").  The
+        input width is W = max(1, max l_q): "pad the latest token of query^0 and
+        query^1 to the same length as query^3".
+          * surviving rows append mask [1, 0^(W-1)] ("appended with values of 0
+            according to the padding", P:L105);
+          * a new row appends "an all-1 vector with the same length of query^3"
+            (P:L105), then 0^(W-l_q) if another insert is longer;
+          * every row appends W KV columns (reading C4: mask and KV both grow by
+            the input width); padding tokens' KV cells are placeholders (fill).
+        Input token t of row b attends to the columns j with mask 1 and
+        j <= S_old + t (the new query's prefill is causal within its block;
+        a survivor's real token is t = 0, so it is an ordinary decode).
+
+        q: [L][B][W][H_q][D]; k_new, v_new: [L][B][W][H_kv][D] (only real tokens
+        are read).  Returns o: [L][B][W][H_q][D], zero on padding tokens and empty
+        rows (their GPU rows are the bubble of P:L128), or None (metadata mode)."""
+        new = [(int(s), int(qd), int(l)) for s, qd, l in new]
+        W = max([1] + [l for _, _, l in new])
+        if self.S + W > self.S_cap:
+            raise Capacity("S would exceed capacity")
+        for s, _, l in new:
+            if self.qid[s] >= 0:
+                raise SlotBusy(f"slot {s} occupied")
+            if l < 1:
+                raise Capacity(f"l_q={l}")
+        S0 = self.S
+        survivors = [b for b in range(self.B) if self.qid[b] >= 0]
+        real = np.zeros((self.B, W), dtype=bool)          # real input tokens
+        for b in survivors:
+            real[b, 0] = True
+        for s, qd, l in new:
+            real[s, :l] = True
+            self.qid[s] = qd
+            self.pad[s] = S0                               # its live region starts here
+        self.mask = np.concatenate([self.mask, real.astype(np.uint8)], axis=1)
+        self.S = S0 + W
+        if not self.kv:
+            return None
+        kc = np.full((self.L, self.B, self.H_kv, W, self.D), self.fill)
+        vc = np.full((self.L, self.B, self.H_kv, W, self.D), self.fill)
+        for b, t in zip(*np.nonzero(real)):
+            kc[:, b, :, t, :] = k_new[:, b, t]
+            vc[:, b, :, t, :] = v_new[:, b, t]
+        self.K = np.concatenate([self.K, kc], axis=3)
+        self.V = np.concatenate([self.V, vc], axis=3)
+        out = np.zeros((self.L, self.B, W, self.H_q, self.D), dtype=np.float64)
+        for b, t in zip(*np.nonzero(real)):
+            live = np.nonzero(self.mask[b, :S0 + t + 1])[0]   # masked columns never enter
+            for l in range(self.L):
+                out[l, b, t] = solo_attention(q[l, b, t], self.K[l, b][:, live, :],
+                                              self.V[l, b][:, live, :])
         return out
 
     # ------------------------------------------------------------------ P:L105-107

@@ -22,6 +22,14 @@ P:L101 and P:L124, DESIGN.md §3 C5):
                  (C20).  A stored (preempted) query is eligible only for slots of
                  the shard holding its stored K/V (C20b); a fresh query for any.
 
+Policy ``"shape"`` (the vector-SHAPING path, Baton without P&D, P:L101-113;
+NEXT-1): step 6 only reserves the lowest free slot for a RAW query; step 1 of the
+next iteration is ``Shard.shape_step``, whose input width is the longest reserved
+prompt.  That iteration is the new query's prefill (it yields its first token,
+C9), so its A decode iterations follow it; everybody else decodes as usual in the
+same padded iteration (the bubble of P:L128).  Control events are not used with
+this policy.
+
 Iteration 0 runs only step 6.  A query's tokens are keyed by (qid, position) so a
 decode step of a query with live length n (after the append) handles position
 n-1 (C3); its prefilled K/V are positions [0, l_q).
@@ -48,6 +56,8 @@ class IterationRecord:
     resized: Optional[int] = None
     moved: List[Tuple[int, int]] = field(default_factory=list)           # (old gslot, new gslot)
     inserted: List[Tuple[int, int, int]] = field(default_factory=list)   # (gslot, qid, l_q)
+    prefilled: List[Tuple[int, int, int]] = field(default_factory=list)  # (gslot, qid, l_q), shape
+    width: List[int] = field(default_factory=list)                       # input width per shard
     S: List[int] = field(default_factory=list)
     pad: List[np.ndarray] = field(default_factory=list)
     qid: List[np.ndarray] = field(default_factory=list)
@@ -56,7 +66,9 @@ class IterationRecord:
 
 class Simulator:
     def __init__(self, wl, G=None, kv=False, fill=0.0, release=True, keep_outputs=False,
-                 snapshot_masks=False):
+                 snapshot_masks=False, policy="pd"):
+        assert policy in ("pd", "shape")
+        self.policy = policy
         self.wl = wl
         self.G = G or wl.gpus
         assert wl.slots % self.G == 0
@@ -76,6 +88,10 @@ class Simulator:
         self.outputs: Dict[Tuple[int, int], np.ndarray] = {}
         self.masks: List[List[np.ndarray]] = []
         self.finished_at = {}
+        self.pending = [[] for _ in range(self.G)]   # shape policy: reserved (b, qid, l_q)
+        if policy == "shape":
+            c = wl.control
+            assert not (c.preempt or c.preempt_frac or c.resize), "shape policy: no control events"
         self.t = 0
 
     # ------------------------------------------------------------------ helpers
@@ -117,9 +133,64 @@ class Simulator:
         return (qid, length, K, V, r)
 
     # ------------------------------------------------------------------ phases
+    def _token_qkv(self, qids, pos):
+        """q/k/v of one token per slot (keyed by (qid, position)): [L][B][H][D]."""
+        wl = self.wl
+        return [np.stack([bf16_bits_to_f64(query_token_bits(
+            wl.seed, kind, l, qids, pos, H, wl.head_dim, scale)) for l in range(wl.layers)])
+            for kind, H, scale in ((KIND_Q, wl.q_heads, wl.scales[0]),
+                                   (KIND_K, wl.kv_heads, wl.scales[1]),
+                                   (KIND_V, wl.kv_heads, wl.scales[2]))]
+
+    def _shape_decode(self, r, sh, rec):
+        """one padded iteration of width W on shard r."""
+        wl = self.wl
+        new = self.pending[r]
+        self.pending[r] = []
+        W = max(l for _, _, l in new)
+        occ = sh.occupied()
+        lens = sh.lens()
+        o = None
+        if self.kv:
+            shp = lambda H: np.zeros((wl.layers, self.Bg, W, H, wl.head_dim))
+            q, k, v = shp(wl.q_heads), shp(wl.kv_heads), shp(wl.kv_heads)
+            # survivors: their decode token at input position 0
+            qids = np.zeros(self.Bg, np.int64)
+            pos = np.zeros(self.Bg, np.int64)
+            for b in occ:
+                qids[b], pos[b] = sh.qid[b], lens[b]
+            tq, tk, tv = self._token_qkv(qids, pos)
+            for b in occ:
+                q[:, b, 0], k[:, b, 0], v[:, b, 0] = tq[:, b], tk[:, b], tv[:, b]
+            # new queries: their whole prompt, positions 0..l_q-1
+            for b, qd, l in new:
+                for t in range(l):
+                    tq, tk, tv = self._token_qkv(np.full(self.Bg, qd), np.full(self.Bg, t))
+                    q[:, b, t], k[:, b, t], v[:, b, t] = tq[:, b], tk[:, b], tv[:, b]
+            o = sh.shape_step(new, q, k, v)
+        else:
+            sh.shape_step(new)
+        rec.width[r] = W
+        for b in occ:
+            g = r * self.Bg + b
+            qid = int(sh.qid[b])
+            rec.decoded.append((g, qid, int(lens[b])))
+            if self.keep_outputs and o is not None:
+                self.outputs[(qid, int(lens[b]))] = o[:, b, 0].copy()
+            self.generated[qid] += 1
+        for b, qd, l in new:
+            rec.prefilled.append((r * self.Bg + b, qd, l))
+            if self.keep_outputs and o is not None:
+                for t in range(l):
+                    self.outputs[(qd, t)] = o[:, b, t].copy()
+
     def _decode(self, rec):
         wl = self.wl
+        rec.width = [1] * self.G
         for r, sh in enumerate(self.shards):
+            if self.pending[r]:
+                self._shape_decode(r, sh, rec)
+                continue
             occ = sh.occupied()
             if not occ:
                 sh.step() if not self.kv else sh.step(*self._zeros_qkv())
@@ -228,8 +299,9 @@ class Simulator:
             self.queue.append((q.qid, q.l_q, None, None, None))
         a = self.active_per_shard()
         while self.queue:
+            reserved = {r * self.Bg + b for r in range(self.G) for b, _, _ in self.pending[r]}
             free = [r * self.Bg + b for r, sh in enumerate(self.shards) for b in range(a)
-                    if sh.qid[b] < 0]
+                    if sh.qid[b] < 0 and r * self.Bg + b not in reserved]
             if not free:
                 break
             pick = None
@@ -244,6 +316,12 @@ class Simulator:
             i, g = pick
             qid, length, K, V, _ = self.queue[i]
             del self.queue[i]
+            if self.policy == "shape":          # raw query: prefilled in the next iteration
+                r, b = self._loc(g)
+                self.pending[r].append((b, qid, length))
+                self.inserted_at[qid] = self.t
+                rec.inserted.append((g, qid, length))
+                continue
             if self.kv and K is None:
                 K, V = self._prefill(qid, length)
             r, b = self._loc(g)
@@ -255,7 +333,8 @@ class Simulator:
     def done(self):
         if self.wl.iterations >= 0 and self.t >= self.wl.iterations:
             return True
-        return (not self.arrivals and not self.queue and not self._live())
+        return (not self.arrivals and not self.queue and not self._live()
+                and not any(self.pending))
 
     def iteration(self):
         rec = IterationRecord(self.t)
