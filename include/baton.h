@@ -207,6 +207,39 @@ int  baton_compact(baton_state *st, int n_active, int32_t *old_to_new, void *str
 int  baton_prefill_attention(const void *q, const void *k, const void *v, void *out, int len,
                              const baton_shape *shape, float scale, void *stream);
 
+/* ---------------------------------------------------------------- NEXT-1
+ * The vector-SHAPING iteration: Baton WITHOUT P&D decoupling (the
+ * "Ours" column of the paper's Table 2 ablation).  Raw queries join the
+ * batch with their whole prompt; "to align the dimensions of IT, it is necessary
+ * to pad the latest token of query^0 and query^1 to the same length as query^3"
+ * (P:L103).  One call = one iteration of input width W over all layers:
+ *   - every occupied slot (survivor) inputs its decode token at t = 0 and W-1
+ *     padding tokens: mask columns [S, S+W) := 1 0^(W-1) ("appended with values
+ *     of 0 according to the padding"), lens += W;
+ *   - every new slot (must be empty, i.e. removed: its row is already zero)
+ *     inputs its prompt, l = new_lens[i] <= W tokens: mask row := 0^S 1^l 0^(W-l),
+ *     pad = S (its live region starts here), lens = W;
+ *   - S += W (reading C4: mask and KV both grow by the input width);
+ *   - K/V rows [lens_before, lens_before + W) of each slot := k_new/v_new rows;
+ *   - for every slot and input token t: attention over the slot's cache rows
+ *     r <= (lens_before + t) with mask 1 (causal inside the new block), on the
+ *     tensor cores (the a8 kernel with a per-slot prefix and the mask).  Rows of
+ *     padding tokens are computed too: that is the bubble the paper measures
+ *     ("even other queries that are already in the decoding phase will
+ *     also have the same overhead").
+ *   W >= max(1, max new_lens); head_dim must be 128.
+ *   new_slots, new_lens : HOST int32[n_new]
+ *   q, out       : device bf16 [layers][slots][q_heads][W][head_dim]
+ *   k_new, v_new : device bf16 [layers][slots][kv_heads][W][head_dim]; rows of
+ *                  padding tokens are stored (masked) and must be finite
+ *   Empty slots produce zero output rows.  Host mirror and device metadata are
+ *   updated like a1 (no baton_mask_update for this iteration).
+ * Errors: BATON_E_INVALID, BATON_E_SLOT_BUSY (a new slot is occupied),
+ *         BATON_E_CAPACITY (new_lens out of [1, W], or S + W > max_ctx). */
+int  baton_shape_step(baton_state *st, int W, int n_new, const int32_t *new_slots,
+                      const int32_t *new_lens, const void *q, const void *k_new, const void *v_new,
+                      void *out, void *stream);
+
 /* ---------------------------------------------------------------- misc */
 const char *baton_error_string(int code);
 /* The cudaError_t of the last BATON_E_CUDA returned on this thread. */

@@ -156,6 +156,15 @@ class BatonShard:
                                     _stream(stream)), "baton_decode_step")
         return out
 
+    def baton_shape_step(self, W, new_slots, new_lens, q, k_new, v_new, out, stream=None):
+        """NEXT-1: one vector-shaping iteration of width W (include/baton.h).
+        q/out [L][slots][q_heads][W][D]; k_new/v_new [L][slots][kv_heads][W][D]."""
+        new_slots, new_lens = list(new_slots), list(new_lens)
+        check(lib.baton_shape_step(self._h, int(W), len(new_slots), _i32(new_slots), _i32(new_lens),
+                                   _ptr(q), _ptr(k_new), _ptr(v_new), _ptr(out), _stream(stream)),
+              "baton_shape_step")
+        return out
+
     def baton_decode_attention(self, layer, q, out, scale=None, stream=None, use_mask=True):
         ws = baton_decode_workspace_bytes(self.shape)
         off = self.workspace.numel() - ws

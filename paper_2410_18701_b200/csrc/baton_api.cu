@@ -303,6 +303,80 @@ int baton_decode_step(baton_state *st, const void *q, const void *k_new, const v
     return BATON_OK;
 }
 
+// ---------------------------------------------------------------- NEXT-1
+// The vector-SHAPING iteration (Baton without P&D): raw queries join
+// with their whole prompt and every row's input is padded to width W.
+int baton_shape_step(baton_state *st, int W, int n_new, const int32_t *new_slots, const int32_t *new_lens,
+                     const void *q, const void *k_new, const void *v_new, void *out, void *stream) {
+    if (st) st->prev_decode = false;
+    if (!st || W < 1 || n_new < 0 || !q || !k_new || !v_new || !out) return BATON_E_INVALID;
+    if (n_new > 0 && (!new_slots || !new_lens)) return BATON_E_INVALID;
+    const baton_shape &s = st->sh;
+    if (!prefill_supported(s.head_dim)) return BATON_E_INVALID;
+    std::vector<int> newlen(s.slots, 0);
+    for (int i = 0; i < n_new; ++i) {
+        const int b = new_slots[i];
+        if (b < 0 || b >= s.slots || newlen[b]) return BATON_E_INVALID;
+        if (st->occ[b]) return BATON_E_SLOT_BUSY;
+        if (new_lens[i] < 1 || new_lens[i] > W) return BATON_E_CAPACITY;
+        newlen[b] = new_lens[i];
+    }
+    if (st->S + W > s.max_ctx) return BATON_E_CAPACITY;
+    const int S0 = st->S;
+    std::vector<MaskOp> ops;
+    std::vector<CopyJob> jobs;
+    const size_t slot_elems = (size_t)s.kv_heads * s.max_ctx * s.head_dim;
+    for (int b = 0; b < s.slots; ++b) {
+        int row0;
+        if (st->occ[b]) {            // survivor: its token at column S0, then W-1 padding
+            ops.push_back({MOP_SET_CELL, b, S0, 0});
+            row0 = st->lens[b];
+            st->lens[b] += W;
+        } else if (newlen[b]) {      // new raw query: row := 0^S0 1^l 0^(W-l)
+            ops.push_back({MOP_SET_ROW, b, S0, S0 + newlen[b]});
+            row0 = 0;
+            st->occ[b] = 1;
+            st->pad[b] = S0;
+            st->lens[b] = W;
+        } else {
+            continue;
+        }
+        // the W input tokens' K/V rows (reading C4: the cache grows by W as well)
+        CopyJob j;
+        const size_t src0 = (size_t)b * s.kv_heads * W * s.head_dim;
+        j.src_k = static_cast<const __nv_bfloat16 *>(k_new) + src0;
+        j.src_v = static_cast<const __nv_bfloat16 *>(v_new) + src0;
+        j.dst_k = static_cast<__nv_bfloat16 *>(st->cfg.k_cache) + b * slot_elems + (size_t)row0 * s.head_dim;
+        j.dst_v = static_cast<__nv_bfloat16 *>(st->cfg.v_cache) + b * slot_elems + (size_t)row0 * s.head_dim;
+        j.src_hs = (int64_t)W * s.head_dim;
+        j.src_ls = j.src_hs * s.kv_heads * s.slots;
+        j.dst_hs = (int64_t)s.max_ctx * s.head_dim;
+        j.dst_ls = (int64_t)st->layer_elems;
+        j.rows = W;
+        j.pad_ = 0;
+        jobs.push_back(j);
+    }
+    st->S = S0 + W;
+    cudaStream_t cs = as_stream(stream);
+    int r = push_meta(st, ops, cs);
+    if (r) return r;
+    for (size_t i0 = 0; i0 < jobs.size(); i0 += MAX_SPLICE_JOBS) {
+        const int nj = (int)std::min(jobs.size() - i0, (size_t)MAX_SPLICE_JOBS);
+        r = cuda_status(launch_kv_copy(jobs.data() + i0, nj, s.layers, s.kv_heads, s.head_dim, cs));
+        if (r) return r;
+    }
+    const size_t qstride = (size_t)s.slots * s.q_heads * W * s.head_dim;
+    const float scale = 1.0f / sqrtf((float)s.head_dim);
+    for (int l = 0; l < s.layers; ++l) {
+        r = cuda_status(launch_extend_attention(
+            static_cast<const __nv_bfloat16 *>(q) + l * qstride, layer_ptr(st->cfg.k_cache, st, l),
+            layer_ptr(st->cfg.v_cache, st, l), static_cast<__nv_bfloat16 *>(out) + l * qstride, W, s.slots,
+            s.q_heads, s.kv_heads, s.head_dim, s.max_ctx, st->d_lens, st->d_pad, st->cfg.mask, scale, cs));
+        if (r) return r;
+    }
+    return BATON_OK;
+}
+
 // ---------------------------------------------------------------- a4
 int baton_remove(baton_state *st, const int32_t *slots, int n, int32_t *released, void *stream) {
     if (st) st->prev_decode = false;

@@ -48,9 +48,11 @@ cudaError_t launch_append_kv(void *k_layer, void *v_layer, const void *k_new, co
                              const int32_t *lens, int slots, int kv_heads, int head_dim,
                              int max_ctx, cudaStream_t s);
 
-enum MaskOpKind : int32_t { MOP_ZERO_ROW = 0, MOP_SHIFT_LEFT = 1, MOP_SHIFT_RIGHT = 2, MOP_SET_ROW = 3 };
+enum MaskOpKind : int32_t { MOP_ZERO_ROW = 0, MOP_SHIFT_LEFT = 1, MOP_SHIFT_RIGHT = 2, MOP_SET_ROW = 3,
+                            MOP_SET_CELL = 4 };
 struct MaskOp {
-    int32_t kind, slot, a, b;   // ZERO_ROW(slot); SHIFT_LEFT(a=p); SHIFT_RIGHT(a=e); SET_ROW(slot, a=pad, b=S)
+    int32_t kind, slot, a, b;   // ZERO_ROW(slot); SHIFT_LEFT(a=p); SHIFT_RIGHT(a=e); SET_ROW(slot, a=pad, b=S);
+                                // SET_CELL(slot, a=column): that one column := 1
 };
 // Applies `ops` in order to every mask row, then writes S/lens/pad (host values) to the device.
 cudaError_t launch_mask_splice(uint8_t *mask, int slots, int max_ctx, const MaskOp *ops, int nops,
@@ -80,6 +82,14 @@ bool prefill_supported(int head_dim);
 cudaError_t launch_prefill_attention(const void *q, const void *k, const void *v, void *out, int len,
                                      int q_heads, int kv_heads, int head_dim, float scale,
                                      cudaStream_t s);
+// NEXT-1 (vector shaping): attention of the W input tokens of every slot over the
+// slot's cache rows [0, lens_b - W + t] where the mask is 1 (prefill_attention.cu).
+// q/out: [slots][q_heads][W][128]; k/v_layer: one layer of the cache; lens/pad: the
+// device metadata after the shaped mask update.
+cudaError_t launch_extend_attention(const void *q, const void *k_layer, const void *v_layer, void *out,
+                                    int W, int slots, int q_heads, int kv_heads, int head_dim, int max_ctx,
+                                    const int32_t *lens, const int32_t *pad, const uint8_t *mask,
+                                    float scale, cudaStream_t s);
 
 // ------------------------------------------------------------ harness generator
 cudaError_t launch_keygen_tokens(void *out, const int32_t *qids, const int32_t *pos, int layers,

@@ -72,13 +72,15 @@ __global__ void mask_splice_kernel(const __grid_constant__ MaskSpliceParams p) {
     __syncthreads();
     for (int i = 0; i < p.nops; ++i) {
         const MaskOp op = p.ops[i];
-        if ((op.kind == MOP_ZERO_ROW || op.kind == MOP_SET_ROW) && op.slot != b) continue;
+        if ((op.kind == MOP_ZERO_ROW || op.kind == MOP_SET_ROW || op.kind == MOP_SET_CELL) && op.slot != b)
+            continue;
         for (int j = threadIdx.x; j < p.max_ctx; j += blockDim.x) {
             uint8_t val;
             switch (op.kind) {
                 case MOP_ZERO_ROW: val = 0; break;
                 case MOP_SHIFT_LEFT: val = (j + op.a < p.max_ctx) ? cur[j + op.a] : 0; break;
                 case MOP_SHIFT_RIGHT: val = (j >= op.a) ? cur[j - op.a] : 0; break;
+                case MOP_SET_CELL: val = (j == op.a) ? 1 : cur[j]; break;
                 default: val = (j >= op.a && j < op.b) ? 1 : 0; break;
             }
             nxt[j] = val;

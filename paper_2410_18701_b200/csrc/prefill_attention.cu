@@ -17,6 +17,14 @@
 //   warps 0-3 softmax: thread = query row; tcgen05.ld of its S row, causal mask,
 //            online max/sum (exp2), P -> bf16 into the K-major SW128 smem layout
 //            the next MMA reads, O rescale in TMEM (tcgen05.ld/st), epilogue.
+//
+// The same kernel runs the EXTEND attention of a vector-shaping iteration
+// (NEXT-1, launch_extend_attention): a CTA per (slot, q head, query
+// tile); query row t of slot b is input token t of width W, its keys are the
+// slot's cache rows 0 .. off_b + t (off_b = lens_b - W, the rows before this
+// iteration), and a key is also dropped where the paper's attention_mask is 0 (the
+// mask bytes of each key tile ride in the V stage, which outlives the softmax of
+// that tile).  Prefill is the case of one slot, off = 0 and no mask.
 #include <cuda.h>
 
 #include "common.cuh"
@@ -41,6 +49,7 @@ struct __align__(1024) PfSmem {
     uint8_t k[KV_BYTES];
     uint8_t v[2][KV_BYTES];
     uint8_t p[P_BYTES];
+    uint8_t mk[2][PF_N + 16];       // extend: mask bytes of the V stage's key tile
     uint64_t bar_q, k_full, k_empty, v_full[2], v_empty[2], s_full, s_free, p_full, o_done;
     uint32_t tmem_base;
 };
@@ -118,11 +127,16 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int b_mn_major) 
 }
 
 struct PfParams {
-    int Hq, Hkv, len, n_mtiles;
+    int Hq, Hkv, len, n_mtiles;     // len = query rows per (slot, head): prompt length or W
     float scale_log2;
     __nv_bfloat16 *out;
+    // extend only (lens == nullptr for prefill)
+    const int32_t *lens, *pad;      // device metadata AFTER the shaped mask update
+    const uint8_t *mask;            // [slots][max_ctx]
+    int max_ctx;
 };
 
+template <bool EXT>
 __global__ void __launch_bounds__(PF_THREADS, 2)
 prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                          const __grid_constant__ CUtensorMap tm_v, const PfParams p) {
@@ -131,10 +145,28 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // heavy tiles (near the diagonal end) first
     const int mt = p.n_mtiles - 1 - (int)(blockIdx.x % p.n_mtiles);
-    const int h = blockIdx.x / p.n_mtiles;
+    const int h = (blockIdx.x / p.n_mtiles) % p.Hq;
+    const int b = blockIdx.x / (p.n_mtiles * p.Hq);           // slot (extend), 0 (prefill)
     const int g = h * p.Hkv / p.Hq;
     const int q0 = mt * PF_M;
-    const int n_kt = (min(q0 + PF_M, p.len) + PF_N - 1) / PF_N;   // key tiles up to the diagonal
+    constexpr bool ext = EXT;
+    int off = 0, kpad = 0;
+    if (ext) {
+        const int lb = p.lens[b];
+        if (lb <= 0) {   // empty slot: zero output rows, nothing else
+            for (int i = threadIdx.x; i < PF_M * PF_D / 8; i += PF_THREADS) {
+                const int r = q0 + i / (PF_D / 8);
+                if (r < p.len)
+                    reinterpret_cast<uint4 *>(p.out + (((size_t)b * p.Hq + h) * p.len + r) * PF_D)[i % (PF_D / 8)] =
+                        make_uint4(0, 0, 0, 0);
+            }
+            return;
+        }
+        off = lb - p.len;
+        kpad = p.pad[b];
+    }
+    const int qrow = b * p.Hq + h, krow = b * p.Hkv + g;        // outer coordinate of the maps
+    const int n_kt = (off + min(q0 + PF_M, p.len) + PF_N - 1) / PF_N;   // key tiles up to the diagonal
 
     if (threadIdx.x == 0) {
         mbar_init(&sm.bar_q, 1);
@@ -168,18 +200,29 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
             prefetch_tmap(&tm_k);
             prefetch_tmap(&tm_v);
             mbar_arrive_expect_tx(&sm.bar_q, Q_BYTES);
-            tma_load_3d(sm.q, &tm_q, 0, q0, h, &sm.bar_q);
-            tma_load_3d(sm.q + Q_REGION, &tm_q, 64, q0, h, &sm.bar_q);
+            tma_load_3d(sm.q, &tm_q, 0, q0, qrow, &sm.bar_q);
+            tma_load_3d(sm.q + Q_REGION, &tm_q, 64, q0, qrow, &sm.bar_q);
             for (int j = 0; j < n_kt; ++j) {
                 if (j > 0) mbar_wait(&sm.k_empty, (j - 1) & 1);          // S(j-1) done with K
                 mbar_arrive_expect_tx(&sm.k_full, KV_BYTES);
-                tma_load_3d(sm.k, &tm_k, 0, j * PF_N, g, &sm.k_full);
-                tma_load_3d(sm.k + KV_REGION, &tm_k, 64, j * PF_N, g, &sm.k_full);
+                tma_load_3d(sm.k, &tm_k, 0, j * PF_N, krow, &sm.k_full);
+                tma_load_3d(sm.k + KV_REGION, &tm_k, 64, j * PF_N, krow, &sm.k_full);
                 const int s = j & 1;
                 if (j >= 2) mbar_wait(&sm.v_empty[s], ((j >> 1) + 1) & 1);   // PV(j-2) done
-                mbar_arrive_expect_tx(&sm.v_full[s], KV_BYTES);
-                tma_load_3d(sm.v[s], &tm_v, 0, j * PF_N, g, &sm.v_full[s]);
-                tma_load_3d(sm.v[s] + KV_REGION, &tm_v, 64, j * PF_N, g, &sm.v_full[s]);
+                uint32_t mbytes = 0;
+                size_t a0 = 0;
+                if (ext) {   // aligned superset of the tile's mask bytes (rows start 16-B aligned)
+                    const size_t row0 = (size_t)b * p.max_ctx;
+                    const size_t j0 = row0 + kpad + j * PF_N;
+                    a0 = j0 & ~(size_t)15;
+                    size_t need = (j0 + PF_N - a0 + 15) & ~(size_t)15;
+                    if (a0 + need > row0 + p.max_ctx) need = row0 + p.max_ctx - a0;
+                    mbytes = (uint32_t)need;
+                }
+                mbar_arrive_expect_tx(&sm.v_full[s], KV_BYTES + mbytes);
+                tma_load_3d(sm.v[s], &tm_v, 0, j * PF_N, krow, &sm.v_full[s]);
+                tma_load_3d(sm.v[s] + KV_REGION, &tm_v, 64, j * PF_N, krow, &sm.v_full[s]);
+                if (mbytes) bulk_g2s(sm.mk[s], p.mask + a0, mbytes, &sm.v_full[s]);
             }
         }
     } else if (warp == 5) {
@@ -229,11 +272,14 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
         const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
         float m = -INFINITY, l = 0.f;
         uint32_t pk[32];                              // P row (64 keys) packed bf16x2
+        const int mrow = ext ? (int)(((size_t)b * p.max_ctx + kpad) & 15) : 0;   // mask byte offset
         for (int j = 0; j < n_kt; ++j) {
             mbar_wait(&sm.s_full, j & 1);
             tc_fence_after();
             const int kbase = j * PF_N;
-            const bool diag = kbase + PF_N > q0;      // tile touches the causal diagonal
+            const bool diag = kbase + PF_N > off + q0;   // tile touches the causal diagonal
+            const uint8_t *mk = sm.mk[j & 1] + mrow;
+            if (ext) mbar_wait(&sm.v_full[j & 1], (j >> 1) & 1);   // this tile's mask bytes
             uint32_t r[2][32];
             tmem_ld32(tS + lane_off, r[0]);
             tmem_ld32(tS + lane_off + 32, r[1]);
@@ -246,19 +292,23 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
                     float x = __uint_as_float(r[c][i]) * p.scale_log2;
-                    if (diag && kbase + c * 32 + i > qi) x = -INFINITY;
+                    if (diag && kbase + c * 32 + i > off + qi) x = -INFINITY;
+                    if (ext && mk[c * 32 + i] == 0) x = -INFINITY;
                     r[c][i] = __float_as_uint(x);
                     mx = fmaxf(mx, x);
                 }
             const float m_new = fmaxf(m, mx);
-            const float alpha = ex2(m - m_new);
+            // a row may see only masked keys so far (extend: holes, padding): keep
+            // exp2 finite -- ex2(-inf - 0) = 0
+            const float mref = (m_new == -INFINITY) ? 0.f : m_new;
+            const float alpha = ex2(m - mref);
             float rs = 0.f;
 #pragma unroll
             for (int c = 0; c < 2; ++c)
 #pragma unroll
                 for (int i = 0; i < 32; i += 2) {
-                    const float e0 = ex2(__uint_as_float(r[c][i]) - m_new);
-                    const float e1 = ex2(__uint_as_float(r[c][i + 1]) - m_new);
+                    const float e0 = ex2(__uint_as_float(r[c][i]) - mref);
+                    const float e1 = ex2(__uint_as_float(r[c][i + 1]) - mref);
                     const __nv_bfloat162 b = __floats2bfloat162_rn(e0, e1);
                     // the PV MMA consumes bf16 P: accumulate the sum of what it multiplies
                     rs += __low2float(b) + __high2float(b);
@@ -283,6 +333,17 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
                     tmem_wait_st();
                 }
             }
+            // extend: cache rows past lens in this tile are stale memory (maybe NaN
+            // bits); P is 0 there but 0 * NaN is not, so zero those V rows (whole 128-B
+            // rows of both halves, swizzle-independent) before the P.V MMA reads them
+            if (ext && kbase + PF_N > off + p.len) {
+                const int first = off + p.len - kbase;
+                for (int i = row; i < (PF_N - first) * 16; i += 128) {
+                    const int rr = first + i / 16, ch = i % 16;
+                    *reinterpret_cast<uint4 *>(sm.v[j & 1] + (ch >> 3) * KV_REGION + rr * 128 + (ch & 7) * 16) =
+                        make_uint4(0, 0, 0, 0);
+                }
+            }
             // P row -> smem, K-major SWIZZLE_128B: 64 keys = one 128-B row, 16-B chunk c
             // of row r at chunk position c ^ (r & 7)
 #pragma unroll
@@ -297,8 +358,8 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
         // epilogue: O / l -> bf16
         mbar_wait(&sm.o_done, (n_kt - 1) & 1);
         tc_fence_after();
-        const float inv = 1.f / l;
-        __nv_bfloat16 *orow = p.out + ((size_t)h * p.len + qi) * PF_D;
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        __nv_bfloat16 *orow = p.out + ((size_t)qrow * p.len + qi) * PF_D;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             uint32_t o[32];
@@ -337,6 +398,26 @@ bool make_map(CUtensorMap *m, const void *base, int heads, int len, int box_rows
 
 bool prefill_supported(int head_dim) { return head_dim == PF_D; }
 
+namespace {
+cudaError_t launch_pf(const CUtensorMap &mq, const CUtensorMap &mk, const CUtensorMap &mv, const PfParams &p,
+                      int slots, cudaStream_t s) {
+    const size_t smem = sizeof(PfSmem) + 1024;
+    static bool attr[2] = {false, false};
+    const bool ext = p.lens != nullptr;
+    if (!attr[ext]) {
+        cudaError_t e = cudaFuncSetAttribute(ext ? prefill_attention_kernel<true> : prefill_attention_kernel<false>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr[ext] = true;
+    }
+    if (ext)
+        prefill_attention_kernel<true><<<p.n_mtiles * p.Hq * slots, PF_THREADS, smem, s>>>(mq, mk, mv, p);
+    else
+        prefill_attention_kernel<false><<<p.n_mtiles * p.Hq * slots, PF_THREADS, smem, s>>>(mq, mk, mv, p);
+    return cudaGetLastError();
+}
+}  // namespace
+
 cudaError_t launch_prefill_attention(const void *q, const void *k, const void *v, void *out, int len,
                                      int q_heads, int kv_heads, int head_dim, float scale,
                                      cudaStream_t s) {
@@ -345,23 +426,39 @@ cudaError_t launch_prefill_attention(const void *q, const void *k, const void *v
     if (!make_map(&mq, q, q_heads, len, PF_M) || !make_map(&mk, k, kv_heads, len, PF_N) ||
         !make_map(&mv, v, kv_heads, len, PF_N))
         return cudaErrorInvalidValue;
-    const size_t smem = sizeof(PfSmem) + 1024;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(prefill_attention_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
-    PfParams p;
+    PfParams p{};
     p.Hq = q_heads;
     p.Hkv = kv_heads;
     p.len = len;
     p.n_mtiles = (len + PF_M - 1) / PF_M;
     p.scale_log2 = scale * 1.4426950408889634f;
     p.out = static_cast<__nv_bfloat16 *>(out);
-    prefill_attention_kernel<<<p.n_mtiles * q_heads, PF_THREADS, smem, s>>>(mq, mk, mv, p);
-    return cudaGetLastError();
+    p.lens = nullptr;
+    return launch_pf(mq, mk, mv, p, 1, s);
+}
+
+cudaError_t launch_extend_attention(const void *q, const void *k_layer, const void *v_layer, void *out,
+                                    int W, int slots, int q_heads, int kv_heads, int head_dim, int max_ctx,
+                                    const int32_t *lens, const int32_t *pad, const uint8_t *mask,
+                                    float scale, cudaStream_t s) {
+    if (head_dim != PF_D || W < 1) return cudaErrorInvalidValue;
+    CUtensorMap mq, mk, mv;
+    // q: [slots*q_heads][W][D]; cache layer: [slots*kv_heads][max_ctx][D]
+    if (!make_map(&mq, q, slots * q_heads, W, PF_M) || !make_map(&mk, k_layer, slots * kv_heads, max_ctx, PF_N) ||
+        !make_map(&mv, v_layer, slots * kv_heads, max_ctx, PF_N))
+        return cudaErrorInvalidValue;
+    PfParams p{};
+    p.Hq = q_heads;
+    p.Hkv = kv_heads;
+    p.len = W;
+    p.n_mtiles = (W + PF_M - 1) / PF_M;
+    p.scale_log2 = scale * 1.4426950408889634f;
+    p.out = static_cast<__nv_bfloat16 *>(out);
+    p.lens = lens;
+    p.pad = pad;
+    p.mask = mask;
+    p.max_ctx = max_ctx;
+    return launch_pf(mq, mk, mv, p, slots, s);
 }
 
 }  // namespace baton
