@@ -40,6 +40,9 @@ class StepStats:
     insert_rows: int = 0        # prefilled rows embedded
     extract_rows: int = 0
     compact_rows: int = 0
+    width: int = 1              # shape policy: input width of the iteration
+    prefill_rows: int = 0       # shape policy: prompt tokens prefilled in the batch
+    bubble_rows: int = 0        # shape policy: padding input tokens computed
 
 
 class Engine:
@@ -71,6 +74,7 @@ class Engine:
         self.outputs: Dict[Tuple[int, int], np.ndarray] = {}
         self.token_source = token_source
         self.prefill_source = prefill_source
+        self.shape_source = None          # shape policy: (t, dec, pre, W) -> q, k, v
         self.use_graph = use_graph
         self.staging = {(self.q.data_ptr(), self.k_new.data_ptr(), self.v_new.data_ptr())}
         # P:L147 "moved to the host memory": stored K/V in pinned host memory (the
@@ -118,11 +122,69 @@ class Engine:
     def done(self):
         return self.planner.finished_all()
 
+    def _shape_tokens(self, dec, pre, W):
+        """Keyed q/k/v of a shaped iteration: [L][B][H][W][D]; input position 0 of a
+        decoding slot is its token, positions t < l of a prefilled slot its prompt
+        tokens, everything else a (zero) padding token."""
+        wl = self.wl
+        L, B, D = wl.layers, self.B, wl.head_dim
+        bufs = [torch.zeros((L, B, H, W, D), dtype=torch.bfloat16, device=self.device)
+                for H in (wl.q_heads, wl.kv_heads, wl.kv_heads)]
+        tmp = [torch.empty((L, B, H, D), dtype=torch.bfloat16, device=self.device)
+               for H in (wl.q_heads, wl.kv_heads, wl.kv_heads)]
+        for t in range(W):
+            qid = np.full(B, -1, np.int32)
+            pos = np.zeros(B, np.int32)
+            if t == 0:
+                for b, q, p in dec:
+                    qid[b], pos[b] = q, p
+            for b, q, n in pre:
+                if t < n:
+                    qid[b], pos[b] = q, t
+            if (qid < 0).all():
+                continue
+            self.d_qid.copy_(torch.from_numpy(qid))
+            self.d_pos.copy_(torch.from_numpy(pos))
+            for (kind, H, sc), dst, tb in zip(((KIND_Q, wl.q_heads, wl.scales[0]),
+                                              (KIND_K, wl.kv_heads, wl.scales[1]),
+                                              (KIND_V, wl.kv_heads, wl.scales[2])), bufs, tmp):
+                baton_keygen_tokens(tb, self.d_qid, self.d_pos, L, B, H, D, kind, 0, wl.seed, sc)
+                dst[:, :, :, t].copy_(tb)
+        return bufs
+
+    def _shape_decode(self, stats, dec, pre):
+        """one shaped iteration (survivors decode, raw queries prefill)."""
+        wl = self.wl
+        W = max(n for _, _, n in pre)
+        if self.shape_source is not None:
+            q, k, v = self.shape_source(self.planner.t, dec, pre, W)
+        else:
+            q, k, v = self._shape_tokens(dec, pre, W)
+        out = torch.empty((wl.layers, self.B, wl.q_heads, W, wl.head_dim), dtype=torch.bfloat16,
+                          device=self.device)
+        self.shard.baton_shape_step(W, [b for b, _, _ in pre], [n for _, _, n in pre], q, k, v, out)
+        stats.width = W
+        stats.prefill_rows = sum(n for _, _, n in pre)
+        stats.bubble_rows = (len(dec) + len(pre)) * W - len(dec) - stats.prefill_rows
+        if self.keep_outputs:
+            layers = self.keep_layers if self.keep_layers is not None else range(wl.layers)
+            o = out[list(layers)].float().cpu().numpy()
+            for b, qq, p in dec:
+                self.outputs[(qq, p)] = o[:, b, :, 0].copy()
+            for b, qq, n in pre:
+                for t in range(n):
+                    self.outputs[(qq, t)] = o[:, b, :, t].copy()
+        return dec
+
     def decode(self, stats):
         """a1 + per layer a2/a3 for the slots the planner says are live."""
         pl = self.planner
         dec = [(pl.local(g), q, p) for g, q, p in pl.decode_plan() if pl.rank_of(g) == self.rank]
         stats.decoded = len(dec)
+        pre = [(pl.local(g), q, n) for g, q, n in pl.prefill_plan() if pl.rank_of(g) == self.rank]
+        if pre:
+            stats.live_rows = sum(p + 1 for _, _, p in dec)
+            return self._shape_decode(stats, dec, pre)
         stats.idle = sum(1 for b, q, p in dec if p >= pl.meta[q].l_q + pl.meta[q].A)
         stats.live_rows = sum(p + 1 for _, _, p in dec)
         if self.token_source is not None:

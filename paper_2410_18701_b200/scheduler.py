@@ -36,6 +36,8 @@ class Decisions:
     victims: List[Tuple[int, int, int]] = field(default_factory=list)   # (gslot, qid, length)
     resize: Optional[int] = None                                         # new active per rank
     inserts: List[Tuple[int, int, int, Optional[int]]] = field(default_factory=list)  # (gslot, qid, len, home)
+    raw: List[Tuple[int, int, int]] = field(default_factory=list)       # shape: reserved (gslot, qid, l_q)
+    prefill: List[Tuple[int, int, int]] = field(default_factory=list)   # shape: prefilled now
 
 
 class Planner:
@@ -43,9 +45,18 @@ class Planner:
         """policy "baton": relay race (remove on completion, insert at once);
         "rtc": the paper's run-to-completion Benchmark -- a finished query
         keeps its slot and keeps decoding (idle EOS tokens) until every query of
-        the batch has finished; only an empty batch is refilled (NEXT-4)."""
-        if policy not in ("baton", "rtc"):
+        the batch has finished; only an empty batch is refilled (NEXT-4);
+        "shape": relay race WITHOUT P&D (vector shaping, NEXT-1) -- a
+        new query takes its slot raw and is prefilled inside the batch in the
+        next iteration (baton_shape_step), whose input width is the longest such
+        prompt; its A decode iterations follow.  No control events."""
+        if policy not in ("baton", "rtc", "shape"):
             raise ValueError(policy)
+        if policy == "shape":
+            c = wl.control
+            if c.preempt or c.preempt_frac or c.resize:
+                raise ValueError("shape policy: no control events")
+        self.raw = {}                                         # shape: gslot -> prompt length
         self.policy = policy
         self.drained = set()                                  # rtc: finished but resident
         self.wl = wl
@@ -82,7 +93,11 @@ class Planner:
     # ---------------------------------------------------------------- phase 1: decode
     def decode_plan(self):
         """Slots that decode this iteration and the position each one handles."""
-        return [(g, q, self.length[g]) for g, q in self.live()]
+        return [(g, q, self.length[g]) for g, q in self.live() if g not in self.raw]
+
+    def prefill_plan(self):
+        """shape policy: raw queries prefilled in this iteration's shaped step."""
+        return [(g, self.occupant[g], n) for g, n in sorted(self.raw.items())]
 
     def idle_decodes(self, decode):
         """Decode entries of queries that already produced all their tokens (rtc)."""
@@ -95,7 +110,7 @@ class Planner:
         for b in range(self.per_rank):
             g = rank * self.per_rank + b
             q = self.occupant[g]
-            flags.append(int(q >= 0 and self.done_tokens[q] + 1 >= self.meta[q].A))
+            flags.append(int(q >= 0 and g not in self.raw and self.done_tokens[q] + 1 >= self.meta[q].A))
         return flags
 
     def _victims(self, candidates, n):
@@ -113,6 +128,10 @@ class Planner:
             for g, q, _ in d.decode:
                 self.done_tokens[q] += 1
                 self.length[g] += 1
+            d.prefill = self.prefill_plan()
+            for g, _, n in d.prefill:          # the prompt is now cached (C9: first token)
+                self.length[g] = n
+            self.raw.clear()
             for g, q in self.live():
                 done = (all_flags[g] != 0) if all_flags is not None else (
                     self.done_tokens[q] >= self.meta[q].A)
@@ -214,6 +233,11 @@ class Planner:
             e = self.queue[idx]
             del self.queue[idx]
             self.occupant[g] = e.qid
-            self.length[g] = e.length
             self.entered[e.qid] = self.t
+            if self.policy == "shape":                        # raw: prefilled next iteration
+                self.length[g] = 0
+                self.raw[g] = e.length
+                d.raw.append((g, e.qid, e.length))
+                continue
+            self.length[g] = e.length
             d.inserts.append((g, e.qid, e.length, e.home))

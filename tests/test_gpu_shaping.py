@@ -152,3 +152,40 @@ def test_shape_step_errors():
     with pytest.raises(BatonError, match="invalid"):
         small.baton_shape_step(1, [0], [1], z(1, 2, 2, 1, 16), z(1, 2, 2, 1, 16),
                                z(1, 2, 2, 1, 16), z(1, 2, 2, 1, 16))
+
+
+@pytest.mark.parametrize("wl_fn", ["w1", "tiles"])
+def test_engine_shape_policy_replay(wl_fn):
+    """The product path (Planner + Engine, policy "shape") against the oracle's
+    shape policy: state bit-exact after every iteration, every output (decodes
+    and prefill rows) within 1e-2."""
+    require_cuda()
+    from paper_2410_18701_b200.engine import Engine
+    if wl_fn == "w1":
+        wl = _w1_128(4, 2)
+    else:
+        qs = [Query(0, 0, 300, 40), Query(1, 0, 170, 30), Query(2, 0, 90, 50),
+              Query(3, 5, 260, 20), Query(4, 5, 140, 25), Query(5, 12, 333, 10)]
+        wl = Workload("shape-tiles", qs, layers=1, q_heads=4, kv_heads=2, head_dim=128, slots=4,
+                      max_ctx=2048)
+    sim = Simulator(wl, kv=True, keep_outputs=True, policy="shape")
+    eng = Engine(wl, keep_outputs=True, policy="shape")
+    osh, sh = sim.shards[0], eng.shard
+    while not sim.done():
+        sim.iteration()
+        eng.iteration()
+        torch.cuda.synchronize()
+        m = sh.baton_query()
+        occ = osh.qid >= 0
+        assert m["S"] == osh.S
+        assert np.array_equal(np.where(occ, m["pad"], 0), np.where(occ, osh.pad, 0))
+        assert np.array_equal(sh.mask[:, :osh.S].cpu().numpy(), osh.mask)
+        for b in np.nonzero(occ)[0]:
+            p, n = int(osh.pad[b]), osh.S - int(osh.pad[b])
+            assert int(m["lens"][b]) == n
+            for cache, ref in ((sh.k_cache, osh.K), (sh.v_cache, osh.V)):
+                assert np.array_equal(bf16_bits(cache[:, b, :, :n]), _f64_to_bits(ref[:, b, :, p:]))
+    assert eng.done()
+    assert set(eng.outputs) == set(sim.outputs)
+    worst = max(row_rel_err(eng.outputs[k], o) for k, o in sim.outputs.items())
+    assert worst <= ATTN_RTOL, worst

@@ -94,3 +94,47 @@ def test_run_to_completion_policy():
     while not base.finished_all():
         base.plan()
     assert base.t < pl.t            # the relay race finishes the same work sooner
+
+
+def _compare_shape(wl, G=None):
+    """Planner policy "shape" (product) == Simulator policy "shape" (oracle)."""
+    G = G or wl.gpus
+    sim = Simulator(wl, G=G, policy="shape")
+    pl = Planner(wl, G, policy="shape")
+    n = 0
+    while True:
+        rec = sim.iteration()
+        d = pl.plan()
+        assert sorted(d.decode) == sorted(rec.decoded), rec.t
+        assert sorted(d.prefill) == sorted(rec.prefilled), rec.t
+        assert sorted(g for g, _ in d.finished) == sorted(rec.removed), rec.t
+        assert d.raw == rec.inserted and not d.inserts, rec.t
+        # a reserved raw slot is still empty in the oracle until its shaped step
+        assert list(np.concatenate(rec.qid)) == [-1 if g in pl.raw else q
+                                                 for g, q in enumerate(pl.occupant)], rec.t
+        # live token counts (the oracle's mask-1 count) of every decoding/prefilled slot
+        lens = np.concatenate(rec.lens)
+        for g, q in enumerate(pl.occupant):
+            if q >= 0 and g not in pl.raw:
+                assert pl.length[g] == lens[g], (rec.t, g)
+        n += 1
+        if sim.done():
+            assert pl.finished_all()
+            break
+    return n
+
+
+def test_shape_policy_w1():
+    wl = w1_workload()
+    wl.max_ctx = 256
+    assert _compare_shape(wl) > 19          # one extra prefill iteration per insert wave
+
+
+@pytest.mark.parametrize("seed", [1, 4, 9])
+def test_shape_policy_random_streams(seed):
+    from baton_inputs import ControlEvents
+    wl = random_stream(seed)
+    wl.control = ControlEvents()
+    wl.max_ctx = 4096
+    wl.iterations = -1
+    _compare_shape(wl)
