@@ -229,8 +229,9 @@ int  baton_prefill_attention(const void *q, const void *k, const void *v, void *
  *     also have the same overhead").
  *   W >= max(1, max new_lens); head_dim must be 128.
  *   new_slots, new_lens : HOST int32[n_new]
- *   q, out       : device bf16 [layers][slots][q_heads][W][head_dim]
- *   k_new, v_new : device bf16 [layers][slots][kv_heads][W][head_dim]; rows of
+ *   q, out       : device bf16 [layers][slots][W][q_heads][head_dim] (token-major,
+ *                  as a model's QKV projection produces them)
+ *   k_new, v_new : device bf16 [layers][slots][W][kv_heads][head_dim]; rows of
  *                  padding tokens are stored (masked) and must be finite
  *   Empty slots produce zero output rows.  Host mirror and device metadata are
  *   updated like a1 (no baton_mask_update for this iteration).

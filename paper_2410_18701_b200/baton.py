@@ -158,7 +158,7 @@ class BatonShard:
 
     def baton_shape_step(self, W, new_slots, new_lens, q, k_new, v_new, out, stream=None):
         """NEXT-1: one vector-shaping iteration of width W (include/baton.h).
-        q/out [L][slots][q_heads][W][D]; k_new/v_new [L][slots][kv_heads][W][D]."""
+        q/out [L][slots][W][q_heads][D]; k_new/v_new [L][slots][W][kv_heads][D] (token-major)."""
         new_slots, new_lens = list(new_slots), list(new_lens)
         check(lib.baton_shape_step(self._h, int(W), len(new_slots), _i32(new_slots), _i32(new_lens),
                                    _ptr(q), _ptr(k_new), _ptr(v_new), _ptr(out), _stream(stream)),

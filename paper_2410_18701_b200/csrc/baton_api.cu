@@ -324,47 +324,28 @@ int baton_shape_step(baton_state *st, int W, int n_new, const int32_t *new_slots
     if (st->S + W > s.max_ctx) return BATON_E_CAPACITY;
     const int S0 = st->S;
     std::vector<MaskOp> ops;
-    std::vector<CopyJob> jobs;
-    const size_t slot_elems = (size_t)s.kv_heads * s.max_ctx * s.head_dim;
+    std::vector<int32_t> row0(s.slots, -1);
     for (int b = 0; b < s.slots; ++b) {
-        int row0;
         if (st->occ[b]) {            // survivor: its token at column S0, then W-1 padding
             ops.push_back({MOP_SET_CELL, b, S0, 0});
-            row0 = st->lens[b];
+            row0[b] = st->lens[b];
             st->lens[b] += W;
         } else if (newlen[b]) {      // new raw query: row := 0^S0 1^l 0^(W-l)
             ops.push_back({MOP_SET_ROW, b, S0, S0 + newlen[b]});
-            row0 = 0;
+            row0[b] = 0;
             st->occ[b] = 1;
             st->pad[b] = S0;
             st->lens[b] = W;
-        } else {
-            continue;
         }
-        // the W input tokens' K/V rows (reading C4: the cache grows by W as well)
-        CopyJob j;
-        const size_t src0 = (size_t)b * s.kv_heads * W * s.head_dim;
-        j.src_k = static_cast<const __nv_bfloat16 *>(k_new) + src0;
-        j.src_v = static_cast<const __nv_bfloat16 *>(v_new) + src0;
-        j.dst_k = static_cast<__nv_bfloat16 *>(st->cfg.k_cache) + b * slot_elems + (size_t)row0 * s.head_dim;
-        j.dst_v = static_cast<__nv_bfloat16 *>(st->cfg.v_cache) + b * slot_elems + (size_t)row0 * s.head_dim;
-        j.src_hs = (int64_t)W * s.head_dim;
-        j.src_ls = j.src_hs * s.kv_heads * s.slots;
-        j.dst_hs = (int64_t)s.max_ctx * s.head_dim;
-        j.dst_ls = (int64_t)st->layer_elems;
-        j.rows = W;
-        j.pad_ = 0;
-        jobs.push_back(j);
     }
     st->S = S0 + W;
     cudaStream_t cs = as_stream(stream);
     int r = push_meta(st, ops, cs);
     if (r) return r;
-    for (size_t i0 = 0; i0 < jobs.size(); i0 += MAX_SPLICE_JOBS) {
-        const int nj = (int)std::min(jobs.size() - i0, (size_t)MAX_SPLICE_JOBS);
-        r = cuda_status(launch_kv_copy(jobs.data() + i0, nj, s.layers, s.kv_heads, s.head_dim, cs));
-        if (r) return r;
-    }
+    // the W input tokens' K/V rows (reading C4: the cache grows by W as well)
+    r = cuda_status(launch_shape_append(st->cfg.k_cache, st->cfg.v_cache, k_new, v_new, row0.data(), s.layers,
+                                        s.slots, s.kv_heads, s.head_dim, s.max_ctx, W, cs));
+    if (r) return r;
     const size_t qstride = (size_t)s.slots * s.q_heads * W * s.head_dim;
     const float scale = 1.0f / sqrtf((float)s.head_dim);
     for (int l = 0; l < s.layers; ++l) {

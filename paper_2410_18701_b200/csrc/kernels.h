@@ -76,6 +76,12 @@ struct CopyJob {
 };
 cudaError_t launch_kv_copy(const CopyJob *jobs, int njobs, int layers, int kv_heads, int head_dim,
                            cudaStream_t s);
+// NEXT-1: append the W input tokens' K/V of every occupied slot to its cache rows
+// [row0[b], row0[b] + W) (row0 < 0: slot skipped), all layers; src token-major
+// [layers][slots][W][kv_heads][head_dim].
+cudaError_t launch_shape_append(void *k_cache, void *v_cache, const void *k_new, const void *v_new,
+                                const int32_t *row0, int layers, int slots, int kv_heads, int head_dim,
+                                int max_ctx, int W, cudaStream_t s);
 
 // ------------------------------------------------------------ a8 prefill attention (tcgen05)
 bool prefill_supported(int head_dim);
@@ -84,8 +90,8 @@ cudaError_t launch_prefill_attention(const void *q, const void *k, const void *v
                                      cudaStream_t s);
 // NEXT-1 (vector shaping): attention of the W input tokens of every slot over the
 // slot's cache rows [0, lens_b - W + t] where the mask is 1 (prefill_attention.cu).
-// q/out: [slots][q_heads][W][128]; k/v_layer: one layer of the cache; lens/pad: the
-// device metadata after the shaped mask update.
+// q/out: [slots][W][q_heads][128] (token-major); k/v_layer: one layer of the cache;
+// lens/pad: the device metadata after the shaped mask update.
 cudaError_t launch_extend_attention(const void *q, const void *k_layer, const void *v_layer, void *out,
                                     int W, int slots, int q_heads, int kv_heads, int head_dim, int max_ctx,
                                     const int32_t *lens, const int32_t *pad, const uint8_t *mask,

@@ -20,7 +20,8 @@
 //
 // The same kernel runs the EXTEND attention of a vector-shaping iteration
 // (NEXT-1, launch_extend_attention): a CTA per (slot, q head, query
-// tile); query row t of slot b is input token t of width W, its keys are the
+// tile); query row t of slot b is input token t of width W (q/out token-major,
+// [slots][W][q_heads][D]: a 4-D Q map with a (64, 1, 128, 1) box), its keys are the
 // slot's cache rows 0 .. off_b + t (off_b = lens_b - W, the rows before this
 // iteration), and a key is also dropped where the paper's attention_mask is 0 (the
 // mask bytes of each key tile ride in the V stage, which outlives the softmax of
@@ -60,6 +61,13 @@ BATON_DEV void tma_load_3d(void *dst, const CUtensorMap *map, int c0, int c1, in
         "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+BATON_DEV void tma_load_4d(void *dst, const CUtensorMap *map, int c0, int c1, int c2, int c3, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
         : "memory");
 }
 BATON_DEV void prefetch_tmap(const CUtensorMap *map) {
@@ -157,7 +165,7 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
             for (int i = threadIdx.x; i < PF_M * PF_D / 8; i += PF_THREADS) {
                 const int r = q0 + i / (PF_D / 8);
                 if (r < p.len)
-                    reinterpret_cast<uint4 *>(p.out + (((size_t)b * p.Hq + h) * p.len + r) * PF_D)[i % (PF_D / 8)] =
+                    reinterpret_cast<uint4 *>(p.out + (((size_t)b * p.len + r) * p.Hq + h) * PF_D)[i % (PF_D / 8)] =
                         make_uint4(0, 0, 0, 0);
             }
             return;
@@ -200,8 +208,13 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
             prefetch_tmap(&tm_k);
             prefetch_tmap(&tm_v);
             mbar_arrive_expect_tx(&sm.bar_q, Q_BYTES);
-            tma_load_3d(sm.q, &tm_q, 0, q0, qrow, &sm.bar_q);
-            tma_load_3d(sm.q + Q_REGION, &tm_q, 64, q0, qrow, &sm.bar_q);
+            if constexpr (EXT) {
+                tma_load_4d(sm.q, &tm_q, 0, h, q0, b, &sm.bar_q);
+                tma_load_4d(sm.q + Q_REGION, &tm_q, 64, h, q0, b, &sm.bar_q);
+            } else {
+                tma_load_3d(sm.q, &tm_q, 0, q0, qrow, &sm.bar_q);
+                tma_load_3d(sm.q + Q_REGION, &tm_q, 64, q0, qrow, &sm.bar_q);
+            }
             for (int j = 0; j < n_kt; ++j) {
                 if (j > 0) mbar_wait(&sm.k_empty, (j - 1) & 1);          // S(j-1) done with K
                 mbar_arrive_expect_tx(&sm.k_full, KV_BYTES);
@@ -359,7 +372,8 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
         mbar_wait(&sm.o_done, (n_kt - 1) & 1);
         tc_fence_after();
         const float inv = l > 0.f ? 1.f / l : 0.f;
-        __nv_bfloat16 *orow = p.out + ((size_t)qrow * p.len + qi) * PF_D;
+        __nv_bfloat16 *orow = EXT ? p.out + (((size_t)b * p.len + qi) * p.Hq + h) * PF_D
+                                  : p.out + ((size_t)qrow * p.len + qi) * PF_D;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             uint32_t o[32];
@@ -443,8 +457,12 @@ cudaError_t launch_extend_attention(const void *q, const void *k_layer, const vo
                                     float scale, cudaStream_t s) {
     if (head_dim != PF_D || W < 1) return cudaErrorInvalidValue;
     CUtensorMap mq, mk, mv;
-    // q: [slots*q_heads][W][D]; cache layer: [slots*kv_heads][max_ctx][D]
-    if (!make_map(&mq, q, slots * q_heads, W, PF_M) || !make_map(&mk, k_layer, slots * kv_heads, max_ctx, PF_N) ||
+    // q: [slots][W][q_heads][D] (token-major) -> dims (D, q_heads, W, slots), box (64, 1, 128, 1)
+    const uint64_t qd[4] = {(uint64_t)PF_D, (uint64_t)q_heads, (uint64_t)W, (uint64_t)slots};
+    const uint64_t qs[3] = {(uint64_t)PF_D * 2, (uint64_t)q_heads * PF_D * 2, (uint64_t)W * q_heads * PF_D * 2};
+    const uint32_t qb[4] = {64, 1, (uint32_t)PF_M, 1};
+    // cache layer: [slots*kv_heads][max_ctx][D]
+    if (!encode_bf16_map(&mq, q, 4, qd, qs, qb) || !make_map(&mk, k_layer, slots * kv_heads, max_ctx, PF_N) ||
         !make_map(&mv, v_layer, slots * kv_heads, max_ctx, PF_N))
         return cudaErrorInvalidValue;
     PfParams p{};

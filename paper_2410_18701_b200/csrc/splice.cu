@@ -6,6 +6,8 @@
 // splice of an iteration is a batch of equal-shape contiguous copies: ONE launch,
 // grid (pieces, layer*kv_head*2, job), 16-B vector loads/stores, 4 loads in
 // flight per thread before the stores (bytes in flight ~ 64 KB per SM).
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -50,7 +52,60 @@ __global__ void __launch_bounds__(CP_THREADS) kv_copy_kernel(const __grid_consta
     }
 }
 
+struct ShapeAppendParams {
+    __nv_bfloat16 *k, *v;
+    const __nv_bfloat16 *kn, *vn;
+    int32_t row0[MAX_SLOTS];
+    int layers, slots, kv_heads, vec_per_row, max_ctx, W;
+};
+
+// grid-stride over (layer, slot, token, kv head, 16-B vector) of the token-major
+// source; each destination row is contiguous in the slot-relative cache
+__global__ void __launch_bounds__(256) shape_append_kernel(const __grid_constant__ ShapeAppendParams p) {
+    const int64_t per_tok = (int64_t)p.kv_heads * p.vec_per_row;
+    const int64_t total = (int64_t)p.layers * p.slots * p.W * per_tok;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t tok = i / per_tok;                 // (layer, slot, t)
+        const int rem = (int)(i - tok * per_tok);
+        const int g = rem / p.vec_per_row, c = rem - g * p.vec_per_row;
+        const int t = (int)(tok % p.W);
+        const int64_t ls = tok / p.W;
+        const int b = (int)(ls % p.slots), l = (int)(ls / p.slots);
+        const int r0 = p.row0[b];
+        if (r0 < 0) continue;
+        const size_t dst = ((((size_t)l * p.slots + b) * p.kv_heads + g) * p.max_ctx + r0 + t) * p.vec_per_row + c;
+        reinterpret_cast<uint4 *>(p.k)[dst] = reinterpret_cast<const uint4 *>(p.kn)[i];
+        reinterpret_cast<uint4 *>(p.v)[dst] = reinterpret_cast<const uint4 *>(p.vn)[i];
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_shape_append(void *k_cache, void *v_cache, const void *k_new, const void *v_new,
+                                const int32_t *row0, int layers, int slots, int kv_heads, int head_dim,
+                                int max_ctx, int W, cudaStream_t s) {
+    if (slots > MAX_SLOTS || head_dim % 8) return cudaErrorInvalidValue;
+    ShapeAppendParams p;
+    p.k = static_cast<__nv_bfloat16 *>(k_cache);
+    p.v = static_cast<__nv_bfloat16 *>(v_cache);
+    p.kn = static_cast<const __nv_bfloat16 *>(k_new);
+    p.vn = static_cast<const __nv_bfloat16 *>(v_new);
+    for (int b = 0; b < slots; ++b) p.row0[b] = row0[b];
+    p.layers = layers;
+    p.slots = slots;
+    p.kv_heads = kv_heads;
+    p.vec_per_row = head_dim / 8;
+    p.max_ctx = max_ctx;
+    p.W = W;
+    const int64_t total = (int64_t)layers * slots * W * kv_heads * p.vec_per_row;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)sms * 8);
+    shape_append_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(p);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_kv_copy(const CopyJob *jobs, int njobs, int layers, int kv_heads, int head_dim,
                            cudaStream_t s) {

@@ -20,9 +20,9 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 bool encode_bf16_map(CUtensorMap *map, const void *base, int rank, const uint64_t *dims,
                      const uint64_t *strides_bytes, const uint32_t *box) {
     auto enc = get_encode();
-    if (!enc || rank < 2 || rank > 3) return false;
-    cuuint64_t d[3], s[2];
-    cuuint32_t b[3], e[3] = {1, 1, 1};
+    if (!enc || rank < 2 || rank > 5) return false;
+    cuuint64_t d[5], s[4];
+    cuuint32_t b[5], e[5] = {1, 1, 1, 1, 1};
     for (int i = 0; i < rank; ++i) {
         d[i] = dims[i];
         b[i] = box[i];

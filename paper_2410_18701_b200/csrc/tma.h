@@ -7,7 +7,7 @@
 
 namespace baton {
 
-// bf16 tensor of `rank` (2 or 3) dims, innermost first; strides in bytes for
+// bf16 tensor of `rank` (2 to 5) dims, innermost first; strides in bytes for
 // dims 1..rank-1; box sizes in elements.  SWIZZLE_128B.  False on failure.
 bool encode_bf16_map(CUtensorMap *map, const void *base, int rank, const uint64_t *dims,
                      const uint64_t *strides_bytes, const uint32_t *box);

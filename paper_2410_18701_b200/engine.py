@@ -123,34 +123,28 @@ class Engine:
         return self.planner.finished_all()
 
     def _shape_tokens(self, dec, pre, W):
-        """Keyed q/k/v of a shaped iteration: [L][B][H][W][D]; input position 0 of a
-        decoding slot is its token, positions t < l of a prefilled slot its prompt
-        tokens, everything else a (zero) padding token."""
+        """Keyed q/k/v of a shaped iteration, token-major [L][B][W][H][D]: input
+        position 0 of a decoding slot is its token, positions t < l of a prefilled
+        slot its prompt tokens, everything else a (zero) padding token.  One keygen
+        launch per tensor over all B*W input tokens."""
         wl = self.wl
         L, B, D = wl.layers, self.B, wl.head_dim
-        bufs = [torch.zeros((L, B, H, W, D), dtype=torch.bfloat16, device=self.device)
-                for H in (wl.q_heads, wl.kv_heads, wl.kv_heads)]
-        tmp = [torch.empty((L, B, H, D), dtype=torch.bfloat16, device=self.device)
-               for H in (wl.q_heads, wl.kv_heads, wl.kv_heads)]
-        for t in range(W):
-            qid = np.full(B, -1, np.int32)
-            pos = np.zeros(B, np.int32)
-            if t == 0:
-                for b, q, p in dec:
-                    qid[b], pos[b] = q, p
-            for b, q, n in pre:
-                if t < n:
-                    qid[b], pos[b] = q, t
-            if (qid < 0).all():
-                continue
-            self.d_qid.copy_(torch.from_numpy(qid))
-            self.d_pos.copy_(torch.from_numpy(pos))
-            for (kind, H, sc), dst, tb in zip(((KIND_Q, wl.q_heads, wl.scales[0]),
-                                              (KIND_K, wl.kv_heads, wl.scales[1]),
-                                              (KIND_V, wl.kv_heads, wl.scales[2])), bufs, tmp):
-                baton_keygen_tokens(tb, self.d_qid, self.d_pos, L, B, H, D, kind, 0, wl.seed, sc)
-                dst[:, :, :, t].copy_(tb)
-        return bufs
+        qid = np.full((B, W), -1, np.int32)
+        pos = np.zeros((B, W), np.int32)
+        for b, q, p in dec:
+            qid[b, 0], pos[b, 0] = q, p
+        for b, q, n in pre:
+            qid[b, :n] = q
+            pos[b, :n] = np.arange(n)
+        d_qid = torch.from_numpy(qid.reshape(-1)).to(self.device)
+        d_pos = torch.from_numpy(pos.reshape(-1)).to(self.device)
+        out = []
+        for kind, H, sc in ((KIND_Q, wl.q_heads, wl.scales[0]), (KIND_K, wl.kv_heads, wl.scales[1]),
+                            (KIND_V, wl.kv_heads, wl.scales[2])):
+            t = torch.empty((L, B, W, H, D), dtype=torch.bfloat16, device=self.device)
+            baton_keygen_tokens(t, d_qid, d_pos, L, B * W, H, D, kind, 0, wl.seed, sc)
+            out.append(t)
+        return out
 
     def _shape_decode(self, stats, dec, pre):
         """one shaped iteration (survivors decode, raw queries prefill)."""
@@ -160,7 +154,7 @@ class Engine:
             q, k, v = self.shape_source(self.planner.t, dec, pre, W)
         else:
             q, k, v = self._shape_tokens(dec, pre, W)
-        out = torch.empty((wl.layers, self.B, wl.q_heads, W, wl.head_dim), dtype=torch.bfloat16,
+        out = torch.empty((wl.layers, self.B, W, wl.q_heads, wl.head_dim), dtype=torch.bfloat16,
                           device=self.device)
         self.shard.baton_shape_step(W, [b for b, _, _ in pre], [n for _, _, n in pre], q, k, v, out)
         stats.width = W
@@ -170,10 +164,10 @@ class Engine:
             layers = self.keep_layers if self.keep_layers is not None else range(wl.layers)
             o = out[list(layers)].float().cpu().numpy()
             for b, qq, p in dec:
-                self.outputs[(qq, p)] = o[:, b, :, 0].copy()
+                self.outputs[(qq, p)] = o[:, b, 0].copy()
             for b, qq, n in pre:
                 for t in range(n):
-                    self.outputs[(qq, t)] = o[:, b, :, t].copy()
+                    self.outputs[(qq, t)] = o[:, b, t].copy()
         return dec
 
     def decode(self, stats):

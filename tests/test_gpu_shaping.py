@@ -50,29 +50,29 @@ def _replay(wl):
             if rec.prefilled:
                 W = rec.width[0]
                 n_shaped += 1
-                q = np.zeros((L, B, Hq, W, D), np.uint16)
-                k = np.zeros((L, B, Hkv, W, D), np.uint16)
-                v = np.zeros((L, B, Hkv, W, D), np.uint16)
+                q = np.zeros((L, B, W, Hq, D), np.uint16)      # token-major (include/baton.h)
+                k = np.zeros((L, B, W, Hkv, D), np.uint16)
+                v = np.zeros((L, B, W, Hkv, D), np.uint16)
                 occ = np.nonzero(pre_qid >= 0)[0]
                 if len(occ):
                     qids, pos = np.where(pre_qid >= 0, pre_qid, 0), pre_lens
                     for kind, H, arr in ((KIND_Q, Hq, q), (KIND_K, Hkv, k), (KIND_V, Hkv, v)):
                         tb = _tok_bits(wl, kind, H, qids, pos)
                         for b in occ:
-                            arr[:, b, :, 0] = tb[:, b]
+                            arr[:, b, 0] = tb[:, b]
                 for g, qid, l in rec.prefilled:
                     for t in range(l):
                         for kind, H, arr in ((KIND_Q, Hq, q), (KIND_K, Hkv, k), (KIND_V, Hkv, v)):
-                            arr[:, g, :, t] = _tok_bits(wl, kind, H, [qid], [t])[:, 0]
-                out = torch.empty((L, B, Hq, W, D), dtype=torch.bfloat16, device="cuda")
+                            arr[:, g, t] = _tok_bits(wl, kind, H, [qid], [t])[:, 0]
+                out = torch.empty((L, B, W, Hq, D), dtype=torch.bfloat16, device="cuda")
                 sh.baton_shape_step(W, [g for g, _, _ in rec.prefilled], [l for _, _, l in rec.prefilled],
                                     _to_dev(q), _to_dev(k), _to_dev(v), out)
                 o = out.float().cpu().numpy()
                 for g, qid, pos in rec.decoded:
-                    worst = max(worst, row_rel_err(o[:, g, :, 0], sim.outputs[(qid, pos)]))
+                    worst = max(worst, row_rel_err(o[:, g, 0], sim.outputs[(qid, pos)]))
                 for g, qid, l in rec.prefilled:
                     for t in range(l):
-                        worst = max(worst, row_rel_err(o[:, g, :, t], sim.outputs[(qid, t)]))
+                        worst = max(worst, row_rel_err(o[:, g, t], sim.outputs[(qid, t)]))
             else:
                 qids = np.where(pre_qid >= 0, pre_qid, 0)
                 q = _to_dev(_tok_bits(wl, KIND_Q, Hq, qids, pre_lens))
@@ -139,13 +139,13 @@ def test_shape_step_errors():
     from paper_2410_18701_b200._lib import BatonError
     sh = BatonShard(1, 2, 2, 2, 128, 64)
     z = lambda *s: torch.zeros(s, dtype=torch.bfloat16, device="cuda")
-    q, kv, out = z(1, 2, 2, 4, 128), z(1, 2, 2, 4, 128), z(1, 2, 2, 4, 128)
+    q, kv, out = z(1, 2, 4, 2, 128), z(1, 2, 4, 2, 128), z(1, 2, 4, 2, 128)
     sh.baton_shape_step(4, [0], [3], q, kv, kv, out)
     with pytest.raises(BatonError, match="busy"):
         sh.baton_shape_step(4, [0], [2], q, kv, kv, out)
     with pytest.raises(BatonError, match="capacity"):
         sh.baton_shape_step(4, [1], [5], q, kv, kv, out)        # l > W
-    big = z(1, 2, 2, 64, 128)
+    big = z(1, 2, 64, 2, 128)
     with pytest.raises(BatonError, match="capacity"):
         sh.baton_shape_step(64, [1], [64], big, big, big, big)   # S + W > max_ctx
     small = BatonShard(1, 2, 2, 2, 16, 64)
