@@ -127,6 +127,13 @@ class BatonShard:
     def layer_v(self, layer):
         return self.v_cache[layer]
 
+    @property
+    def S(self):
+        """Shared logical length S (host mirror, no device sync)."""
+        S = ctypes.c_int32()
+        check(lib.baton_query(self._h, ctypes.byref(S), None, None, None), "baton_query")
+        return S.value
+
     def baton_query(self):
         S = ctypes.c_int32()
         pad = (ctypes.c_int32 * self.B)()

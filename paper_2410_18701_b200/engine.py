@@ -20,7 +20,7 @@ from typing import Dict, List, Optional, Tuple
 import numpy as np
 import torch
 
-from .baton import BatonShard, baton_keygen_tokens, baton_keygen_history
+from .baton import BatonShard, baton_keygen_tokens, baton_keygen_history, baton_prefill_attention
 from .comm import gather_completion_flags
 from .scheduler import Planner
 
@@ -43,12 +43,13 @@ class StepStats:
     width: int = 1              # shape policy: input width of the iteration
     prefill_rows: int = 0       # shape policy: prompt tokens prefilled in the batch
     bubble_rows: int = 0        # shape policy: padding input tokens computed
+    S: int = 0                  # shared logical length after the iteration (host mirror)
 
 
 class Engine:
     def __init__(self, wl, rank=0, world=1, device=None, group=None, keep_outputs=False,
                  keep_layers=None, token_source=None, prefill_source=None, use_graph=True,
-                 stash_host=False, policy="baton"):
+                 stash_host=False, policy="baton", prefill_attention=False):
         self.wl = wl
         self.rank = rank
         self.world = world
@@ -75,6 +76,9 @@ class Engine:
         self.token_source = token_source
         self.prefill_source = prefill_source
         self.shape_source = None          # shape policy: (t, dec, pre, W) -> q, k, v
+        # P&D accounting: run a8 (baton_prefill_attention, every layer) on each fresh
+        # insert, so a policy comparison charges the decoupled prefill its attention
+        self.prefill_attention = prefill_attention
         self.use_graph = use_graph
         self.staging = {(self.q.data_ptr(), self.k_new.data_ptr(), self.v_new.data_ptr())}
         # P:L147 "moved to the host memory": stored K/V in pinned host memory (the
@@ -117,6 +121,16 @@ class Engine:
         baton_keygen_history(V, wl.layers, wl.kv_heads, wl.head_dim, qid, 0, length, KIND_V,
                              wl.seed, wl.scales[2])
         return K, V
+
+    def _prefill_attn(self, qid, n, K, V):
+        """a8 over every layer of a fresh query's prompt (output discarded)."""
+        wl = self.wl
+        Q = torch.empty((wl.layers, wl.q_heads, n, wl.head_dim), dtype=torch.bfloat16, device=self.device)
+        baton_keygen_history(Q, wl.layers, wl.q_heads, wl.head_dim, qid, 0, n, KIND_Q, wl.seed,
+                             wl.scales[0])
+        O = torch.empty_like(Q)
+        for l in range(wl.layers):
+            baton_prefill_attention(Q[l], K[l], V[l], O[l], n, wl.q_heads, wl.kv_heads, wl.head_dim)
 
     # ---------------------------------------------------------------- one iteration
     def done(self):
@@ -254,6 +268,8 @@ class Engine:
                     K, V = self.stash.pop(q)
                 else:
                     K, V = self._prefill(q, n)
+                    if self.prefill_attention:
+                        self._prefill_attn(q, n, K, V)
                 slots.append(b)
                 ks.append(K)
                 vs.append(V)
@@ -261,6 +277,7 @@ class Engine:
             sh.baton_insert_many(slots, ks, vs, lens)
             stats.inserted = len(ins)
             stats.insert_rows = sum(lens)
+        stats.S = sh.S
         return stats
 
     def run(self, max_iters=None):

@@ -1,13 +1,20 @@
-"""NEXT-4: Baton's relay race vs the paper's run-to-completion Benchmark on B200.
+"""NEXT-4 / NEXT-1: Baton's policies vs the paper's run-to-completion Benchmark on B200.
 
-    python scripts/policy_compare.py [--dataset d2|d1] [--batches 2,4,6,8,10]
+    python scripts/policy_compare.py [--dataset d2|d1] [--batches 2,4,6,8,10] [--no-shape]
 
-Runs the whole synthetic dataset through the same libbaton kernels under both
-policies (Planner policy "baton" vs "rtc": a finished query keeps decoding idle
-EOS tokens until its whole batch is done) and reports, per batch size,
-the completion time of the dataset (device time of all iterations) and useful
-decode tokens/s -- the B200 counterpart of Tables 2/3, with the
-paper's datasets replaced by the length mixes of P:L212 (model GEMMs excluded).
+Runs the whole synthetic dataset through the same libbaton kernels under
+  * "rtc"   -- the paper's Benchmark: a finished query keeps decoding idle EOS
+               tokens until its whole batch is done;
+  * "shape" -- Baton WITHOUT P&D ("Ours"): a new query is prefilled
+               inside the batch, every row padded to its prompt length (NEXT-1);
+  * "baton" -- Baton WITH P&D decoupling ("Ours-PD"): width-1 decode for
+               everybody, the prompt prefilled separately by a8;
+and reports, per batch size, the completion time of the dataset (device time of
+all iterations) and useful decode tokens/s: the B200 counterpart of Tables 2/3
+(P:L230-289), with the paper's datasets replaced by the length mixes of P:L212.
+Every arm pays its prefill attention (rtc and baton: a8 per fresh insert; shape:
+in the shaped iteration).  Model GEMMs are excluded (no weights), so the bubble
+of the shape arm costs only its attention here.
 """
 import argparse
 import json
@@ -37,7 +44,7 @@ def dataset(name, batch):
 
 def run(name, batch, policy):
     wl = dataset(name, batch)
-    eng = Engine(wl, policy=policy, use_graph=True)
+    eng = Engine(wl, policy=policy, use_graph=True, prefill_attention=policy != "shape")
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -48,19 +55,31 @@ def run(name, batch, policy):
     useful = sum(s.decoded - s.idle for s in st)
     assert useful == wl.decode_tokens()
     return {"iterations": len(st), "ms": ms, "useful_tokens": useful,
-            "idle_tokens": sum(s.idle for s in st), "useful_tok_per_s": useful / (ms / 1e3)}
+            "idle_tokens": sum(s.idle for s in st), "useful_tok_per_s": useful / (ms / 1e3),
+            "shaped_iterations": sum(1 for s in st if s.prefill_rows),
+            "bubble_rows": sum(s.bubble_rows for s in st),
+            "max_S": max(s.S for s in st)}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--dataset", default="d2")
     ap.add_argument("--batches", default="2,4,6,8,10")
+    ap.add_argument("--no-shape", action="store_true")
     args = ap.parse_args()
     for b in [int(x) for x in args.batches.split(",")]:
         base = run(args.dataset, b, "rtc")
         bat = run(args.dataset, b, "baton")
-        print(json.dumps({"dataset": args.dataset, "batch": b, "benchmark_rtc": base, "baton": bat,
-                          "completion_speedup": base["ms"] / bat["ms"]}), flush=True)
+        line = {"dataset": args.dataset, "batch": b, "benchmark_rtc": base, "baton_pd": bat,
+                "completion_speedup": base["ms"] / bat["ms"]}
+        if not args.no_shape:
+            try:
+                shp = run(args.dataset, b, "shape")
+                line["baton_shape"] = shp
+                line["pd_over_shape"] = shp["ms"] / bat["ms"]     # Table 2: Ours-PD vs Ours
+            except Exception as e:                                 # KV growth (Fig. 8)
+                line["baton_shape"] = {"error": str(e)}
+        print(json.dumps(line), flush=True)
         torch.cuda.empty_cache()
 
 
