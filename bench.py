@@ -442,10 +442,12 @@ def run_baton(args, rank, world, local_rank):
 
 
 # ------------------------------------------------------------------ the oracle arm
-def oracle_sample(budget_s=15.0, t0=T0_DEFAULT, max_steps=None):
+def oracle_sample(budget_s=15.0, t0=T0_DEFAULT, max_steps=None, n_slots=None, warmup=0):
     """Time the fp64 oracle (O-2 Shard.step, as it stands) on a bounded sample of
-    the same workload: ONE layer of the 7B batch at iteration t0, all live slots.
-    Returns seconds per layer-iteration and the live slot count."""
+    the same workload: ONE layer of the 7B batch at iteration t0, all live slots
+    (or the ``n_slots`` longest).  ``warmup`` untimed steps first.
+    Returns seconds per timed step, the sampled slot count, L, the timed steps and
+    the live slot count of the full batch."""
     from baton_inputs import config_workload, KIND_K, KIND_V, KIND_Q, bf16_bits_to_f64
     from baton_inputs import query_history_bits, query_token_bits
     from oracle import Shard, Simulator
@@ -454,20 +456,32 @@ def oracle_sample(budget_s=15.0, t0=T0_DEFAULT, max_steps=None):
     while sim.t <= t0:
         sim.iteration()
     osh = sim.shards[0]
-    sh = Shard(wl.slots, 1, wl.q_heads, wl.kv_heads, wl.head_dim, wl.max_ctx, kv=True)
-    occ = [b for b in range(wl.slots) if osh.qid[b] >= 0]
+    live = [b for b in range(wl.slots) if osh.qid[b] >= 0]
     lens = osh.lens()
-    for b in sorted(occ, key=lambda b: -lens[b]):
+    if n_slots:   # rows at evenly spaced length quantiles: the sample's mean length ~ the batch's
+        by_len = sorted(live, key=lambda b: lens[b])
+        picked = [by_len[int((i + 0.5) * len(by_len) / n_slots)] for i in range(n_slots)]
+    else:
+        picked = live
+    # the oracle keeps DENSE [rows][S] tensors, so a sample shard holds exactly the
+    # sampled rows (its cost is then linear in them)
+    rows = len(picked) if n_slots else wl.slots
+    sh = Shard(rows, 1, wl.q_heads, wl.kv_heads, wl.head_dim, wl.max_ctx, kv=True)
+    occ = []
+    for i, b in enumerate(sorted(picked, key=lambda b: -lens[b])):
+        row = i if n_slots else b
         q = int(osh.qid[b])
         n = int(lens[b])
         K = bf16_bits_to_f64(query_history_bits(wl.seed, KIND_K, 1, q, 0, n, wl.kv_heads, wl.head_dim, 0))
         V = bf16_bits_to_f64(query_history_bits(wl.seed, KIND_V, 1, q, 0, n, wl.kv_heads, wl.head_dim, 0))
-        sh.insert(b, q, n, K, V)
+        sh.insert(row, q, n, K, V)
+        occ.append(row)
     times = []
     step = 0
+    warm = warmup
     while True:
-        qids = np.zeros(wl.slots, np.int64)
-        pos = np.zeros(wl.slots, np.int64)
+        qids = np.zeros(sh.B, np.int64)
+        pos = np.zeros(sh.B, np.int64)
         cur = sh.lens()
         for b in occ:
             qids[b], pos[b] = sh.qid[b], cur[b]
@@ -476,27 +490,37 @@ def oracle_sample(budget_s=15.0, t0=T0_DEFAULT, max_steps=None):
         vv = bf16_bits_to_f64(query_token_bits(wl.seed, KIND_V, 0, qids, pos, wl.kv_heads, wl.head_dim, 0))[None]
         t1 = time.perf_counter()
         sh.step(qv, kv, vv)
+        if warm > 0:
+            warm -= 1
+            continue
         times.append(time.perf_counter() - t1)
         step += 1
-        if sum(times) >= budget_s or (max_steps and step >= max_steps):
+        if (max_steps and step >= max_steps) or (not max_steps and sum(times) >= budget_s):
             break
-    return float(np.mean(times)), len(occ), wl.layers, step
+    return float(np.mean(times)), len(occ), wl.layers, step, len(live)
 
 
 def run_reference(args):
-    t_step, live, L, n = oracle_sample(budget_s=args.ref_budget, t0=args.t0,
-                                       max_steps=args.steps + args.warmup)
-    value = live / (L * t_step)
+    """The reference arm of this tier is the oracle (fp64 CPU).  A step = one oracle
+    layer-iteration of a 4-row shard holding the live queries of the t0 batch at the
+    12.5/37.5/62.5/87.5% length quantiles (the dense oracle's cost is linear in
+    rows; the sample's mean length tracks the batch's), so W + K steps end within
+    about a minute; tokens/s is extrapolated to all L layers: m / (L * t_step)."""
+    m = 4
+    t_step, m, L, n, live = oracle_sample(t0=args.t0, max_steps=args.steps, n_slots=m,
+                                          warmup=args.warmup)
+    value = m / (L * t_step)
     cores = 1
     line = {
         "impl": "reference", "metric": "decode tokens/s (7B-shape Baton batch)",
-        "value": value, "unit": "tokens/s", "n_gpus": args.gpus, "steps": n, "warmup": 0,
-        "ms_per_step": t_step * L * 1e3, "higher_is_better": True, "scaling": "weak",
+        "value": value, "unit": "tokens/s", "n_gpus": args.gpus, "steps": n, "warmup": args.warmup,
+        "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (keyed generator)",
         "config": {"workload": "7b", "t0": args.t0},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle",
-                         "sample": f"O-2 Shard.step (fp64 NumPy), 1 of {L} layers, {live} live slots "
-                                   f"at iteration {args.t0}, {n} steps; extrapolated x{L} layers"},
+                         "sample": f"O-2 Shard.step (fp64 NumPy), per step 1 of {L} layers x {m} of {live} "
+                                   f"live slots (length quantiles) at iteration {args.t0}; {n} timed steps "
+                                   f"after {args.warmup} warm-up; tokens/s = {m} / ({L} x step time)"},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -595,7 +619,7 @@ def main():
                            "h2d_bytes_per_step": int(r["e2e"]["h2d"]),
                            "d2h_bytes_per_step": int(r["e2e"]["d2h"])}
         if world == 1 and not args.no_cpu_baseline:
-            t_step, live, L, n = oracle_sample(budget_s=15.0, t0=args.t0)
+            t_step, live, L, n, _ = oracle_sample(budget_s=15.0, t0=args.t0)
             line["cpu_baseline"] = {
                 "value": live / (L * t_step), "unit": "tokens/s", "cores": 1, "kind": "oracle",
                 "sample": f"O-2 Shard.step (fp64 NumPy, single thread), 1 of {L} layers, {live} live "
