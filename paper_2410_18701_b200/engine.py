@@ -49,7 +49,8 @@ class StepStats:
 class Engine:
     def __init__(self, wl, rank=0, world=1, device=None, group=None, keep_outputs=False,
                  keep_layers=None, token_source=None, prefill_source=None, use_graph=True,
-                 stash_host=False, policy="baton", prefill_attention=False):
+                 stash_host=False, policy="baton", prefill_attention=False, async_prefill=False,
+                 prefill_lookahead=None):
         self.wl = wl
         self.rank = rank
         self.world = world
@@ -79,6 +80,13 @@ class Engine:
         # P&D accounting: run a8 (baton_prefill_attention, every layer) on each fresh
         # insert, so a policy comparison charges the decoupled prefill its attention
         self.prefill_attention = prefill_attention
+        # asynchronous P&D: queued fresh queries are prefilled on a side
+        # stream ahead of their insert (keyed K/V + a8 when prefill_attention);
+        # the insert waits on that query's event only
+        self.async_prefill = async_prefill
+        self.prefill_stream = torch.cuda.Stream(device=self.device) if async_prefill else None
+        self.prefill_lookahead = prefill_lookahead or 2 * self.B
+        self.prefetched: Dict[int, Tuple[torch.Tensor, torch.Tensor, torch.cuda.Event]] = {}
         self.use_graph = use_graph
         self.staging = {(self.q.data_ptr(), self.k_new.data_ptr(), self.v_new.data_ptr())}
         # P:L147 "moved to the host memory": stored K/V in pinned host memory (the
@@ -266,6 +274,12 @@ class Engine:
             for b, q, n, home in ins:
                 if home is not None:
                     K, V = self.stash.pop(q)
+                elif q in self.prefetched:
+                    K, V, ev = self.prefetched.pop(q)
+                    torch.cuda.current_stream(self.device).wait_event(ev)
+                    # allocated on the prefill stream, read on this one
+                    K.record_stream(torch.cuda.current_stream(self.device))
+                    V.record_stream(torch.cuda.current_stream(self.device))
                 else:
                     K, V = self._prefill(q, n)
                     if self.prefill_attention:
@@ -277,8 +291,28 @@ class Engine:
             sh.baton_insert_many(slots, ks, vs, lens)
             stats.inserted = len(ins)
             stats.insert_rows = sum(lens)
+        if self.async_prefill:
+            self._prefetch()
         stats.S = sh.S
         return stats
+
+    def _prefetch(self):
+        """Launch the prefill of the next queued fresh queries on the side stream."""
+        pl = self.planner
+        todo = []
+        for e in list(pl.queue)[:self.prefill_lookahead]:
+            if e.home is None and e.qid not in self.prefetched:
+                todo.append(e)
+        if not todo:
+            return
+        with torch.cuda.stream(self.prefill_stream):
+            for e in todo:
+                K, V = self._prefill(e.qid, e.length)
+                if self.prefill_attention:
+                    self._prefill_attn(e.qid, e.length, K, V)
+                ev = torch.cuda.Event()
+                ev.record(self.prefill_stream)
+                self.prefetched[e.qid] = (K, V, ev)
 
     def run(self, max_iters=None):
         all_stats = []

@@ -8,7 +8,9 @@ Runs the whole synthetic dataset through the same libbaton kernels under
   * "shape" -- Baton WITHOUT P&D ("Ours"): a new query is prefilled
                inside the batch, every row padded to its prompt length (NEXT-1);
   * "baton" -- Baton WITH P&D decoupling ("Ours-PD"): width-1 decode for
-               everybody, the prompt prefilled separately by a8;
+               everybody, the prompt prefilled separately by a8 -- in the decode
+               stream, and asynchronously on a side stream ahead of the insert
+               (P:L215, Engine(async_prefill=True));
 and reports, per batch size, the completion time of the dataset (device time of
 all iterations) and useful decode tokens/s: the B200 counterpart of Tables 2/3
 (P:L230-289), with the paper's datasets replaced by the length mixes of P:L212.
@@ -42,9 +44,10 @@ def dataset(name, batch):
                     max_ctx=4096)
 
 
-def run(name, batch, policy):
+def run(name, batch, policy, async_prefill=False):
     wl = dataset(name, batch)
-    eng = Engine(wl, policy=policy, use_graph=True, prefill_attention=policy != "shape")
+    eng = Engine(wl, policy=policy, use_graph=True, prefill_attention=policy != "shape",
+                 async_prefill=async_prefill)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -70,8 +73,10 @@ def main():
     for b in [int(x) for x in args.batches.split(",")]:
         base = run(args.dataset, b, "rtc")
         bat = run(args.dataset, b, "baton")
+        asy = run(args.dataset, b, "baton", async_prefill=True)
         line = {"dataset": args.dataset, "batch": b, "benchmark_rtc": base, "baton_pd": bat,
-                "completion_speedup": base["ms"] / bat["ms"]}
+                "baton_pd_async": asy, "completion_speedup": base["ms"] / bat["ms"],
+                "async_over_sync_pd": bat["ms"] / asy["ms"]}
         if not args.no_shape:
             try:
                 shp = run(args.dataset, b, "shape")

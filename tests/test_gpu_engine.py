@@ -48,9 +48,9 @@ def _check_state(eng, sim):
         assert np.array_equal(bf16_bits(Vd), _f64_to_bf16_bits(Vo)), f"V slot {b}"
 
 
-def _replay(wl, check_every=1, use_graph=True):
+def _replay(wl, check_every=1, use_graph=True, **engine_kwargs):
     from paper_2410_18701_b200.engine import Engine
-    eng = Engine(wl, keep_outputs=True, use_graph=use_graph)
+    eng = Engine(wl, keep_outputs=True, use_graph=use_graph, **engine_kwargs)
     sim = Simulator(wl, kv=True, keep_outputs=True, fill=np.nan)
     n = 0
     while True:
@@ -227,3 +227,13 @@ def test_early_prefetch_sees_previous_append(hq, hkv):
             sh.baton_decode_attention(l, q, ref)                  # stateless, no early
             torch.cuda.synchronize()
             assert torch.equal(o1, ref), (it, l)
+
+
+@pytest.mark.parametrize("seed", [5, 12])
+def test_async_prefill_replay(seed):
+    """Asynchronous P&D: queued queries are prefilled (keyed K/V + a8 on
+    their prompts) on a side stream ahead of their insert; the state and every
+    output stay bit-exact with the oracle."""
+    require_cuda()
+    wl = random_stream(seed)
+    _replay(wl, async_prefill=True, prefill_attention=wl.head_dim == 128, prefill_lookahead=3)
