@@ -322,11 +322,21 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
         if (d.flags & F_END) break;
         if (trace && threadIdx.x == 0 && (d.flags & F_FIRST) && citem < 8)
             tr[10 + 4 * citem] = gtimer();
-        if (trace && threadIdx.x == 0 && ctile < (TRACE_W - 40) / 2) {
+        if (trace && threadIdx.x == 0 && ctile < 4) {
             tr[40 + 2 * ctile] = t_w;
             tr[41 + 2 * ctile] = gtimer() | (was_ready ? (1LL << 62) : 0);
         }
         ++ctile;
+        // phase clocks of warp 0 on its 3rd tile (debug): [48] start [49] S done
+        // [50] softmax done [51] P fragments done [52] P.V done [53] released
+        const bool ph = trace && warp == 0 && ctile == 3;
+        auto phase_clock = [&](int slot, float dep) {
+            if (ph) {
+                if (__float_as_uint(dep) == 0x7fc00001u) tr[63] = 1;   // wait for dep
+                if (lane == 0) tr[slot] = clock64();
+            }
+        };
+        phase_clock(48, 0.f);
         if (d.flags & F_FIRST) {
             const uint32_t *qw = reinterpret_cast<const uint32_t *>(st.q + r4 * QROW);
 #pragma unroll
@@ -407,6 +417,7 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
                 mx0 = fmaxf(mx0, __shfl_xor_sync(FULL_MASK, mx0, o2));
                 mx1 = fmaxf(mx1, __shfl_xor_sync(FULL_MASK, mx1, o2));
             }
+            phase_clock(49, x[0][0] + x[NG - 1][3]);
             const float mn0 = fmaxf(m[0], mx0), mn1 = fmaxf(m[1], mx1);
             const float rf0 = (mn0 == -INFINITY) ? 0.f : mn0, rf1 = (mn1 == -INFINITY) ? 0.f : mn1;
             const float al0 = ex2(m[0] - rf0), al1 = ex2(m[1] - rf1);
@@ -451,6 +462,7 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
             // or p23 (k >= 8).
             const int srcA = c2 * 4 + (r4 >> 1), srcB = (c2 + 1) * 4 + (r4 >> 1);
             const uint32_t sh = (r4 & 1) ? 16 : 0;
+            phase_clock(50, o[7][3] + l[0]);
             uint32_t pb0[NG], pb1[NG];
 #pragma unroll
             for (int j = 0; j < NG; ++j) {
@@ -459,6 +471,7 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
                 pb0[j] = ((x0 >> sh) & 0xffffu) | (((x1 >> sh) & 0xffffu) << 16);
                 pb1[j] = ((y0 >> sh) & 0xffffu) | (((y1 >> sh) & 0xffffu) << 16);
             }
+            phase_clock(51, __uint_as_float(pb0[0] ^ pb1[NG - 1]));
             // ---- O^T += V^T P^T: A = V^T (16 dims x 16 keys) via ldmatrix.trans
 #pragma unroll
             for (int mt = 0; mt < 8; ++mt) {
@@ -473,7 +486,9 @@ decode_gqa_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constan
             }
         }
         __syncwarp();
+        phase_clock(52, o[0][0] + o[7][3]);
         if (lane == 0) mbar_arrive(&sm.empty[stage]);
+        phase_clock(53, 0.f);
         if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -639,6 +654,18 @@ bool gqa_supported(int q_heads, int kv_heads, int head_dim) {
     return head_dim == D && kv_heads > 0 && q_heads == GS * kv_heads;
 }
 
+cudaError_t launch_gqa_combine(const DecodeArgs &a, cudaStream_t s) {
+    static int num_sms = 0;
+    if (!num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return launch_pdl(decode_combine_kernel, dim3(num_sms), dim3(128), 0, s, a.lens,
+                      (const float *)a.partial, static_cast<__nv_bfloat16 *>(a.out), a.slots,
+                      a.q_heads, a.max_chunks);
+}
+
 template <int CW, int KP, int STAGES, int MINB, int RB = 2>
 cudaError_t launch_gqa_v(const DecodeArgs &a, cudaStream_t s) {
     constexpr int TILE = CW * KP, THREADS = (CW + 1) * 32;
@@ -688,16 +715,16 @@ cudaError_t launch_gqa_v(const DecodeArgs &a, cudaStream_t s) {
         return cudaErrorInvalidValue;
     cudaError_t e = launch_pdl(decode_gqa_kernel<CW, KP, STAGES, RB, MINB>, dim3(MINB * num_sms), dim3(THREADS), smem, s, km, vm, p);
     if (e != cudaSuccess) return e;
-    return launch_pdl(decode_combine_kernel, dim3(num_sms), dim3(128), 0, s, a.lens,
-                      (const float *)a.partial, static_cast<__nv_bfloat16 *>(a.out), a.slots,
-                      a.q_heads, a.max_chunks);
+    return launch_gqa_combine(a, s);
 }
 
 cudaError_t launch_decode_gqa(const DecodeArgs &a, cudaStream_t s) {
+    // default: the tcgen05 kernel (decode_gqa_tc.cu) + the PDL combine; the mma.sync
+    // kernel of this file stays selectable (profiles/r01_gqa_engine_sweep.md)
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("BATON_GQA_VARIANT");
-        v = e ? atoi(e) : 0;
+        v = e ? atoi(e) : 20;
     }
     // sweep variants (profiles/r01_gqa_engine_sweep.md); 0 is the default
     switch (v) {
@@ -706,7 +733,18 @@ cudaError_t launch_decode_gqa(const DecodeArgs &a, cudaStream_t s) {
         case 6: return launch_gqa_v<4, 32, 2, 1>(a, s);      // 2 MMA chains / warp
         case 9: return launch_gqa_v<8, 16, 2, 1>(a, s);      // 8 consumer warps
         case 10: return launch_gqa_v<4, 32, 3, 1, 1>(a, s);  // 2 chains, 3 stages, 1 merge buffer
-        default: return launch_gqa_v<4, 16, 4, 1>(a, s);
+        case 20: {                                           // tcgen05 (decode_gqa_tc.cu)
+            cudaError_t e = launch_decode_gqa_tc(a, s, false);
+            if (e != cudaSuccess || a.dry) return e;
+            return launch_gqa_combine(a, s);
+        }
+        case 21: return launch_decode_gqa_tc(a, s, true);    // tcgen05, in-kernel merge
+        default: {
+            cudaError_t e = launch_decode_gqa_tc(a, s, false);
+            if (e != cudaSuccess || a.dry) return e;
+            return launch_gqa_combine(a, s);
+        }
+        case 0: return launch_gqa_v<4, 16, 4, 1>(a, s);      // mma.sync, 4 warps x 16 keys
     }
 }
 

@@ -40,6 +40,9 @@ cudaError_t launch_decode_attention(const DecodeArgs &a, cudaStream_t s);
 // GQA groups of 8 q heads per kv head (head_dim 128): tensor-core variant
 bool gqa_supported(int q_heads, int kv_heads, int head_dim);
 cudaError_t launch_decode_gqa(const DecodeArgs &a, cudaStream_t s);
+// tcgen05 variants: 20 = separate combine kernel, 21 = fused in-kernel merge
+cudaError_t launch_decode_gqa_tc(const DecodeArgs &a, cudaStream_t s, bool fused);
+cudaError_t launch_gqa_combine(const DecodeArgs &a, cudaStream_t s);
 
 // ------------------------------------------------------------ metadata / mask
 cudaError_t launch_mask_update(uint8_t *mask, int32_t *S, int32_t *lens, int slots, int max_ctx,

@@ -27,8 +27,9 @@ def main():
     args = ap.parse_args()
     lib = _lib._load()
     mha = args.config != "70b"
-    fn = lib.baton_debug_mha_trace if mha else lib.baton_debug_gqa_trace
-    shape = (8, 1024, 32) if mha else (8, 256, 64)
+    tc = not mha and os.environ.get("BATON_GQA_VARIANT") in ("20", "21")
+    fn = lib.baton_debug_mha_trace if mha else (lib.baton_debug_gqa_tc_trace if tc else lib.baton_debug_gqa_trace)
+    shape = (8, 1024, 32) if mha else ((1, 160, 68) if tc else (8, 256, 64))
     fn.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t]
     hook = {}
     orig_run = bench_configs.Engine.iteration
@@ -60,6 +61,15 @@ def main():
     bench_configs.Engine.iteration = counted
     res = bench_configs.run(args.config, steps, warm, torch.device("cuda"))
     buf = hook["buf"]
+    if tc:   # one launch (the step's last layer): entry spread, first S issue, exits
+        rows = buf[0][buf[0][:, 0] > 0]
+        t0 = rows[:, 0].min()
+        first_s = [r[4] - t0 for r in rows if r[4]]
+        print(json.dumps({"tc_ctas": len(rows), "enter_spread_ns": int(rows[:, 0].max() - t0),
+                          "first_S_med_ns": float(np.median(first_s)), "first_S_min_ns": int(min(first_s)),
+                          "exit_med_ns": float(np.median(rows[:, 1] - t0)), "exit_max_ns": int(rows[:, 1].max() - t0)}))
+        print(json.dumps({"config_run": res}))
+        return
     t0 = buf[:, :, 0][buf[:, :, 0] > 0].min()
     layers = []
     for s in range(8):
@@ -85,7 +95,8 @@ def main():
                      for k in range(min(int(r[3]), nk))],
                     [] if mha else
                     [[int(r[40 + 2 * t] - t0), int((r[41 + 2 * t] & ((1 << 62) - 1)) - t0),
-                      int(r[41 + 2 * t] >> 62)] for t in range(12) if r[40 + 2 * t]],
+                      int(r[41 + 2 * t] >> 62)] for t in range(4) if r[40 + 2 * t]]
+                    + [[int(x) for x in r[48:54]]],
                     int(r[5] - t0) if mha and r[5] else 0]
                    for r in rows]   # smid, enter, built, exit, items (w, issued, first ready, done),
         #                             tile ready times (GQA), producer past the wait (MHA)
