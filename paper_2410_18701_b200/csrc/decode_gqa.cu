@@ -738,7 +738,9 @@ cudaError_t launch_decode_gqa(const DecodeArgs &a, cudaStream_t s) {
             if (e != cudaSuccess || a.dry) return e;
             return launch_gqa_combine(a, s);
         }
-        case 21: return launch_decode_gqa_tc(a, s, true);    // tcgen05, in-kernel merge
+        case 21:                                             // tcgen05, in-kernel merge
+            if (a.max_chunks <= 32) return launch_decode_gqa_tc(a, s, true);
+            [[fallthrough]];
         default: {
             cudaError_t e = launch_decode_gqa_tc(a, s, false);
             if (e != cudaSuccess || a.dry) return e;

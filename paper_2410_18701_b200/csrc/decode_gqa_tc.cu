@@ -90,6 +90,7 @@ struct __align__(1024) TSmem {
     int32_t red[2][2][4][GS];                // [group][tile parity][warp][head] tile max (encoded)
     float lsum[2][4][GS];
     int32_t last[2];
+    float mf[2][32][GS], ml[2][32][GS];      // fused merge: chunk m / l per head (<= 32 chunks)
     uint32_t tmem_base;
 };
 
@@ -506,38 +507,57 @@ decode_gqa_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_cons
                         if (r == 0) sm.last[grp] = atom_add_acq_rel_gpu(tk, 1) == d.nchunks - 1;
                         named_bar_sync(1 + grp, 128);
                         if (sm.last[grp]) {
-#pragma unroll 1
-                            for (int h = 0; h < GS; ++h) {
-                                const float *pc = p.partial + (bh0 + h) * p.max_chunks * (D + PREC_PAD);
-                                float Mc = -INFINITY;
-                                for (int c0 = 0; c0 < d.nchunks; c0 += 8) {
-                                    float mv[8];
-#pragma unroll
-                                    for (int k = 0; k < 8; ++k)
-                                        mv[k] = c0 + k < d.nchunks ? __ldcg(pc + (c0 + k) * (D + PREC_PAD) + D) : -INFINITY;
-#pragma unroll
-                                    for (int k = 0; k < 8; ++k) Mc = fmaxf(Mc, mv[k]);
-                                }
-                                float Lc = 0.f, Oc = 0.f;
-                                for (int c0 = 0; c0 < d.nchunks; c0 += 8) {
-                                    float mv[8], lv[8], ov[8];
-#pragma unroll
-                                    for (int k = 0; k < 8; ++k) {
-                                        const bool ok = c0 + k < d.nchunks;
-                                        const float *rr = pc + (ok ? c0 + k : 0) * (D + PREC_PAD);
-                                        mv[k] = ok ? __ldcg(rr + D) : -INFINITY;
-                                        lv[k] = ok ? __ldcg(rr + D + 1) : 0.f;
-                                        ov[k] = ok ? __ldcg(rr + r) : 0.f;
-                                    }
-#pragma unroll
-                                    for (int k = 0; k < 8; ++k) {
-                                        const float f = (mv[k] == -INFINITY) ? 0.f : ex2(mv[k] - Mc);
-                                        Lc = fmaf(f, lv[k], Lc);
-                                        Oc = fmaf(f, ov[k], Oc);
-                                    }
-                                }
-                                p.out[(bh0 + h) * D + r] = __float2bfloat16_rn(Lc > 0.f ? Oc / Lc : 0.f);
+                            // parallel merge of the 8 heads: (A) thread (head, chunk) loads m, l;
+                            // the group derives each chunk's weight f = 2^(m_c - M) in smem;
+                            // (B) thread = dim accumulates all heads, 4 chunks per round trip.
+                            // Chunks are taken in ascending order (batch-invariant).
+                            const int nch = d.nchunks;
+                            for (int i2 = r; i2 < GS * nch; i2 += 128) {
+                                const int h = i2 & 7, c = i2 >> 3;
+                                const float *rr = p.partial + ((bh0 + h) * p.max_chunks + c) * (D + PREC_PAD);
+                                sm.mf[grp][c][h] = __ldcg(rr + D);
+                                sm.ml[grp][c][h] = __ldcg(rr + D + 1);
                             }
+                            named_bar_sync(1 + grp, 128);
+                            float Mh[GS], Lh[GS];
+#pragma unroll
+                            for (int h = 0; h < GS; ++h) {
+                                float Mc = -INFINITY;
+                                for (int c = 0; c < nch; ++c) Mc = fmaxf(Mc, sm.mf[grp][c][h]);
+                                float Lc = 0.f;
+                                for (int c = 0; c < nch; ++c) {
+                                    const float mc = sm.mf[grp][c][h];
+                                    Lc = fmaf((mc == -INFINITY) ? 0.f : ex2(mc - Mc), sm.ml[grp][c][h], Lc);
+                                }
+                                Mh[h] = Mc;
+                                Lh[h] = Lc;
+                            }
+                            float Oh[GS];
+#pragma unroll
+                            for (int h = 0; h < GS; ++h) Oh[h] = 0.f;
+                            for (int c0 = 0; c0 < nch; c0 += 4) {
+                                float ov[4][GS];
+#pragma unroll
+                                for (int k = 0; k < 4; ++k)
+#pragma unroll
+                                    for (int h = 0; h < GS; ++h)
+                                        ov[k][h] = c0 + k < nch
+                                                       ? __ldcg(p.partial + ((bh0 + h) * p.max_chunks + c0 + k) * (D + PREC_PAD) + r)
+                                                       : 0.f;
+#pragma unroll
+                                for (int k = 0; k < 4; ++k)
+#pragma unroll
+                                    for (int h = 0; h < GS; ++h) {
+                                        if (c0 + k < nch) {
+                                            const float mc = sm.mf[grp][c0 + k][h];
+                                            const float f = (mc == -INFINITY) ? 0.f : ex2(mc - Mh[h]);
+                                            Oh[h] = fmaf(f, ov[k][h], Oh[h]);
+                                        }
+                                    }
+                            }
+#pragma unroll
+                            for (int h = 0; h < GS; ++h)
+                                p.out[(bh0 + h) * D + r] = __float2bfloat16_rn(Lh[h] > 0.f ? Oh[h] / Lh[h] : 0.f);
                             if (r == 0) *tk = 0;   // ready for the next launch
                         }
                     }
@@ -586,6 +606,7 @@ cudaError_t launch_decode_gqa_tc(const DecodeArgs &a, cudaStream_t s, bool fused
     p.partial = a.partial;
     p.tickets = a.tickets;
     p.fused = fused;
+    if (fused && a.max_chunks > 32) return cudaErrorInvalidValue;   // see TSmem::mf
     p.B = a.slots;
     p.Hq = a.q_heads;
     p.Hkv = a.kv_heads;
