@@ -17,7 +17,7 @@ decisions is implemented separately by the oracle and
 by the product scheduler.  Nothing here implements Baton's arithmetic.
 """
 from dataclasses import dataclass, field
-from typing import Dict, List, Tuple
+from typing import Optional, Dict, List, Tuple
 
 import numpy as np
 
@@ -34,6 +34,7 @@ class Query:
     l_q: int         # prefilled length (prompt), >= 1
     A: int           # answer length = number of decode iterations, >= 1
     kind: str = ""
+    priority: int = 0  # SLA priority (reading C25): higher preempts lower
 
 
 @dataclass
@@ -62,6 +63,9 @@ class Workload:
     scales: Tuple[int, int, int] = SCALES_FLAT
     control: ControlEvents = field(default_factory=ControlEvents)
     iterations: int = -1  # -1 = until every query finished
+    # P:L146-147 batch-size governor (reading C26): (hi, lo) fractions of a shard's
+    # token budget active_slots x max_ctx; None = off
+    governor: Optional[Tuple[float, float]] = None
 
     @property
     def slots_per_gpu(self):

@@ -30,6 +30,19 @@ C9), so its A decode iterations follow it; everybody else decodes as usual in th
 same padded iteration (the bubble of P:L128).  Control events are not used with
 this policy.
 
+Priorities and the memory governor (readings C25/C26; off unless the
+workload sets query priorities / ``governor``):
+  * the queue is served by (priority desc, then stored victims -- newest batch
+    first, in eviction order -- then FCFS arrival order);
+  * C25: before any insert of the phase, if the best waiting query has no
+    eligible free (and admissible) slot while a live query of LOWER priority sits
+    on an eligible shard, that query is stored (victim order: lowest priority, then
+    C17) -- at most one such preemption per iteration -- and the urgent query then
+    takes the freed slot;
+  * C26: after step 5, a shard whose live tokens exceed hi * T (T = active slots x
+    max_ctx) stores victims (same order) until it does not; an insert is admitted
+    only if live tokens + its length <= lo * T on its shard.
+
 Iteration 0 runs only step 6.  A query's tokens are keyed by (qid, position) so a
 decode step of a query with live length n (after the append) handles position
 n-1 (C3); its prefilled K/V are positions [0, l_q).
@@ -84,6 +97,8 @@ class Simulator:
         self.inserted_at = {}
         self.arrivals = deque(sorted(wl.queries, key=lambda q: (q.arrival, q.qid)))
         self.queue = deque()     # entries: (qid, length, K, V, home shard or None)
+        self.ticket = {}         # qid -> queue order key within a priority class (C25)
+        self.prio = {q.qid: q.priority for q in wl.queries}
         self.n_active = wl.initial_active()
         self.outputs: Dict[Tuple[int, int], np.ndarray] = {}
         self.masks: List[List[np.ndarray]] = []
@@ -92,6 +107,8 @@ class Simulator:
         if policy == "shape":
             c = wl.control
             assert not (c.preempt or c.preempt_frac or c.resize), "shape policy: no control events"
+            assert wl.governor is None and not any(q.priority for q in wl.queries), \
+                "shape policy: no priorities / governor (stored K/V re-enter by embedding)"
         self.t = 0
 
     # ------------------------------------------------------------------ helpers
@@ -109,8 +126,30 @@ class Simulator:
         return out
 
     def _victim_order(self, live):
-        # C17: most recently inserted first, ties by higher qid
-        return sorted(live, key=lambda x: (-self.inserted_at[x[1]], -x[1]))
+        # C25 lowest priority first; C17 then most recently inserted, ties by higher qid
+        return sorted(live, key=lambda x: (self.prio[x[1]], -self.inserted_at[x[1]], -x[1]))
+
+    def _usage(self, r):
+        """Live tokens held by shard r (C26)."""
+        sh = self.shards[r]
+        lens = sh.lens()
+        return int(sum(lens[b] for b in sh.occupied()))
+
+    def _budget(self):
+        return self.active_per_shard() * self.wl.max_ctx
+
+    def _govern(self, rec):
+        """C26: store victims while a shard exceeds hi * T."""
+        gov = self.wl.governor
+        if gov is None:
+            return []
+        out = []
+        for r, sh in enumerate(self.shards):
+            while self._usage(r) > gov[0] * self._budget() and sh.occupied():
+                live = [(r * self.Bg + b, int(sh.qid[b])) for b in sh.occupied()]
+                g, _ = self._victim_order(live)[0]
+                out.append(self._evict(g, rec))
+        return out
 
     def _prefill(self, qid, length):
         wl = self.wl
@@ -293,21 +332,63 @@ class Simulator:
                         rec.moved.append((r * self.Bg + old, r * self.Bg + new))
         return out
 
+    def _requeue(self, victims):
+        """Stored victims re-enter ahead of every earlier entry of their priority,
+        in eviction order (C8/C17; C25 orders across priorities)."""
+        for i, v in enumerate(victims):
+            self.ticket[v[0]] = -(self.t * 100000) + i
+            self.queue.append(v)
+
+    def _admissible(self, r, length):
+        gov = self.wl.governor
+        return gov is None or self._usage(r) + length <= gov[1] * self._budget()
+
+    def _order(self):
+        return sorted(range(len(self.queue)),
+                      key=lambda i: (-self.prio[self.queue[i][0]], self.ticket[self.queue[i][0]]))
+
+    def _free(self):
+        a = self.active_per_shard()
+        reserved = {r * self.Bg + b for r in range(self.G) for b, _, _ in self.pending[r]}
+        return [r * self.Bg + b for r, sh in enumerate(self.shards) for b in range(a)
+                if sh.qid[b] < 0 and r * self.Bg + b not in reserved]
+
+    def _priority_preempt(self, rec):
+        """C25, before any insert: the best waiting query, if it has no
+        eligible admissible free slot, stores the lowest-priority live query of an
+        eligible shard whose priority is lower than its own."""
+        if not self.queue:
+            return
+        qid0, length, _, _, home = self.queue[self._order()[0]]
+        if any((home is None or g // self.Bg == home) and self._admissible(g // self.Bg, length)
+               for g in self._free()):
+            return
+        a = self.active_per_shard()
+        live = [(g, q) for g, q in self._live()
+                if (home is None or g // self.Bg == home) and g % self.Bg < a
+                and self.prio[q] < self.prio[qid0]]
+        if not live:
+            return
+        g, _ = self._victim_order(live)[0]
+        v = self._evict(g, rec)
+        self._release_all(rec)
+        self._requeue([v])
+
     def _insert_phase(self, rec):
         while self.arrivals and self.arrivals[0].arrival <= self.t:
             q = self.arrivals.popleft()
+            self.ticket[q.qid] = len(self.ticket) + 1
             self.queue.append((q.qid, q.l_q, None, None, None))
-        a = self.active_per_shard()
+        if self.t > 0 and self.policy == "pd":
+            self._priority_preempt(rec)
         while self.queue:
-            reserved = {r * self.Bg + b for r in range(self.G) for b, _, _ in self.pending[r]}
-            free = [r * self.Bg + b for r, sh in enumerate(self.shards) for b in range(a)
-                    if sh.qid[b] < 0 and r * self.Bg + b not in reserved]
-            if not free:
-                break
+            free = self._free()
             pick = None
-            for i, entry in enumerate(self.queue):
+            for i in self._order():
+                entry = self.queue[i]
                 home = entry[4]
-                elig = [g for g in free if home is None or g // self.Bg == home]
+                elig = [g for g in free if (home is None or g // self.Bg == home)
+                        and self._admissible(g // self.Bg, entry[1])]
                 if elig:
                     pick = (i, elig[0])
                     break
@@ -346,8 +427,11 @@ class Simulator:
             victims += self._resize(rec)
             if victims:
                 self._release_all(rec)
-            for v in reversed(victims):
-                self.queue.appendleft(v)
+            gv = self._govern(rec)
+            if gv:
+                self._release_all(rec)
+            victims += gv
+            self._requeue(victims)
         self._insert_phase(rec)
         for sh in self.shards:
             rec.S.append(sh.S)

@@ -9,7 +9,11 @@ and replicated: every rank runs the same planner on the same inputs (the
 workload, the control events, and the per-iteration completion flags that the
 engine all-gathers), so no rank ever broadcasts a decision.
 
-Policy readings (DESIGN.md §3): C5 release after removals and before inserts;
+Policy readings: C25 priorities (the queue is served by priority,
+then stored victims newest first, then FCFS; at most one preemption of a lower-
+priority live query per iteration, before the inserts), C26 the memory governor
+((hi, lo) of a rank's token budget: store victims above hi, admit inserts up to
+lo); C5 release after removals and before inserts;
 C7 inserts of an iteration in ascending slot order; C8 FCFS, lowest free slot,
 stored queries re-enter at the queue head; C9 A decode iterations per query;
 C17 victims = most recently inserted, ties by higher qid; C18/C19 resize and
@@ -59,6 +63,8 @@ class Planner:
         self.raw = {}                                         # shape: gslot -> prompt length
         self.policy = policy
         self.drained = set()                                  # rtc: finished but resident
+        self.prio = {q.qid: q.priority for q in wl.queries}
+        self.ticket = {}                                      # queue order within a priority
         self.wl = wl
         self.world = world
         if wl.slots % world:
@@ -114,8 +120,31 @@ class Planner:
         return flags
 
     def _victims(self, candidates, n):
-        order = sorted(candidates, key=lambda gq: (self.entered[gq[1]], gq[1]), reverse=True)
+        # C25 lowest priority first; C17 then most recently inserted, ties by higher qid
+        order = sorted(candidates, key=lambda gq: (self.prio[gq[1]], -self.entered[gq[1]], -gq[1]))
         return order[:n]
+
+    def _usage(self, r):
+        """Live tokens on rank r (C26)."""
+        base = r * self.per_rank
+        return sum(self.length[base + b] for b in range(self.per_rank) if self.occupant[base + b] >= 0)
+
+    def _admissible(self, r, length):
+        gov = self.wl.governor
+        return gov is None or self._usage(r) + length <= gov[1] * self.active * self.wl.max_ctx
+
+    def _requeue(self, entries):
+        for i, e in enumerate(entries):
+            self.ticket[e.qid] = -(self.t * 100000) + i
+            self.queue.append(e)
+
+    def _order(self):
+        return sorted(range(len(self.queue)),
+                      key=lambda i: (-self.prio[self.queue[i].qid], self.ticket[self.queue[i].qid]))
+
+    def _free(self):
+        return [r * self.per_rank + b for r in range(self.world) for b in range(self.active)
+                if self.occupant[r * self.per_rank + b] < 0]
 
     # ---------------------------------------------------------------- one iteration
     def plan(self, all_flags=None):
@@ -160,8 +189,18 @@ class Planner:
                     stored.append(self._store(g, q, d))
             if self.t in ctl.resize:
                 stored += self._resize(ctl.resize[self.t], d)
-            for e in reversed(stored):
-                self.queue.appendleft(e)
+            gov = self.wl.governor
+            if gov is not None:                               # C26
+                for r in range(self.world):
+                    while self._usage(r) > gov[0] * self.active * self.wl.max_ctx:
+                        base = r * self.per_rank
+                        occ = [(base + b, self.occupant[base + b]) for b in range(self.per_rank)
+                               if self.occupant[base + b] >= 0]
+                        if not occ:
+                            break
+                        g, q = self._victims(occ, 1)[0]
+                        stored.append(self._store(g, q, d))
+            self._requeue(stored)
         self._admit()
         self._fill(d)
         self.t += 1
@@ -208,21 +247,42 @@ class Planner:
         while (self.next_arrival < len(self.pending)
                and self.pending[self.next_arrival].arrival <= self.t):
             q = self.pending[self.next_arrival]
+            self.ticket[q.qid] = len(self.ticket) + 1
             self.queue.append(QueueEntry(q.qid, q.l_q, None))
             self.next_arrival += 1
+
+    def _priority_preempt(self, d):
+        """C25, before any insert: the best waiting query, if it has no
+        eligible admissible free slot, stores the lowest-priority live query of an
+        eligible rank whose priority is lower than its own."""
+        if not self.queue:
+            return
+        e0 = self.queue[self._order()[0]]
+        if any((e0.home is None or self.rank_of(g) == e0.home) and self._admissible(self.rank_of(g), e0.length)
+               for g in self._free()):
+            return
+        live = [(g, q) for g, q in self.live()
+                if (e0.home is None or self.rank_of(g) == e0.home) and self.local(g) < self.active
+                and self.prio[q] < self.prio[e0.qid]]
+        if not live:
+            return
+        g, q = self._victims(live, 1)[0]
+        self._requeue([self._store(g, q, d)])
 
     def _fill(self, d):
         if self.policy == "rtc" and self.live():
             return                                            # batch still running
+        if self.t > 0 and self.policy == "baton":
+            self._priority_preempt(d)
         while self.queue:
-            free = [r * self.per_rank + b for r in range(self.world) for b in range(self.active)
-                    if self.occupant[r * self.per_rank + b] < 0]
+            free = self._free()
             if not free:
                 return
             chosen = None
-            for idx, e in enumerate(self.queue):
+            for idx in self._order():
+                e = self.queue[idx]
                 for g in free:
-                    if e.home is None or self.rank_of(g) == e.home:
+                    if (e.home is None or self.rank_of(g) == e.home) and self._admissible(self.rank_of(g), e.length):
                         chosen = (idx, g)
                         break
                 if chosen:

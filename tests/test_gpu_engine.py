@@ -237,3 +237,15 @@ def test_async_prefill_replay(seed):
     require_cuda()
     wl = random_stream(seed)
     _replay(wl, async_prefill=True, prefill_attention=wl.head_dim == 128, prefill_lookahead=3)
+
+
+@pytest.mark.parametrize("seed", [1, 3, 8])
+def test_policy_stream_replay(seed):
+    """§3.3 policies (C25 priority preemption, C26 memory governor): the engine's
+    stores and re-inserts keep the state bit-exact and every output within 1e-2."""
+    require_cuda()
+    import sys
+    import os
+    sys.path.insert(0, os.path.dirname(__file__))
+    from test_oracle_policies import _policy_stream
+    _replay(_policy_stream(seed))
