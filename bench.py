@@ -33,6 +33,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 T0_DEFAULT = 512          # steady-state start iteration of the Poisson workload
+INS_AHEAD = 8             # e2e: steps of lookahead for the prefilled K/V H2D of upcoming inserts
 
 
 def _peaks():
@@ -348,7 +349,10 @@ def run_baton(args, rank, world, local_rank):
                       for shp in ((L, B, Hq, D), (L, B, Hkv, D), (L, B, Hkv, D))) for _ in range(2)]
         ready = [torch.cuda.Event() for _ in range(2)]
         free = [torch.cuda.Event() for _ in range(2)]
-        copy_stream = torch.cuda.Stream()
+        # two copy streams: a step's q/k/v must not queue behind a prefilled K/V
+        # transfer (hundreds of MB for one insert, several decode steps of PCIe time)
+        copy_stream = torch.cuda.Stream(priority=-1)
+        ins_stream = torch.cuda.Stream()
         res_h = torch.empty((B, Hq, D), dtype=torch.bfloat16).pin_memory()
         counters = {"h2d": 0, "d2h": 0}
 
@@ -366,8 +370,9 @@ def run_baton(args, rank, world, local_rank):
             torch.cuda.current_stream().wait_event(ready[slot])
             return sets[slot]
 
-        # prefilled K/V of the queries inserted at window step i arrive on the copy
-        # stream two steps ahead (inserts are known from the window plan)
+        # prefilled K/V of the queries inserted at window step i arrive on their own
+        # copy stream INS_AHEAD steps ahead (inserts are known from the window plan;
+        # one 7B insert of ~550 tokens is ~0.6 GB, ~12 ms of PCIe at 50 GB/s)
         ins_at = {}
         for q, n, t_ins in fresh:
             ins_at.setdefault(t_ins - t_base, []).append(q)
@@ -376,10 +381,10 @@ def run_baton(args, rank, world, local_rank):
         def prefetch_inserts(i):
             for q in ins_at.get(i, []):
                 a, b = pref_h[q]
-                with torch.cuda.stream(copy_stream):
+                with torch.cuda.stream(ins_stream):
                     da, db = a.to(dev, non_blocking=True), b.to(dev, non_blocking=True)
                     ev = torch.cuda.Event()
-                    ev.record(copy_stream)
+                    ev.record(ins_stream)
                 counters["h2d"] += (a.numel() + b.numel()) * 2
                 pref_dev[q] = (da, db, ev)
 
@@ -397,7 +402,7 @@ def run_baton(args, rank, world, local_rank):
         def step(eng2, i, warm):
             if i + 1 < n_iters:
                 h2d(i + 1)
-            prefetch_inserts(i + 2)
+            prefetch_inserts(i + INS_AHEAD)
             st_ = eng2.iteration()
             free[i % 2].record()
             res_h.copy_(eng2.out[L - 1], non_blocking=True)   # the step's result to the host
@@ -412,8 +417,8 @@ def run_baton(args, rank, world, local_rank):
         for ev in free:
             ev.record()
         h2d(0)
-        prefetch_inserts(0)
-        prefetch_inserts(1)
+        for i in range(INS_AHEAD):
+            prefetch_inserts(i)
         for i in range(W):
             step(eng, i, True)
         if world > 1:
