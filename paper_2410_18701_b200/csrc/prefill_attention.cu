@@ -40,6 +40,7 @@ constexpr int PF_M = 128;         // queries per tile (UMMA M, TMEM lanes)
 constexpr int PF_N = 64;          // keys per tile (UMMA N of S, K of PV)
 constexpr int PF_D = 128;         // head_dim
 constexpr int PF_THREADS = 192;   // 4 softmax warps + producer warp + MMA warp
+constexpr float RESCALE_T = 8.f;  // lazy-rescale threshold (log2 units): P <= 256
 constexpr int Q_BYTES = PF_M * PF_D * 2;        // 32 KB: two 16 KB swizzle regions (dims 0-63, 64-127)
 constexpr int Q_REGION = Q_BYTES / 2;
 constexpr int KV_BYTES = PF_N * PF_D * 2;       // 16 KB: two 8 KB regions
@@ -234,9 +235,13 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
                     r[c][i] = __float_as_uint(x);
                     mx = fmaxf(mx, x);
                 }
-            const float m_new = fmaxf(m, mx);
-            // a row may see only masked keys so far (extend: holes, padding): keep
-            // exp2 finite -- ex2(-inf - 0) = 0
+            // Lazy rescale: P is taken relative to a reference max m that moves only
+            // when the row max exceeds it by more than RESCALE_T (log2 units), so P <=
+            // 2^RESCALE_T (exact in fp32 accumulation, same bf16 rounding of P) and the
+            // O rows in TMEM are rescaled only on those tiles, not whenever the max moves.
+            // A row may see only masked keys so far (extend: holes, padding): keep exp2
+            // finite -- ex2(-inf - 0) = 0.
+            const float m_new = (mx > m + RESCALE_T || m == -INFINITY) ? fmaxf(m, mx) : m;
             const float mref = (m_new == -INFINITY) ? 0.f : m_new;
             const float alpha = ex2(m - mref);
             float rs = 0.f;

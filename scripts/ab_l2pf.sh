@@ -1,4 +1,5 @@
 #!/bin/bash
+# (the prefetch code was reverted after this A/B: profiles/r01_l2_prefetch_ab.md; the env vars are no-ops now)
 # A/B of the pre-wait L2 prefetch of statically assigned items (decode kernels),
 # alternating runs: GQA (70B shard, BATON_GQA_L2PF = static items per CTA) and
 # MHA (bench.py 7B, BATON_MHA_L2PF = "static items,prefetching CTAs").

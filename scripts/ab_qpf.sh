@@ -1,4 +1,5 @@
 #!/bin/bash
+# (the prefetch code was reverted after this A/B: profiles/r01_l2_prefetch_ab.md; the env vars are no-ops now)
 # A/B of the pre-wait L2 prefetch of q rows (BATON_QPF) and the e2e pass of bench.py
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
