@@ -28,6 +28,8 @@
 // that tile).  Prefill is the case of one slot, off = 0 and no mask.
 #include <cuda.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "tcgen05.cuh"
@@ -40,7 +42,6 @@ constexpr int PF_M = 128;         // queries per tile (UMMA M, TMEM lanes)
 constexpr int PF_N = 64;          // keys per tile (UMMA N of S, K of PV)
 constexpr int PF_D = 128;         // head_dim
 constexpr int PF_THREADS = 192;   // 4 softmax warps + producer warp + MMA warp
-constexpr float RESCALE_T = 8.f;  // lazy-rescale threshold (log2 units): P <= 256
 constexpr int Q_BYTES = PF_M * PF_D * 2;        // 32 KB: two 16 KB swizzle regions (dims 0-63, 64-127)
 constexpr int Q_REGION = Q_BYTES / 2;
 constexpr int KV_BYTES = PF_N * PF_D * 2;       // 16 KB: two 8 KB regions
@@ -62,6 +63,7 @@ using namespace tc;
 struct PfParams {
     int Hq, Hkv, len, n_mtiles;     // len = query rows per (slot, head): prompt length or W
     float scale_log2;
+    float rescale_t;                // lazy-rescale threshold (log2 units): P <= 2^rescale_t
     __nv_bfloat16 *out;
     // extend only (lens == nullptr for prefill)
     const int32_t *lens, *pad;      // device metadata AFTER the shaped mask update
@@ -236,12 +238,12 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
                     mx = fmaxf(mx, x);
                 }
             // Lazy rescale: P is taken relative to a reference max m that moves only
-            // when the row max exceeds it by more than RESCALE_T (log2 units), so P <=
-            // 2^RESCALE_T (exact in fp32 accumulation, same bf16 rounding of P) and the
+            // when the row max exceeds it by more than rescale_t (log2 units), so P <=
+            // 2^rescale_t (exact in fp32 accumulation, same bf16 rounding of P) and the
             // O rows in TMEM are rescaled only on those tiles, not whenever the max moves.
             // A row may see only masked keys so far (extend: holes, padding): keep exp2
             // finite -- ex2(-inf - 0) = 0.
-            const float m_new = (mx > m + RESCALE_T || m == -INFINITY) ? fmaxf(m, mx) : m;
+            const float m_new = (mx > m + p.rescale_t || m == -INFINITY) ? fmaxf(m, mx) : m;
             const float mref = (m_new == -INFINITY) ? 0.f : m_new;
             const float alpha = ex2(m - mref);
             float rs = 0.f;
@@ -345,6 +347,14 @@ namespace {
 cudaError_t launch_pf(const CUtensorMap &mq, const CUtensorMap &mk, const CUtensorMap &mv, const PfParams &p,
                       int slots, cudaStream_t s) {
     const size_t smem = sizeof(PfSmem) + 1024;
+    static float rescale_t = -1.f;   // BATON_PF_RESCALE_T (0 = rescale whenever the max moves)
+    if (rescale_t < 0.f) {
+        const char *e = getenv("BATON_PF_RESCALE_T");
+        rescale_t = e ? (float)atof(e) : 8.f;
+        if (rescale_t < 0.f) rescale_t = 0.f;
+    }
+    PfParams pp = p;
+    pp.rescale_t = rescale_t;
     static bool attr[2] = {false, false};
     const bool ext = p.lens != nullptr;
     if (!attr[ext]) {
@@ -354,9 +364,9 @@ cudaError_t launch_pf(const CUtensorMap &mq, const CUtensorMap &mk, const CUtens
         attr[ext] = true;
     }
     if (ext)
-        prefill_attention_kernel<true><<<p.n_mtiles * p.Hq * slots, PF_THREADS, smem, s>>>(mq, mk, mv, p);
+        prefill_attention_kernel<true><<<p.n_mtiles * p.Hq * slots, PF_THREADS, smem, s>>>(mq, mk, mv, pp);
     else
-        prefill_attention_kernel<false><<<p.n_mtiles * p.Hq * slots, PF_THREADS, smem, s>>>(mq, mk, mv, p);
+        prefill_attention_kernel<false><<<p.n_mtiles * p.Hq * slots, PF_THREADS, smem, s>>>(mq, mk, mv, pp);
     return cudaGetLastError();
 }
 }  // namespace

@@ -3,7 +3,7 @@
     python scripts/bench_prefill.py [--iters N]
 
 Prints one JSON line per shape: causal FLOPs (4*H*D*sum_i (i+1), the algorithmic
-work of the masked product), CUDA-event time per launch and TFLOP/s as a fraction
+work of the masked product), CUDA-event time per launch (graph of --iters launches) and TFLOP/s as a fraction
 of the measured dense bf16 peak (MEASURED_PEAKS.json bf16_tflops, burst)."""
 import argparse
 import json
@@ -20,6 +20,7 @@ from paper_2410_18701_b200.baton import baton_prefill_attention  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--only", default=None, help="e.g. 70b:3400 (one shape)")
     args = ap.parse_args()
     peak = 1657.7
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -27,6 +28,8 @@ def main():
         peak = json.load(open(p))["bf16_tflops"]
     shapes = [("7b", 32, 32, 512), ("7b", 32, 32, 1024), ("7b", 32, 32, 1800),
               ("13b", 40, 40, 1024), ("70b", 64, 8, 3400)]
+    if args.only:
+        shapes = [s for s in shapes if f"{s[0]}:{s[3]}" == args.only]
     for name, Hq, Hkv, n in shapes:
         D = 128
         q = torch.randn((Hq, n, D), device="cuda").to(torch.bfloat16)
@@ -36,10 +39,20 @@ def main():
         for _ in range(3):
             baton_prefill_attention(q, k, v, o, n, Hq, Hkv, D)
         torch.cuda.synchronize()
+        # graph-replayed launches: the per-call host work (three tensor-map encodes)
+        # would otherwise starve the GPU on the short prompts
+        g = torch.cuda.CUDAGraph()
+        st = torch.cuda.Stream()
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st), torch.cuda.graph(g, stream=st):
+            for _ in range(args.iters):
+                baton_prefill_attention(q, k, v, o, n, Hq, Hkv, D)
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for _ in range(args.iters):
-            baton_prefill_attention(q, k, v, o, n, Hq, Hkv, D)
+        g.replay()
         e1.record()
         torch.cuda.synchronize()
         us = e0.elapsed_time(e1) * 1e3 / args.iters
