@@ -9,14 +9,18 @@
 // columns each) so one CTA's softmax overlaps the other's MMAs.  Warp roles
 // (DESIGN.md §6.3):
 //   warp 4   TMA producer: the Q tile once (128 x 128, SWIZZLE_128B), then per
-//            64-key tile K (single buffer, refilled as soon as S(j) is done) and
-//            V (2-stage ring) -- cp.async.bulk.tensor with mbarrier tx-counts
-//   warp 5   MMA issuer (one elected thread): S = Q K^T (M=128, N=64, K=16 x8)
-//            into TMEM, then O += P V (M=128, N=128, K=16 x4) into TMEM, each
-//            completion published with tcgen05.commit -> mbarrier
+//            64-key tile K and V, each through a 2-stage ring -- cp.async.bulk.tensor
+//            with mbarrier tx-counts
+//   warp 5   MMA issuer (one elected thread): S(j) = Q K(j)^T (M=128, N=64, K=16 x8)
+//            into TMEM buffer j&1, then O += P(j) V(j) (M=128, N=128, K=16 x4) with
+//            P(j) read from TMEM (the "TS" form: P overwrites the first 32 columns of
+//            its own S buffer, bf16 pairs), then S(j+2) into the buffer P(j) just
+//            left -- the tensor pipe runs those in issue order, so S(j+2) cannot
+//            overwrite P(j) before the P.V MMA has read it.  The softmax therefore
+//            always finds the next scores ready.
 //   warps 0-3 softmax: thread = query row; tcgen05.ld of its S row, causal mask,
-//            online max/sum (exp2), P -> bf16 into the K-major SW128 smem layout
-//            the next MMA reads, O rescale in TMEM (tcgen05.ld/st), epilogue.
+//            online max/sum (exp2, lazy rescale), P -> bf16 -> tcgen05.st into TMEM,
+//            O rescale in TMEM (tcgen05.ld/st) when the reference max moves, epilogue.
 //
 // The same kernel runs the EXTEND attention of a vector-shaping iteration
 // (NEXT-1, launch_extend_attention): a CTA per (slot, q head, query
@@ -46,15 +50,13 @@ constexpr int Q_BYTES = PF_M * PF_D * 2;        // 32 KB: two 16 KB swizzle regi
 constexpr int Q_REGION = Q_BYTES / 2;
 constexpr int KV_BYTES = PF_N * PF_D * 2;       // 16 KB: two 8 KB regions
 constexpr int KV_REGION = KV_BYTES / 2;
-constexpr int P_BYTES = PF_M * PF_N * 2;        // 16 KB: 128 rows x 64 keys (one 128-B atom per row)
 
 struct __align__(1024) PfSmem {
     uint8_t q[Q_BYTES];
-    uint8_t k[KV_BYTES];
+    uint8_t k[2][KV_BYTES];
     uint8_t v[2][KV_BYTES];
-    uint8_t p[P_BYTES];
     uint8_t mk[2][PF_N + 16];       // extend: mask bytes of the V stage's key tile
-    uint64_t bar_q, k_full, k_empty, v_full[2], v_empty[2], s_full, s_free, p_full, o_done;
+    uint64_t bar_q, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], p_full[2], pv_done[2];
     uint32_t tmem_base;
 };
 
@@ -105,19 +107,18 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
 
     if (threadIdx.x == 0) {
         mbar_init(&sm.bar_q, 1);
-        mbar_init(&sm.k_full, 1);
-        mbar_init(&sm.k_empty, 1);
         for (int s = 0; s < 2; ++s) {
+            mbar_init(&sm.k_full[s], 1);
+            mbar_init(&sm.k_empty[s], 1);
             mbar_init(&sm.v_full[s], 1);
             mbar_init(&sm.v_empty[s], 1);
+            mbar_init(&sm.s_full[s], 1);
+            mbar_init(&sm.p_full[s], 128);
+            mbar_init(&sm.pv_done[s], 1);
         }
-        mbar_init(&sm.s_full, 1);
-        mbar_init(&sm.s_free, 128);
-        mbar_init(&sm.p_full, 128);
-        mbar_init(&sm.o_done, 1);
         fence_mbar_init();
     }
-    if (warp == 0) {   // TMEM: S in columns [0,64), O in [128,256)
+    if (warp == 0) {   // TMEM: S/P buffers in columns [0,64) and [64,128), O in [128,256)
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
                          smem_u32(&sm.tmem_base)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -143,11 +144,11 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
                 tma_load_3d(sm.q + Q_REGION, &tm_q, 64, q0, qrow, &sm.bar_q);
             }
             for (int j = 0; j < n_kt; ++j) {
-                if (j > 0) mbar_wait(&sm.k_empty, (j - 1) & 1);          // S(j-1) done with K
-                mbar_arrive_expect_tx(&sm.k_full, KV_BYTES);
-                tma_load_3d(sm.k, &tm_k, 0, j * PF_N, krow, &sm.k_full);
-                tma_load_3d(sm.k + KV_REGION, &tm_k, 64, j * PF_N, krow, &sm.k_full);
                 const int s = j & 1;
+                if (j >= 2) mbar_wait(&sm.k_empty[s], ((j >> 1) + 1) & 1);   // S(j-2) done with K
+                mbar_arrive_expect_tx(&sm.k_full[s], KV_BYTES);
+                tma_load_3d(sm.k[s], &tm_k, 0, j * PF_N, krow, &sm.k_full[s]);
+                tma_load_3d(sm.k[s] + KV_REGION, &tm_k, 64, j * PF_N, krow, &sm.k_full[s]);
                 if (j >= 2) mbar_wait(&sm.v_empty[s], ((j >> 1) + 1) & 1);   // PV(j-2) done
                 uint32_t mbytes = 0;
                 size_t a0 = 0;
@@ -169,40 +170,41 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
         // ======================= MMA issuer =======================
         if (lane == 0) {
             constexpr uint32_t idS = idesc_bf16(PF_M, PF_N, 0);   // B = K tile, K-major
-            constexpr uint32_t idO = idesc_bf16(PF_M, PF_D, 1);   // B = V tile, MN-major
-            const uint32_t qa = smem_u32(sm.q), pa = smem_u32(sm.p), ka = smem_u32(sm.k);
+            constexpr uint32_t idO = idesc_bf16(PF_M, PF_D, 1);   // A = P (TMEM, K-major), B = V tile, MN-major
+            const uint32_t qa = smem_u32(sm.q);
             mbar_wait(&sm.bar_q, 0);
-            // S(j+1) = Q K(j+1)^T is issued as soon as the softmax warps hold S(j) in
-            // registers, BEFORE waiting for P(j): the tensor pipe computes the next
-            // scores while the softmax of this tile runs, and PV(j) runs under the
-            // softmax of tile j+1.
+            // order: S(0), S(1), PV(0), S(2), PV(1), S(3), ...  S(j+2) goes into the TMEM
+            // buffer that P(j) occupies; it is issued after PV(j), and the tensor pipe
+            // executes in issue order.
             auto issue_s = [&](int j) {
-                mbar_wait(&sm.k_full, j & 1);
-                if (j > 0) mbar_wait(&sm.s_free, (j - 1) & 1);   // softmax has read S(j-1)
+                const int b2 = j & 1;
+                mbar_wait(&sm.k_full[b2], (j >> 1) & 1);
                 tc_fence_after();
+                const uint32_t ka = smem_u32(sm.k[b2]);
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {   // K = head_dim in steps of 16 (32 B)
-                    umma_f16(tS, smem_desc(qa + (k >> 2) * Q_REGION + (k & 3) * 32, 16, 1024),
+                    umma_f16(tS + 64 * b2, smem_desc(qa + (k >> 2) * Q_REGION + (k & 3) * 32, 16, 1024),
                              smem_desc(ka + (k >> 2) * KV_REGION + (k & 3) * 32, 16, 1024), idS, k > 0);
                 }
-                umma_commit(&sm.s_full);
-                umma_commit(&sm.k_empty);
+                umma_commit(&sm.s_full[b2]);
+                umma_commit(&sm.k_empty[b2]);
             };
             issue_s(0);
+            if (n_kt > 1) issue_s(1);
             for (int j = 0; j < n_kt; ++j) {
                 const int s = j & 1;
-                if (j + 1 < n_kt) issue_s(j + 1);
-                mbar_wait(&sm.p_full, j & 1);                   // P(j) written, O rescaled
+                mbar_wait(&sm.p_full[s], (j >> 1) & 1);           // P(j) in TMEM, O rescaled
                 mbar_wait(&sm.v_full[s], (j >> 1) & 1);
                 tc_fence_after();
                 const uint32_t va = smem_u32(sm.v[s]);
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {   // K = 64 keys in steps of 16
-                    umma_f16(tO, smem_desc(pa + k * 32, 16, 1024),
-                             smem_desc(va + k * 2048, KV_REGION, 1024), idO, (j > 0 || k > 0));
+                for (int k = 0; k < 4; ++k) {   // K = 64 keys in steps of 16 (8 TMEM columns of bf16 pairs)
+                    umma_f16_ts(tO, tS + 64 * s + 8 * k, smem_desc(va + k * 2048, KV_REGION, 1024), idO,
+                                (j > 0 || k > 0));
                 }
-                umma_commit(&sm.o_done);
+                umma_commit(&sm.pv_done[s]);
                 umma_commit(&sm.v_empty[s]);
+                if (j + 2 < n_kt) issue_s(j + 2);
             }
         }
     } else {
@@ -214,18 +216,18 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
         uint32_t pk[32];                              // P row (64 keys) packed bf16x2
         const int mrow = ext ? (int)(((size_t)b * p.max_ctx + kpad) & 15) : 0;   // mask byte offset
         for (int j = 0; j < n_kt; ++j) {
-            mbar_wait(&sm.s_full, j & 1);
+            const int sb = j & 1;
+            const uint32_t tSj = tS + 64 * sb + lane_off;
+            mbar_wait(&sm.s_full[sb], (j >> 1) & 1);
             tc_fence_after();
             const int kbase = j * PF_N;
             const bool diag = kbase + PF_N > off + q0;   // tile touches the causal diagonal
             const uint8_t *mk = sm.mk[j & 1] + mrow;
             if (ext) mbar_wait(&sm.v_full[j & 1], (j >> 1) & 1);   // this tile's mask bytes
             uint32_t r[2][32];
-            tmem_ld32(tS + lane_off, r[0]);
-            tmem_ld32(tS + lane_off + 32, r[1]);
+            tmem_ld32(tSj, r[0]);
+            tmem_ld32(tSj + 32, r[1]);
             tmem_wait_ld();
-            tc_fence_before();
-            mbar_arrive(&sm.s_free);                  // S(j) is in registers: next S may start
             float mx = -INFINITY;
 #pragma unroll
             for (int c = 0; c < 2; ++c)
@@ -260,11 +262,13 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
                 }
             l = l * alpha + rs;
             m = m_new;
-            if (j > 0) {
-                mbar_wait(&sm.o_done, (j - 1) & 1);   // PV(j-1) done: O stable, P buffer free
+            // warp-uniform: tcgen05.ld/st are .sync.aligned (all 32 lanes converged)
+            if (j > 0 && __any_sync(FULL_MASK, alpha != 1.f)) {
+                // O is stable once PV(j-1) is done (PV(j-3) on that barrier completed
+                // before S(j-1), which this warp group already read: at most one phase behind)
+                mbar_wait(&sm.pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
                 tc_fence_after();
-                // warp-uniform: tcgen05.ld/st are .sync.aligned (all 32 lanes converged)
-                if (__any_sync(FULL_MASK, alpha != 1.f)) {
+                {
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
                         uint32_t o[32];
@@ -287,20 +291,17 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
                     *reinterpret_cast<uint4 *>(sm.v[j & 1] + (ch >> 3) * KV_REGION + rr * 128 + (ch & 7) * 16) =
                         make_uint4(0, 0, 0, 0);
                 }
+                fence_async_smem();   // generic-proxy writes -> the tensor core's reads
             }
-            // P row -> smem, K-major SWIZZLE_128B: 64 keys = one 128-B row, 16-B chunk c
-            // of row r at chunk position c ^ (r & 7)
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                uint8_t *dst = sm.p + row * 128 + ((c ^ (row & 7)) << 4);
-                *reinterpret_cast<uint4 *>(dst) = make_uint4(pk[c * 4], pk[c * 4 + 1], pk[c * 4 + 2], pk[c * 4 + 3]);
-            }
-            fence_async_smem();
+            // P row -> TMEM over the first 32 columns of this S buffer (bf16 pairs,
+            // key 2c in the low half of column c): the A operand of PV(j)
+            tmem_st32(tSj, pk);
+            tmem_wait_st();
             tc_fence_before();
-            mbar_arrive(&sm.p_full);
+            mbar_arrive(&sm.p_full[sb]);
         }
-        // epilogue: O / l -> bf16
-        mbar_wait(&sm.o_done, (n_kt - 1) & 1);
+        // epilogue: O / l -> bf16 once the last PV is done (the tensor pipe completes in order)
+        mbar_wait(&sm.pv_done[(n_kt - 1) & 1], ((n_kt - 1) >> 1) & 1);
         tc_fence_after();
         const float inv = l > 0.f ? 1.f / l : 0.f;
         __nv_bfloat16 *orow = EXT ? p.out + (((size_t)b * p.len + qi) * p.Hq + h) * PF_D
