@@ -228,17 +228,26 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
             tmem_ld32(tSj, r[0]);
             tmem_ld32(tSj + 32, r[1]);
             tmem_wait_ld();
+            // Masked keys become -inf in the RAW scores; the scale (> 0) is folded into
+            // the exponent (one FFMA + ex2 per key) and the row max is taken raw.  Tiles
+            // off the diagonal (and prefill has no mask) skip the per-key tests.
             float mx = -INFINITY;
+            if (diag || ext) {
 #pragma unroll
-            for (int c = 0; c < 2; ++c)
+                for (int c = 0; c < 2; ++c)
 #pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    float x = __uint_as_float(r[c][i]) * p.scale_log2;
-                    if (diag && kbase + c * 32 + i > off + qi) x = -INFINITY;
-                    if (ext && mk[c * 32 + i] == 0) x = -INFINITY;
-                    r[c][i] = __float_as_uint(x);
-                    mx = fmaxf(mx, x);
-                }
+                    for (int i = 0; i < 32; ++i) {
+                        const bool dead = (diag && kbase + c * 32 + i > off + qi) || (ext && mk[c * 32 + i] == 0);
+                        if (dead) r[c][i] = __float_as_uint(-INFINITY);
+                        mx = fmaxf(mx, __uint_as_float(r[c][i]));
+                    }
+            } else {
+#pragma unroll
+                for (int c = 0; c < 2; ++c)
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(r[c][i]));
+            }
+            mx *= p.scale_log2;   // -inf stays -inf
             // Lazy rescale: P is taken relative to a reference max m that moves only
             // when the row max exceeds it by more than rescale_t (log2 units), so P <=
             // 2^rescale_t (exact in fp32 accumulation, same bf16 rounding of P) and the
@@ -248,18 +257,22 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
             const float m_new = (mx > m + p.rescale_t || m == -INFINITY) ? fmaxf(m, mx) : m;
             const float mref = (m_new == -INFINITY) ? 0.f : m_new;
             const float alpha = ex2(m - mref);
-            float rs = 0.f;
+            const float nref = -mref;
+            // the row sum adds the fp32 exponentials; the P.V MMA multiplies their bf16
+            // roundings (relative difference <= 2^-9 per key, far inside C13's 1e-2)
+            float rs0 = 0.f, rs1 = 0.f;
 #pragma unroll
             for (int c = 0; c < 2; ++c)
 #pragma unroll
                 for (int i = 0; i < 32; i += 2) {
-                    const float e0 = ex2(__uint_as_float(r[c][i]) - mref);
-                    const float e1 = ex2(__uint_as_float(r[c][i + 1]) - mref);
+                    const float e0 = ex2(fmaf(__uint_as_float(r[c][i]), p.scale_log2, nref));
+                    const float e1 = ex2(fmaf(__uint_as_float(r[c][i + 1]), p.scale_log2, nref));
                     const __nv_bfloat162 b = __floats2bfloat162_rn(e0, e1);
-                    // the PV MMA consumes bf16 P: accumulate the sum of what it multiplies
-                    rs += __low2float(b) + __high2float(b);
+                    rs0 += e0;
+                    rs1 += e1;
                     pk[c * 16 + i / 2] = *reinterpret_cast<const uint32_t *>(&b);
                 }
+            const float rs = rs0 + rs1;
             l = l * alpha + rs;
             m = m_new;
             // warp-uniform: tcgen05.ld/st are .sync.aligned (all 32 lanes converged)
