@@ -207,6 +207,23 @@ int  baton_compact(baton_state *st, int n_active, int32_t *old_to_new, void *str
 int  baton_prefill_attention(const void *q, const void *k, const void *v, void *out, int len,
                              const baton_shape *shape, float scale, void *stream);
 
+/* a8, batched (NEXT-2: the prefill side of P&D at scale): the same causal
+ * attention for n prompts in ONE launch, e.g. every query queued for insertion in an
+ * iteration ("all original queries awaiting processing are initially
+ * prefilled"; P:L215 asynchronous P&D).  Prompt i is its own causal problem; no
+ * attention crosses prompts.
+ *   Q, O : device bf16 [q_heads][T][head_dim];  K, V : [kv_heads][T][head_dim], the
+ *          prompts packed along the token axis: prompt i occupies rows
+ *          [cu_lens[i], cu_lens[i+1]), T = cu_lens[n].
+ *   cu_lens : HOST int32 [n+1], cu_lens[0] = 0, strictly increasing (every prompt
+ *          has >= 1 token); read during the call only.
+ *   1 <= n <= 64 and sum_i ceil(len_i / 128) <= 1024.  Same result, row for row and
+ *   bit for bit, as n separate baton_prefill_attention calls.
+ * Errors: BATON_E_INVALID. */
+int  baton_prefill_attention_varlen(const void *q, const void *k, const void *v, void *out,
+                                    const int32_t *cu_lens, int n, const baton_shape *shape,
+                                    float scale, void *stream);
+
 /* ---------------------------------------------------------------- NEXT-1
  * The vector-SHAPING iteration: Baton WITHOUT P&D decoupling (the
  * "Ours" column of the paper's Table 2 ablation).  Raw queries join the

@@ -72,6 +72,8 @@ _SIGS = {
     "baton_compact": (_I, [_P, _I, _I32P, _P]),
     "baton_prefill_attention": (_I, [_P, _P, _P, _P, _I, ctypes.POINTER(baton_shape),
                                      ctypes.c_float, _P]),
+    "baton_prefill_attention_varlen": (_I, [_P, _P, _P, _P, _I32P, _I, ctypes.POINTER(baton_shape),
+                                            ctypes.c_float, _P]),
     "baton_shape_step": (_I, [_P, _I, _I, _I32P, _I32P, _P, _P, _P, _P, _P]),
     "baton_error_string": (ctypes.c_char_p, [_I]),
     "baton_cuda_error": (_I, []),

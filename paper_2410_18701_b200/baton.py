@@ -64,6 +64,22 @@ def baton_prefill_attention(q, k, v, out, length, q_heads, kv_heads, head_dim, s
     return out
 
 
+def baton_prefill_attention_varlen(q, k, v, out, lens, q_heads, kv_heads, head_dim, scale=None,
+                                   stream=None):
+    """a8 batched (include/baton.h): n prompts packed along the token axis in one launch.
+    q, out: [q_heads][T][head_dim]; k, v: [kv_heads][T][head_dim]; lens: the n prompt
+    lengths (prompt i starts at sum(lens[:i]))."""
+    cu = np.zeros(len(lens) + 1, np.int32)
+    cu[1:] = np.cumsum(np.asarray(lens, np.int64))
+    shape = make_shape(1, 1, q_heads, kv_heads, head_dim, 16)
+    check(lib.baton_prefill_attention_varlen(_ptr(q), _ptr(k), _ptr(v), _ptr(out),
+                                             cu.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                             len(lens), ctypes.byref(shape),
+                                             ctypes.c_float(scale or 1.0 / math.sqrt(head_dim)),
+                                             _stream(stream)), "baton_prefill_attention_varlen")
+    return out
+
+
 def baton_keygen_tokens(out, qids, pos, layers, n_slots, heads, head_dim, kind, layer0, seed,
                         scale_exp, stream=None):
     check(lib.baton_keygen_tokens(_ptr(out), _ptr(qids), _ptr(pos), layers, n_slots, heads,

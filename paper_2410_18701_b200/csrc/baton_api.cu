@@ -550,6 +550,29 @@ int baton_prefill_attention(const void *q, const void *k, const void *v, void *o
                                                 shape->head_dim, scale, as_stream(stream)));
 }
 
+int baton_prefill_attention_varlen(const void *q, const void *k, const void *v, void *out,
+                                   const int32_t *cu_lens, int n, const baton_shape *shape, float scale,
+                                   void *stream) {
+    if (!q || !k || !v || !out || !cu_lens || !shape || n < 1 || n > prefill_varlen_max_prompts() ||
+        !(scale > 0.f))
+        return BATON_E_INVALID;
+    if (shape->q_heads < 1 || shape->kv_heads < 1 || shape->q_heads % shape->kv_heads ||
+        !prefill_supported(shape->head_dim))
+        return BATON_E_INVALID;
+    if (cu_lens[0] != 0) return BATON_E_INVALID;
+    int tiles = 0;
+    for (int i = 0; i < n; ++i) {
+        const int len = cu_lens[i + 1] - cu_lens[i];
+        if (len < 1) return BATON_E_INVALID;
+        tiles += (len + 127) / 128;
+    }
+    if (tiles > 1024) return BATON_E_INVALID;
+    for (const void *ptr : {q, k, v, (const void *)out})
+        if (reinterpret_cast<uintptr_t>(ptr) & 15) return BATON_E_INVALID;
+    return cuda_status(launch_prefill_attention_varlen(q, k, v, out, cu_lens, n, shape->q_heads, shape->kv_heads,
+                                                       shape->head_dim, scale, as_stream(stream)));
+}
+
 // ---------------------------------------------------------------- misc
 const char *baton_error_string(int code) {
     switch (code) {

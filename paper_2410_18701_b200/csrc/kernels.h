@@ -88,6 +88,12 @@ cudaError_t launch_shape_append(void *k_cache, void *v_cache, const void *k_new,
 
 // ------------------------------------------------------------ a8 prefill attention (tcgen05)
 bool prefill_supported(int head_dim);
+int prefill_varlen_max_prompts();
+// n prompts packed along the token axis: Q/O [q_heads][T][D], K/V [kv_heads][T][D],
+// prompt i at rows [cu_lens[i], cu_lens[i+1]) (host array), T = cu_lens[n]
+cudaError_t launch_prefill_attention_varlen(const void *q, const void *k, const void *v, void *out,
+                                            const int32_t *cu_lens, int n, int q_heads, int kv_heads,
+                                            int head_dim, float scale, cudaStream_t s);
 cudaError_t launch_prefill_attention(const void *q, const void *k, const void *v, void *out, int len,
                                      int q_heads, int kv_heads, int head_dim, float scale,
                                      cudaStream_t s);

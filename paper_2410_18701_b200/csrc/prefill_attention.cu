@@ -32,6 +32,7 @@
 // that tile).  Prefill is the case of one slot, off = 0 and no mask.
 #include <cuda.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -46,6 +47,8 @@ constexpr int PF_M = 128;         // queries per tile (UMMA M, TMEM lanes)
 constexpr int PF_N = 64;          // keys per tile (UMMA N of S, K of PV)
 constexpr int PF_D = 128;         // head_dim
 constexpr int PF_THREADS = 192;   // 4 softmax warps + producer warp + MMA warp
+constexpr int VL_MAXP = 64;       // prompts per varlen prefill launch
+constexpr int VL_MAXT = 1024;     // (prompt, query tile) entries per launch
 constexpr int Q_BYTES = PF_M * PF_D * 2;        // 32 KB: two 16 KB swizzle regions (dims 0-63, 64-127)
 constexpr int Q_REGION = Q_BYTES / 2;
 constexpr int KV_BYTES = PF_N * PF_D * 2;       // 16 KB: two 8 KB regions
@@ -84,7 +87,7 @@ BATON_DEV float2 fadd2(float2 a, float2 b) {
 }
 
 struct PfParams {
-    int Hq, Hkv, len, n_mtiles;     // len = query rows per (slot, head): prompt length or W
+    int Hq, Hkv, len, n_mtiles;     // extend: len = W query rows per (slot, head)
     float scale_log2;
     float rescale_t;                // lazy-rescale threshold (log2 units): P <= 2^rescale_t
     __nv_bfloat16 *out;
@@ -92,6 +95,12 @@ struct PfParams {
     const int32_t *lens, *pad;      // device metadata AFTER the shaped mask update
     const uint8_t *mask;            // [slots][max_ctx]
     int max_ctx;
+    // prefill only: prompts packed along the token axis (varlen), prompt i at rows
+    // [vl_start[i], vl_start[i] + vl_len[i]); CTA c takes query tile vl_tile[c / Hq]
+    // (prompt << 16 | m-tile, heaviest first) of q head c % Hq
+    int32_t total;                  // packed token rows (the maps' second extent)
+    int32_t vl_start[VL_MAXP], vl_len[VL_MAXP];
+    uint32_t vl_tile[VL_MAXT];
 };
 
 template <bool EXT>
@@ -101,13 +110,23 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
     extern __shared__ uint8_t smem_raw[];
     PfSmem &sm = *reinterpret_cast<PfSmem *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // heavy tiles (near the diagonal end) first
-    const int mt = p.n_mtiles - 1 - (int)(blockIdx.x % p.n_mtiles);
-    const int h = (blockIdx.x / p.n_mtiles) % p.Hq;
-    const int b = blockIdx.x / (p.n_mtiles * p.Hq);           // slot (extend), 0 (prefill)
+    constexpr bool ext = EXT;
+    int mt, h, b, s0 = 0, len = p.len;
+    if (EXT) {   // heavy tiles (near the diagonal end) first within a (slot, head)
+        mt = p.n_mtiles - 1 - (int)(blockIdx.x % p.n_mtiles);
+        h = (blockIdx.x / p.n_mtiles) % p.Hq;
+        b = blockIdx.x / (p.n_mtiles * p.Hq);                 // slot
+    } else {     // prefill: the host lists (prompt, query tile) heaviest first
+        const uint32_t e = p.vl_tile[blockIdx.x / p.Hq];
+        const int pi = (int)(e >> 16);
+        mt = (int)(e & 0xffff);
+        h = blockIdx.x % p.Hq;
+        b = 0;
+        s0 = p.vl_start[pi];
+        len = p.vl_len[pi];
+    }
     const int g = h * p.Hkv / p.Hq;
     const int q0 = mt * PF_M;
-    constexpr bool ext = EXT;
     int off = 0, kpad = 0;
     if (ext) {
         const int lb = p.lens[b];
@@ -124,7 +143,10 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
         kpad = p.pad[b];
     }
     const int qrow = b * p.Hq + h, krow = b * p.Hkv + g;        // outer coordinate of the maps
-    const int n_kt = (off + min(q0 + PF_M, p.len) + PF_N - 1) / PF_N;   // key tiles up to the diagonal
+    // key tiles up to the diagonal.  Varlen prefill: a tile may run past this prompt
+    // into the next one's rows; those keys are past every query row of the tile
+    // (causally masked, P = 0 exactly) and their V rows are finite
+    const int n_kt = (off + min(q0 + PF_M, len) + PF_N - 1) / PF_N;
 
     if (threadIdx.x == 0) {
         mbar_init(&sm.bar_q, 1);
@@ -161,15 +183,15 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
                 tma_load_4d(sm.q, &tm_q, 0, h, q0, b, &sm.bar_q);
                 tma_load_4d(sm.q + Q_REGION, &tm_q, 64, h, q0, b, &sm.bar_q);
             } else {
-                tma_load_3d(sm.q, &tm_q, 0, q0, qrow, &sm.bar_q);
-                tma_load_3d(sm.q + Q_REGION, &tm_q, 64, q0, qrow, &sm.bar_q);
+                tma_load_3d(sm.q, &tm_q, 0, s0 + q0, qrow, &sm.bar_q);
+                tma_load_3d(sm.q + Q_REGION, &tm_q, 64, s0 + q0, qrow, &sm.bar_q);
             }
             for (int j = 0; j < n_kt; ++j) {
                 const int s = j & 1;
                 if (j >= 2) mbar_wait(&sm.k_empty[s], ((j >> 1) + 1) & 1);   // S(j-2) done with K
                 mbar_arrive_expect_tx(&sm.k_full[s], KV_BYTES);
-                tma_load_3d(sm.k[s], &tm_k, 0, j * PF_N, krow, &sm.k_full[s]);
-                tma_load_3d(sm.k[s] + KV_REGION, &tm_k, 64, j * PF_N, krow, &sm.k_full[s]);
+                tma_load_3d(sm.k[s], &tm_k, 0, s0 + j * PF_N, krow, &sm.k_full[s]);
+                tma_load_3d(sm.k[s] + KV_REGION, &tm_k, 64, s0 + j * PF_N, krow, &sm.k_full[s]);
                 if (j >= 2) mbar_wait(&sm.v_empty[s], ((j >> 1) + 1) & 1);   // PV(j-2) done
                 uint32_t mbytes = 0;
                 size_t a0 = 0;
@@ -182,8 +204,8 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
                     mbytes = (uint32_t)need;
                 }
                 mbar_arrive_expect_tx(&sm.v_full[s], KV_BYTES + mbytes);
-                tma_load_3d(sm.v[s], &tm_v, 0, j * PF_N, krow, &sm.v_full[s]);
-                tma_load_3d(sm.v[s] + KV_REGION, &tm_v, 64, j * PF_N, krow, &sm.v_full[s]);
+                tma_load_3d(sm.v[s], &tm_v, 0, s0 + j * PF_N, krow, &sm.v_full[s]);
+                tma_load_3d(sm.v[s] + KV_REGION, &tm_v, 64, s0 + j * PF_N, krow, &sm.v_full[s]);
                 if (mbytes) bulk_g2s(sm.mk[s], p.mask + a0, mbytes, &sm.v_full[s]);
             }
         }
@@ -340,13 +362,13 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
         tc_fence_after();
         const float inv = l > 0.f ? 1.f / l : 0.f;
         __nv_bfloat16 *orow = EXT ? p.out + (((size_t)b * p.len + qi) * p.Hq + h) * PF_D
-                                  : p.out + ((size_t)qrow * p.len + qi) * PF_D;
+                                  : p.out + ((size_t)qrow * p.total + s0 + qi) * PF_D;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             uint32_t o[32];
             tmem_ld32(tO + lane_off + c * 32, o);
             tmem_wait_ld();
-            if (qi < p.len) {
+            if (qi < len) {
                 uint32_t w[16];
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
@@ -401,29 +423,58 @@ cudaError_t launch_pf(const CUtensorMap &mq, const CUtensorMap &mk, const CUtens
     }
     if (ext)
         prefill_attention_kernel<true><<<p.n_mtiles * p.Hq * slots, PF_THREADS, smem, s>>>(mq, mk, mv, pp);
-    else
-        prefill_attention_kernel<false><<<p.n_mtiles * p.Hq * slots, PF_THREADS, smem, s>>>(mq, mk, mv, pp);
+    else   // prefill: n_mtiles = number of (prompt, query tile) entries
+        prefill_attention_kernel<false><<<p.n_mtiles * p.Hq, PF_THREADS, smem, s>>>(mq, mk, mv, pp);
     return cudaGetLastError();
 }
 }  // namespace
 
-cudaError_t launch_prefill_attention(const void *q, const void *k, const void *v, void *out, int len,
-                                     int q_heads, int kv_heads, int head_dim, float scale,
-                                     cudaStream_t s) {
-    if (head_dim != PF_D || len < 1) return cudaErrorInvalidValue;
-    CUtensorMap mq, mk, mv;
-    if (!make_map(&mq, q, q_heads, len, PF_M) || !make_map(&mk, k, kv_heads, len, PF_N) ||
-        !make_map(&mv, v, kv_heads, len, PF_N))
-        return cudaErrorInvalidValue;
+int prefill_varlen_max_prompts() { return VL_MAXP; }
+
+cudaError_t launch_prefill_attention_varlen(const void *q, const void *k, const void *v, void *out,
+                                            const int32_t *cu_lens, int n, int q_heads, int kv_heads,
+                                            int head_dim, float scale, cudaStream_t s) {
+    if (head_dim != PF_D || n < 1 || n > VL_MAXP || cu_lens[0] != 0) return cudaErrorInvalidValue;
     PfParams p{};
+    // (prompt, query tile) entries, heaviest first (key tiles up to the diagonal),
+    // ties by prompt then tile: a longest-processing-time order over all prompts
+    int ne = 0;
+    for (int i = 0; i < n; ++i) {
+        const int len = cu_lens[i + 1] - cu_lens[i];
+        if (len < 1) return cudaErrorInvalidValue;
+        p.vl_start[i] = cu_lens[i];
+        p.vl_len[i] = len;
+        const int nm = (len + PF_M - 1) / PF_M;
+        if (ne + nm > VL_MAXT || nm > 0xffff) return cudaErrorInvalidValue;
+        for (int mt = 0; mt < nm; ++mt) p.vl_tile[ne++] = ((uint32_t)i << 16) | (uint32_t)mt;
+    }
+    auto cost = [&](uint32_t e) {
+        const int len = p.vl_len[e >> 16], q0 = (int)(e & 0xffff) * PF_M;
+        return (std::min(q0 + PF_M, len) + PF_N - 1) / PF_N;
+    };
+    std::stable_sort(p.vl_tile, p.vl_tile + ne, [&](uint32_t a, uint32_t b) { return cost(a) > cost(b); });
+    const int total = cu_lens[n];
+    CUtensorMap mq, mk, mv;
+    if (!make_map(&mq, q, q_heads, total, PF_M) || !make_map(&mk, k, kv_heads, total, PF_N) ||
+        !make_map(&mv, v, kv_heads, total, PF_N))
+        return cudaErrorInvalidValue;
     p.Hq = q_heads;
     p.Hkv = kv_heads;
-    p.len = len;
-    p.n_mtiles = (len + PF_M - 1) / PF_M;
+    p.len = 0;
+    p.total = total;
+    p.n_mtiles = ne;
     p.scale_log2 = scale * 1.4426950408889634f;
     p.out = static_cast<__nv_bfloat16 *>(out);
     p.lens = nullptr;
     return launch_pf(mq, mk, mv, p, 1, s);
+}
+
+cudaError_t launch_prefill_attention(const void *q, const void *k, const void *v, void *out, int len,
+                                     int q_heads, int kv_heads, int head_dim, float scale,
+                                     cudaStream_t s) {
+    if (len < 1) return cudaErrorInvalidValue;
+    const int32_t cu[2] = {0, len};
+    return launch_prefill_attention_varlen(q, k, v, out, cu, 1, q_heads, kv_heads, head_dim, scale, s);
 }
 
 cudaError_t launch_extend_attention(const void *q, const void *k_layer, const void *v_layer, void *out,

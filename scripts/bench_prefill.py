@@ -14,7 +14,7 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-from paper_2410_18701_b200.baton import baton_prefill_attention  # noqa: E402
+from paper_2410_18701_b200.baton import baton_prefill_attention, baton_prefill_attention_varlen  # noqa: E402
 
 
 def main():
@@ -30,6 +30,52 @@ def main():
               ("13b", 40, 40, 1024), ("70b", 64, 8, 3400)]
     if args.only:
         shapes = [s for s in shapes if f"{s[0]}:{s[3]}" == args.only]
+    def graph_us(fn):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        # graph-replayed launches: the per-call host work (three tensor-map encodes)
+        # would otherwise starve the GPU on the short prompts
+        g = torch.cuda.CUDAGraph()
+        st = torch.cuda.Stream()
+        st.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(st), torch.cuda.graph(g, stream=st):
+            for _ in range(args.iters):
+                fn()
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) * 1e3 / args.iters
+
+    # NEXT-2: the prompts of one iteration's inserts in ONE varlen launch vs one
+    # launch per prompt (same arithmetic, bit-identical rows)
+    batches = [("13b", 40, 40, [600, 550]), ("7b", 32, 32, [1500, 350, 120, 900]),
+               ("70b", 64, 8, [3400, 300, 200])]
+    for name, Hq, Hkv, lens in ([] if args.only else batches):
+        D, T = 128, sum(lens)
+        q = torch.randn((Hq, T, D), device="cuda").to(torch.bfloat16)
+        k = torch.randn((Hkv, T, D), device="cuda").to(torch.bfloat16)
+        v = torch.randn((Hkv, T, D), device="cuda").to(torch.bfloat16)
+        o = torch.empty_like(q)
+        us_v = graph_us(lambda: baton_prefill_attention_varlen(q, k, v, o, lens, Hq, Hkv, D))
+        parts = []
+        s0 = 0
+        for n in lens:
+            parts.append((q[:, s0:s0 + n].contiguous(), k[:, s0:s0 + n].contiguous(),
+                          v[:, s0:s0 + n].contiguous(), torch.empty((Hq, n, D), dtype=torch.bfloat16,
+                                                                    device="cuda"), n))
+            s0 += n
+        us_s = graph_us(lambda: [baton_prefill_attention(a, b, c, d, n, Hq, Hkv, D) for a, b, c, d, n in parts])
+        flops = sum(4.0 * Hq * D * (n * (n + 1) / 2) for n in lens)
+        print(json.dumps({"shape": name, "varlen": lens, "q_heads": Hq, "kv_heads": Hkv, "us": us_v,
+                          "us_separate": us_s, "tflops": flops / us_v / 1e6,
+                          "tflops_separate": flops / us_s / 1e6, "frac": flops / us_v / 1e6 / peak}))
+
     for name, Hq, Hkv, n in shapes:
         D = 128
         q = torch.randn((Hq, n, D), device="cuda").to(torch.bfloat16)

@@ -83,3 +83,60 @@ def test_prefill_last_row_equals_decode_attention():
     a = bits_to_f64(bf16_bits(O[:, n - 1]))
     b = bits_to_f64(bf16_bits(od[0]))
     assert row_rel_err(a, b) <= ATTN_RTOL
+
+
+def _packed(seed, Hq, Hkv, lens, D=128):
+    T = int(sum(lens))
+    return _case(seed, Hq, Hkv, T, D)
+
+
+@pytest.mark.parametrize("Hq,Hkv,lens", [(4, 2, [1, 5, 127, 128, 129, 300]), (8, 1, [700, 33, 256, 129]),
+                                         (64, 8, [200, 1, 65])])
+def test_prefill_varlen_matches_oracle(Hq, Hkv, lens):
+    """NEXT-2 batched prefill: every packed prompt is its own causal problem (O-1 per
+    prefix of that prompt); nothing crosses prompt boundaries."""
+    require_cuda()
+    from paper_2410_18701_b200.baton import baton_prefill_attention_varlen
+    Q, K, V = _packed(sum(lens) + Hq, Hq, Hkv, lens)
+    O = torch.full_like(Q, float("nan"))
+    baton_prefill_attention_varlen(Q, K, V, O, lens, Hq, Hkv, 128)
+    torch.cuda.synchronize()
+    got = bits_to_f64(bf16_bits(O))
+    assert np.isfinite(got).all()
+    s0 = 0
+    worst = 0.0
+    for n in lens:
+        sl = slice(s0, s0 + n)
+        rows = sorted(set([0, n - 1, n // 2] + list(np.random.default_rng(n).integers(0, n, 8))))
+        ref = _reference(Q[:, sl], K[:, sl], V[:, sl], rows)
+        worst = max(worst, max(row_rel_err(got[:, s0 + i], ref[i]) for i in rows))
+        s0 += n
+    assert worst <= ATTN_RTOL, worst
+
+
+def test_prefill_varlen_equals_separate_calls_bitwise():
+    require_cuda()
+    from paper_2410_18701_b200.baton import baton_prefill_attention, baton_prefill_attention_varlen
+    Hq, Hkv, lens = 8, 2, [700, 33, 256, 129, 1, 511]
+    Q, K, V = _packed(77, Hq, Hkv, lens)
+    O = torch.empty_like(Q)
+    baton_prefill_attention_varlen(Q, K, V, O, lens, Hq, Hkv, 128)
+    s0 = 0
+    for n in lens:
+        sl = slice(s0, s0 + n)
+        o1 = torch.empty((Hq, n, 128), dtype=torch.bfloat16, device="cuda")
+        baton_prefill_attention(Q[:, sl].contiguous(), K[:, sl].contiguous(), V[:, sl].contiguous(), o1, n,
+                                Hq, Hkv, 128)
+        torch.cuda.synchronize()
+        assert np.array_equal(bf16_bits(O[:, sl]), bf16_bits(o1)), n
+        s0 += n
+
+
+def test_prefill_varlen_errors():
+    require_cuda()
+    from paper_2410_18701_b200.baton import baton_prefill_attention_varlen, BatonError
+    Q, K, V = _case(1, 2, 2, 10)
+    O = torch.empty_like(Q)
+    for lens in ([4, 0, 6], [1] * 65, [10] * 0):
+        with pytest.raises((BatonError, ValueError)):
+            baton_prefill_attention_varlen(Q, K, V, O, lens, 2, 2, 128)
