@@ -33,7 +33,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 T0_DEFAULT = 512          # steady-state start iteration of the Poisson workload
-INS_AHEAD = 8             # e2e: steps of lookahead for the prefilled K/V H2D of upcoming inserts
+INS_AHEAD = 16            # e2e: steps of lookahead for the prefilled K/V H2D of upcoming inserts
+INS_PIECE = 8 << 20       # e2e: bytes per insert H2D piece
+INS_BUDGET = 48 << 20     # e2e: insert H2D bytes issued per step (PCIe ~97 MB per 1.95 ms step; mean need ~32 MB)
 
 
 def _peaks():
@@ -342,7 +344,7 @@ def run_baton(args, rank, world, local_rank):
         del q_all, k_all, v_all
         pref.clear()
         gc.collect()
-        torch.cuda.empty_cache()
+        # (no empty_cache: the freed prefilled-K/V blocks serve the e2e insert buffers)
         # double-buffered device staging, filled by a copy stream one step ahead so
         # the PCIe transfer of step i+1 overlaps the decode of step i
         sets = [tuple(torch.empty(shp, dtype=torch.bfloat16, device=dev)
@@ -371,38 +373,76 @@ def run_baton(args, rank, world, local_rank):
             return sets[slot]
 
         # prefilled K/V of the queries inserted at window step i arrive on their own
-        # copy stream INS_AHEAD steps ahead (inserts are known from the window plan;
-        # one 7B insert of ~550 tokens is ~0.6 GB, ~12 ms of PCIe at 50 GB/s)
+        # copy stream, enqueued INS_AHEAD steps ahead (inserts are known from the window
+        # plan) and issued in pieces of at most INS_PIECE bytes, INS_BUDGET bytes per
+        # step: one 7B insert of ~550 tokens is ~0.6 GB (~12 ms of PCIe at 50 GB/s), and
+        # issued whole it could sit in a copy engine's queue ahead of the next step's q/k/v
         ins_at = {}
         for q, n, t_ins in fresh:
             ins_at.setdefault(t_ins - t_base, []).append(q)
         pref_dev = {}
+        pending = []          # [qid, [(dst, src) flat views], part index, element offset, event]
 
         def prefetch_inserts(i):
             for q in ins_at.get(i, []):
                 a, b = pref_h[q]
-                with torch.cuda.stream(ins_stream):
-                    da, db = a.to(dev, non_blocking=True), b.to(dev, non_blocking=True)
-                    ev = torch.cuda.Event()
-                    ev.record(ins_stream)
-                counters["h2d"] += (a.numel() + b.numel()) * 2
+                # allocated on the decode stream (whose cached blocks from the device pass
+                # have these shapes: no cudaMalloc stalling the host mid-window); the copy
+                # stream fills them, the decode stream waits on `ev` before the insert
+                da = torch.empty(a.shape, dtype=a.dtype, device=dev)
+                db = torch.empty(b.shape, dtype=b.dtype, device=dev)
+                ev = torch.cuda.Event()
                 pref_dev[q] = (da, db, ev)
+                pending.append([q, [(da.view(-1), a.view(-1)), (db.view(-1), b.view(-1))], 0, 0, ev])
+
+        def pump(budget, until=None, gate=None):
+            """Issue queued insert pieces: `budget` bytes, or through query `until`.
+            `gate`: a decode-stream event the pieces wait for.  The host runs many steps
+            ahead of the GPU, so without it a per-step budget is no pacing at all: the
+            copy engine would take pieces queued for later steps while this step's q/k/v
+            copy still waits on its event, and stall the decode behind them."""
+            if gate is not None and pending:
+                ins_stream.wait_event(gate)
+            with torch.cuda.stream(ins_stream):
+                while pending and (budget > 0 or until is not None):
+                    ent = pending[0]
+                    dst, src = ent[1][ent[2]]
+                    n = min(src.numel() - ent[3], INS_PIECE // 2)
+                    dst[ent[3]:ent[3] + n].copy_(src[ent[3]:ent[3] + n], non_blocking=True)
+                    budget -= 2 * n
+                    counters["h2d"] += 2 * n
+                    ent[3] += n
+                    if ent[3] == src.numel():
+                        ent[2], ent[3] = ent[2] + 1, 0
+                        if ent[2] == len(ent[1]):
+                            ent[4].record(ins_stream)
+                            pending.pop(0)
+                            if ent[0] == until:
+                                return
 
         def prefill_host(qid, n):
             if qid not in pref_dev:          # not prefetched (should not happen): copy now
                 a, b = pref_h[qid]
                 counters["h2d"] += (a.numel() + b.numel()) * 2
                 return a.to(dev, non_blocking=True), b.to(dev, non_blocking=True)
+            if any(e[0] == qid for e in pending):   # burst: issue the rest of its pieces now
+                pump(0, until=qid)
             da, db, ev = pref_dev.pop(qid)
             torch.cuda.current_stream().wait_event(ev)
             da.record_stream(torch.cuda.current_stream())
             db.record_stream(torch.cuda.current_stream())
             return da, db
 
+        step_ev = []             # (step, event at its start on the decode stream, inserts)
+
         def step(eng2, i, warm):
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev0.record()
+            step_ev.append((i, ev0, len(ins_at.get(i, []))))
             if i + 1 < n_iters:
                 h2d(i + 1)
             prefetch_inserts(i + INS_AHEAD)
+            pump(INS_BUDGET, gate=ev0)
             st_ = eng2.iteration()
             free[i % 2].record()
             res_h.copy_(eng2.out[L - 1], non_blocking=True)   # the step's result to the host
@@ -417,8 +457,13 @@ def run_baton(args, rank, world, local_rank):
         for ev in free:
             ev.record()
         h2d(0)
+        # steady state: the prefetch pipeline is full when the window opens (the inserts
+        # of the next INS_AHEAD steps have landed); inside the timed region the pieces of
+        # the inserts INS_AHEAD steps ahead move, and those are the bytes counted
         for i in range(INS_AHEAD):
             prefetch_inserts(i)
+        pump(1 << 62)
+        torch.cuda.synchronize()   # pipeline fill done (else it queues ahead of the first steps' tokens)
         for i in range(W):
             step(eng, i, True)
         if world > 1:
@@ -428,13 +473,18 @@ def run_baton(args, rank, world, local_rank):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
+        h0 = time.perf_counter()
         st2 = [step(eng, W + i, False) for i in range(K_steps)]
+        host_ms = (time.perf_counter() - h0) * 1e3
         e1.record()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         ms2 = e0.elapsed_time(e1)
-        e2e = {"ms": ms2, "tokens": sum(s.decoded for s in st2), "h2d": counters["h2d"] / K_steps,
+        marks = [x for x in step_ev if x[0] >= W] + [(None, e1, 0)]
+        step_ms = [(marks[k][0], marks[k][2], marks[k][1].elapsed_time(marks[k + 1][1]))
+                   for k in range(len(marks) - 1)]
+        e2e = {"ms": ms2, "host_ms": host_ms, "step_ms": step_ms, "tokens": sum(s.decoded for s in st2), "h2d": counters["h2d"] / K_steps,
                "d2h": counters["d2h"] / K_steps}
         release(eng)
 
@@ -622,7 +672,14 @@ def main():
         if r["e2e"]:
             line["e2e"] = {"value": e2e_tok / (e2e_ms / 1e3), "unit": "tokens/s",
                            "h2d_bytes_per_step": int(r["e2e"]["h2d"]),
-                           "d2h_bytes_per_step": int(r["e2e"]["d2h"])}
+                           "d2h_bytes_per_step": int(r["e2e"]["d2h"]),
+                           "host_enqueue_ms_per_step": r["e2e"]["host_ms"] / r["iters"],
+                           "step_ms_p50_p90_max": [statistics.median([x[2] for x in r["e2e"]["step_ms"]]),
+                                                   sorted(x[2] for x in r["e2e"]["step_ms"])[
+                                                       int(0.9 * (len(r["e2e"]["step_ms"]) - 1))],
+                                                   max(x[2] for x in r["e2e"]["step_ms"])],
+                           "slowest_steps": sorted(((round(x[2], 2), x[0], x[1]) for x in r["e2e"]["step_ms"]),
+                                                   reverse=True)[:4]}
         if world == 1 and not args.no_cpu_baseline:
             t_step, live, L, n, _ = oracle_sample(budget_s=15.0, t0=args.t0)
             line["cpu_baseline"] = {
