@@ -599,6 +599,12 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # test-only overrides (tests/test_gpu_bench_multirank.py runs 2 ranks on ONE GPU over
+    # gloo to exercise this N>1 path; the driver's N>1 runs use the defaults: nccl, one GPU
+    # per rank)
+    backend = os.environ.get("BATON_BENCH_BACKEND", "nccl")
+    if "BATON_BENCH_DEVICE" in os.environ:
+        local_rank = int(os.environ["BATON_BENCH_DEVICE"])
 
     if args.impl == "reference":
         if rank == 0:
@@ -608,7 +614,11 @@ def main():
     import torch
     import torch.distributed as dist
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group(backend)
     r = run_baton(args, rank, world, local_rank)
 
     # max over ranks of the device time; tokens summed over ranks
@@ -616,10 +626,11 @@ def main():
     e2e_ms = r["e2e"]["ms"] if r["e2e"] else 0.0
     e2e_tok = r["e2e"]["tokens"] if r["e2e"] else 0
     if world > 1:
-        t = torch.tensor([ms, e2e_ms], dtype=torch.float64, device="cuda")
+        rdev = "cuda" if backend == "nccl" else "cpu"
+        t = torch.tensor([ms, e2e_ms], dtype=torch.float64, device=rdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, e2e_ms = t.tolist()
-        c = torch.tensor([tokens, e2e_tok], dtype=torch.float64, device="cuda")
+        c = torch.tensor([tokens, e2e_tok], dtype=torch.float64, device=rdev)
         dist.all_reduce(c)
         tokens, e2e_tok = [int(x) for x in c.tolist()]
 
