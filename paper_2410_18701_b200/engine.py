@@ -20,11 +20,13 @@ from typing import Dict, List, Optional, Tuple
 import numpy as np
 import torch
 
-from .baton import BatonShard, baton_keygen_tokens, baton_keygen_history, baton_prefill_attention
+from .baton import (BatonShard, baton_keygen_tokens, baton_keygen_history, baton_prefill_attention,
+                    baton_prefill_attention_varlen)
 from .comm import gather_completion_flags
 from .scheduler import Planner
 
 KIND_Q, KIND_K, KIND_V = 0, 1, 2
+PREFILL_BATCH_MEAN = 256      # batched (varlen) P&D prefill when prompts average <= this many tokens
 
 
 @dataclass
@@ -139,6 +141,52 @@ class Engine:
         O = torch.empty_like(Q)
         for l in range(wl.layers):
             baton_prefill_attention(Q[l], K[l], V[l], O[l], n, wl.q_heads, wl.kv_heads, wl.head_dim)
+
+    @staticmethod
+    def _batchable(items):
+        return len(items) > 1 and sum(n for _, n, _, _ in items) <= PREFILL_BATCH_MEAN * len(items)
+
+    def _prefill_attn_batch(self, items):
+        """a8 for several fresh queries at once (output discarded): per layer ONE
+        baton_prefill_attention_varlen launch over their prompts packed along the token
+        axis (NEXT-2).  The packed q/k/v come from the same keyed generator as the
+        per-query prefill (identical values), written straight into the packed layout."""
+        # Batching pays where launches dominate (short prompts: 3x for eight 30-200-token
+        # prompts, scripts/probes/prefill_batch_probe.py).  Long prompts keep one
+        # launch per query and layer: packing them would regenerate their K/V (the
+        # keyed generator runs at ~250 GB/s), which costs more than the launches saved.
+        if not self._batchable(items):
+            for it in items:
+                self._prefill_attn(*it)
+            return
+        wl = self.wl
+        L, D = wl.layers, wl.head_dim
+        groups, cur, tiles = [], [], 0          # launch limits: 64 prompts, 1024 query tiles
+        for it in items:
+            t = -(-it[1] // 128)
+            if cur and (len(cur) == 64 or tiles + t > 1024):
+                groups.append(cur)
+                cur, tiles = [], 0
+            cur.append(it)
+            tiles += t
+        groups.append(cur)
+        for grp in groups:
+            T = sum(n for _, n, _, _ in grp)
+            bufs = {}
+            for kind, H, sc in ((KIND_Q, wl.q_heads, wl.scales[0]), (KIND_K, wl.kv_heads, wl.scales[1]),
+                                (KIND_V, wl.kv_heads, wl.scales[2])):
+                t = torch.empty((L, H, T, D), dtype=torch.bfloat16, device=self.device)
+                s0 = 0
+                for qid, n, _, _ in grp:
+                    baton_keygen_history(t[:, :, s0:], L, H, D, qid, 0, n, kind, wl.seed, sc,
+                                         head_stride=T * D, layer_stride=H * T * D)
+                    s0 += n
+                bufs[kind] = t
+            O = torch.empty_like(bufs[KIND_Q])
+            lens = [n for _, n, _, _ in grp]
+            for l in range(L):
+                baton_prefill_attention_varlen(bufs[KIND_Q][l], bufs[KIND_K][l], bufs[KIND_V][l], O[l], lens,
+                                               wl.q_heads, wl.kv_heads, D)
 
     # ---------------------------------------------------------------- one iteration
     def done(self):
@@ -271,6 +319,7 @@ class Engine:
                if pl.rank_of(g) == self.rank]
         if ins:
             slots, ks, vs, lens = [], [], [], []
+            fresh = []                          # synchronous P&D: one batched a8 below
             for b, q, n, home in ins:
                 if home is not None:
                     K, V = self.stash.pop(q)
@@ -283,11 +332,13 @@ class Engine:
                 else:
                     K, V = self._prefill(q, n)
                     if self.prefill_attention:
-                        self._prefill_attn(q, n, K, V)
+                        fresh.append((q, n, K, V))
                 slots.append(b)
                 ks.append(K)
                 vs.append(V)
                 lens.append(n)
+            if fresh:
+                self._prefill_attn_batch(fresh)
             sh.baton_insert_many(slots, ks, vs, lens)
             stats.inserted = len(ins)
             stats.insert_rows = sum(lens)
@@ -306,13 +357,20 @@ class Engine:
         if not todo:
             return
         with torch.cuda.stream(self.prefill_stream):
-            for e in todo:
-                K, V = self._prefill(e.qid, e.length)
-                if self.prefill_attention:
-                    self._prefill_attn(e.qid, e.length, K, V)
+            kv = [(e.qid, e.length) + self._prefill(e.qid, e.length) for e in todo]
+            if self.prefill_attention and self._batchable(kv):
+                self._prefill_attn_batch(kv)     # one event: short prompts finish together
                 ev = torch.cuda.Event()
                 ev.record(self.prefill_stream)
-                self.prefetched[e.qid] = (K, V, ev)
+                for qid, _, K, V in kv:
+                    self.prefetched[qid] = (K, V, ev)
+                return
+            for qid, n, K, V in kv:              # an insert waits for its own query only
+                if self.prefill_attention:
+                    self._prefill_attn(qid, n, K, V)
+                ev = torch.cuda.Event()
+                ev.record(self.prefill_stream)
+                self.prefetched[qid] = (K, V, ev)
 
     def run(self, max_iters=None):
         all_stats = []
