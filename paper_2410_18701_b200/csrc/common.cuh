@@ -57,15 +57,16 @@ BATON_DEV bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
-// Watchdog: a pipeline deadlock reports the waiting barrier and traps after ~2 s
-// (turns a hung GPU into a launch error).  try_wait itself suspends in hardware,
+// Watchdog: a pipeline deadlock reports the waiting barrier and traps after ~30 s
+// (turns a hung GPU into a launch error; long enough for compute-sanitizer racecheck,
+// under which a producer can lag its consumers by seconds).  try_wait suspends in hardware,
 // so the clock is read only every 1024 unsuccessful tries.
 BATON_DEV void mbar_wait(uint64_t *bar, uint32_t parity) {
     if (mbar_try_wait(bar, parity)) return;
     const long long t0 = clock64();
     for (uint32_t n = 1;; ++n) {
         if (mbar_try_wait(bar, parity)) return;
-        if ((n & 1023) == 0 && clock64() - t0 > 4000000000LL) {
+        if ((n & 1023) == 0 && clock64() - t0 > 60000000000LL) {
             printf("baton watchdog: block %d thread %d stuck on mbarrier smem+0x%x parity %u\n",
                    blockIdx.x, threadIdx.x, smem_u32(bar), parity);
             __trap();
