@@ -238,6 +238,7 @@ def run_baton(args, rank, world, local_rank):
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
+        eng.gather_s, eng.gathers = 0.0, 0
         e0.record()
         st = []
         marks = []                 # one event after every iteration: per-iteration ms
@@ -254,6 +255,7 @@ def run_baton(args, rank, world, local_rank):
             dist.barrier()
         it_ms = [a.elapsed_time(b) for a, b in zip([e0] + marks[:-1], marks)]
         timed_window.iter_ms = it_ms
+        timed_window.gather_us = 1e6 * eng.gather_s / max(1, eng.gathers)
         return e0.elapsed_time(e1), st
 
     # ================= pass 1: `value` -- graph-replayed decode, inputs in HBM
@@ -265,6 +267,7 @@ def run_baton(args, rank, world, local_rank):
     clocks.mark("t_start")
     ms, stats = timed_window(eng)
     iter_ms = list(timed_window.iter_ms)
+    gather_us = timed_window.gather_us
     clocks.mark("t_end")
     clk = clocks.stop()
     release(eng)
@@ -493,7 +496,7 @@ def run_baton(args, rank, world, local_rank):
                 iter_ms=iter_ms,
                 attn_launches=attn_launches, splice_rows=splice_rows, tau=tau, L=L,
                 n_launch=n_launch, clocks=clk, e2e=e2e, iters=K_steps,
-                live_slots=tokens / K_steps, live_rows=live_rows)
+                live_slots=tokens / K_steps, live_rows=live_rows, gather_us=gather_us)
 
 
 # ------------------------------------------------------------------ the oracle arm
@@ -630,6 +633,16 @@ def main():
         t = torch.tensor([ms, e2e_ms], dtype=torch.float64, device=rdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, e2e_ms = t.tolist()
+        # SURVEY §8(d) for N > 1: the flag all-gather's host-blocking time per iteration
+        # (max over ranks) and the per-rank attention-byte imbalance (max / mean)
+        g = torch.tensor([r["gather_us"]], dtype=torch.float64, device=rdev)
+        dist.all_reduce(g, op=dist.ReduceOp.MAX)
+        bts = [torch.zeros(1, dtype=torch.float64, device=rdev) for _ in range(world)]
+        dist.all_gather(bts, torch.tensor([float(r["attn_bytes"])], dtype=torch.float64, device=rdev))
+        bts = [float(x.item()) for x in bts]
+        multi = {"allgather_us_per_iter": float(g.item()),
+                 "rank_attn_bytes_max_over_mean": max(bts) / (sum(bts) / world) if sum(bts) else None,
+                 "collective": "all_gather of int32 completion flags per iteration (" + backend + ")"}
         c = torch.tensor([tokens, e2e_tok], dtype=torch.float64, device=rdev)
         dist.all_reduce(c)
         tokens, e2e_tok = [int(x) for x in c.tolist()]
@@ -680,6 +693,8 @@ def main():
             "gpu_launches": r["n_launch"],
             "clocks": r["clocks"],
         }
+        if world > 1:
+            line["multi_gpu"] = multi
         if r["e2e"]:
             line["e2e"] = {"value": e2e_tok / (e2e_ms / 1e3), "unit": "tokens/s",
                            "h2d_bytes_per_step": int(r["e2e"]["h2d"]),

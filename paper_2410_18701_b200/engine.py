@@ -14,6 +14,7 @@ One process per GPU.  Per iteration (reading of P:L101 / P:L124):
 
 Every device byte is produced by libbaton kernels (plus the harness keygen).
 """
+import time
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Tuple
 
@@ -89,6 +90,7 @@ class Engine:
         self.prefill_stream = torch.cuda.Stream(device=self.device) if async_prefill else None
         self.prefill_lookahead = prefill_lookahead or 2 * self.B
         self.prefetched: Dict[int, Tuple[torch.Tensor, torch.Tensor, torch.cuda.Event]] = {}
+        self.gather_s, self.gathers = 0.0, 0   # completion-flag all-gathers (world > 1)
         self.use_graph = use_graph
         self.staging = {(self.q.data_ptr(), self.k_new.data_ptr(), self.v_new.data_ptr())}
         # P:L147 "moved to the host memory": stored K/V in pinned host memory (the
@@ -279,7 +281,13 @@ class Engine:
         return dec
 
     def _gather_flags(self, local_flags):
-        return gather_completion_flags(local_flags, self.world, self.group, self.device)
+        if self.world == 1:
+            return gather_completion_flags(local_flags, self.world, self.group, self.device)
+        t0 = time.perf_counter()
+        out = gather_completion_flags(local_flags, self.world, self.group, self.device)
+        self.gather_s += time.perf_counter() - t0   # host-blocking: the collective + its D2H
+        self.gathers += 1
+        return out
 
     def iteration(self):
         pl = self.planner

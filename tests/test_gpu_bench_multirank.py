@@ -30,6 +30,8 @@ def test_bench_two_ranks_one_gpu():
     assert d["n_gpus"] == 2 and d["steps"] == 4 and d["scaling"] == "weak"
     assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
     assert d["config"]["parallelism"] == "slots/2 GPU"
+    assert d["multi_gpu"]["allgather_us_per_iter"] > 0
+    assert 1.0 <= d["multi_gpu"]["rank_attn_bytes_max_over_mean"] < 2.0
     # tokens are summed over ranks (each decodes its own 32 slots): more than one
     # rank's worth per step
     tokens_per_step = d["value"] * d["ms_per_step"] / 1e3
