@@ -677,7 +677,7 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "traffic_source": "profiles/r01_traffic.json (one ncu --set full launch)",
-                         "kernel": "decode_attention_kernel<128>",
+                         "kernel": "decode_attention_kernel<128, 4, 2, 3>",
                          "bytes_per_launch": per_launch,
                          "peak_source": peak_kind,
                          "avg_launch_us": 1e6 * r["attn_time_s"] / max(1, r["attn_launches"]),

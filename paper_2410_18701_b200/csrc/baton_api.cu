@@ -34,7 +34,7 @@ struct baton_state {
     static constexpr int kGraphs = 4;
     cudaStream_t cap_stream = nullptr;
     cudaGraphExec_t step_exec[kGraphs] = {nullptr, nullptr, nullptr, nullptr};
-    const void *step_io[kGraphs][5] = {};   // q, k_new, v_new, out, MHA variant
+    const void *step_io[kGraphs][4] = {};
     unsigned long long step_used[kGraphs] = {0, 0, 0, 0};
     unsigned long long step_clock = 0;
     ~baton_state() {
@@ -205,19 +205,8 @@ int baton_decode_attention(const void *q, const void *k, const void *v, const ui
 }
 
 namespace {
-// MHA pipeline variant from the host mirror's split-K work items (lens + `extra`, the
-// rows a pending mask update adds); -1 for shapes that do not take the MHA kernel
-int pick_variant(const baton_state *st, int extra) {
-    const baton_shape &s = st->sh;
-    if (s.head_dim != 128 || gqa_supported(s.q_heads, s.kv_heads, s.head_dim)) return -1;
-    long long items = 0;
-    for (int b = 0; b < s.slots; ++b)
-        if (st->occ[b]) items += (long long)s.q_heads * ((st->lens[b] + extra + CHUNK - 1) / CHUNK);
-    return mha_variant_for_items(items);
-}
-
 DecodeArgs layer_args(baton_state *st, int layer, const void *q, const void *k_new, const void *v_new,
-                      void *out, bool early, int variant = -1) {
+                      void *out, bool early) {
     const baton_shape &s = st->sh;
     DecodeArgs a;
     a.q = q;
@@ -240,7 +229,6 @@ DecodeArgs layer_args(baton_state *st, int layer, const void *q, const void *k_n
     a.max_chunks = st->max_chunks;
     a.scale = 1.0f / sqrtf((float)s.head_dim);
     a.early = early;
-    a.variant = variant;
     return a;
 }
 }  // namespace
@@ -251,7 +239,7 @@ int baton_decode_layer(baton_state *st, int layer, const void *q, const void *k_
     if ((k_new == nullptr) != (v_new == nullptr)) return BATON_E_INVALID;
     // a2 fused into a3: one launch streams the cache and embeds the new token
     const int r = cuda_status(launch_decode_attention(
-        layer_args(st, layer, q, k_new, v_new, out, st->prev_decode, pick_variant(st, 0)), as_stream(stream)));
+        layer_args(st, layer, q, k_new, v_new, out, st->prev_decode), as_stream(stream)));
     st->prev_decode = r == BATON_OK;
     return r;
 }
@@ -264,8 +252,7 @@ int baton_decode_step(baton_state *st, const void *q, const void *k_new, const v
     const baton_shape &s = st->sh;
     const size_t qstride = (size_t)s.slots * s.q_heads * s.head_dim;
     const size_t kstride = (size_t)s.slots * s.kv_heads * s.head_dim;
-    const int variant = pick_variant(st, 1);   // lens after this step's mask update
-    const void *io[5] = {q, k_new, v_new, out, reinterpret_cast<const void *>((intptr_t)variant)};
+    const void *io[4] = {q, k_new, v_new, out};
     int slot = -1;
     for (int i = 0; i < baton_state::kGraphs; ++i)
         if (st->step_exec[i] && std::memcmp(io, st->step_io[i], sizeof(io)) == 0) slot = i;
@@ -282,7 +269,7 @@ int baton_decode_step(baton_state *st, const void *q, const void *k_new, const v
         cudaError_t e = cudaSuccess;
         if (!st->cap_stream) e = cudaStreamCreateWithFlags(&st->cap_stream, cudaStreamNonBlocking);
         if (e != cudaSuccess) return cuda_status(e);
-        DecodeArgs probe = layer_args(st, 0, q, k_new, v_new, out, false, variant);
+        DecodeArgs probe = layer_args(st, 0, q, k_new, v_new, out, false);
         probe.dry = true;   // kernel attributes must be set outside the capture
         if ((e = launch_decode_attention(probe, st->cap_stream)) != cudaSuccess) return cuda_status(e);
         if ((e = cudaStreamBeginCapture(st->cap_stream, cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
@@ -294,7 +281,7 @@ int baton_decode_step(baton_state *st, const void *q, const void *k_new, const v
             const __nv_bfloat16 *vl = static_cast<const __nv_bfloat16 *>(v_new) + l * kstride;
             __nv_bfloat16 *ol = static_cast<__nv_bfloat16 *>(out) + l * qstride;
             // layer 0 follows the mask update (writes lens): no early prefetch
-            e = launch_decode_attention(layer_args(st, l, ql, kl, vl, ol, l > 0, variant), st->cap_stream);
+            e = launch_decode_attention(layer_args(st, l, ql, kl, vl, ol, l > 0), st->cap_stream);
         }
         cudaGraph_t g = nullptr;
         const cudaError_t e2 = cudaStreamEndCapture(st->cap_stream, &g);

@@ -544,33 +544,18 @@ cudaError_t launch_d(const DecodeArgs &a, cudaStream_t s) {
                       dim3((CW + 1) * 32), smem, s, p);
 }
 
-// head_dim 128 pipeline variants (consumer warps, ring stages, CTAs per SM): an
-// explicit BATON_MHA_VARIANT (sweeps) wins, else the caller's choice, else 0.
-int mha_variant(int requested) {
-    static int env = -2;
-    if (env == -2) {
+// head_dim 128 pipeline variants (consumer warps, ring stages, CTAs per SM), chosen
+// by BATON_MHA_VARIANT for sweeps; 0 is the default.
+int mha_variant() {
+    static int v = -1;
+    if (v < 0) {
         const char *e = getenv("BATON_MHA_VARIANT");
-        env = e ? atoi(e) : -1;
+        v = e ? atoi(e) : 0;
     }
-    if (env >= 0) return env;
-    return requested >= 0 ? requested : 0;
+    return v;
 }
 
 }  // namespace
-
-// Few work items per resident CTA leave the default's 5 CTAs/SM with a long tail: below
-// three items per CTA of the default grid, (4 warps, 2 stages, 3 CTAs/SM) wins.  Measured
-// on the stress shard (16 live slots, ~1.5k items): 15.9k vs 12.8k tok/s; on configs[1]
-// (~3.3k items) the default is 2% faster (profiles/r01_mha_sweep.md).
-int mha_variant_for_items(long long items) {
-    static int num_sms = 0;
-    if (!num_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    return items < 3LL * 5 * num_sms ? 3 : 0;
-}
 
 size_t decode_partial_bytes(int slots, int q_heads, int head_dim, int max_ctx) {
     return (size_t)slots * q_heads * ceil_div(max_ctx, CHUNK) * (head_dim + PREC_PAD) * sizeof(float);
@@ -587,14 +572,17 @@ cudaError_t launch_decode_attention(const DecodeArgs &a, cudaStream_t s) {
         case 32: return launch_d<32, 4, 3, 2>(a, s);
         case 64: return launch_d<64, 4, 3, 2>(a, s);
         case 128:
-            switch (mha_variant(a.variant)) {
+            switch (mha_variant()) {
                 // measured on the cfg2 t0 state (profiles/r01_mha_sweep.md), us/launch:
                 // (4,3,2) 66.2  (4,6,1) 93.6  (8,3,1) 82.3  (4,2,3) 59.8  (2,3,3) 64.2
                 // (2,2,5) 58.7  (2,2,4) 59.2  (1,4,5) 64.6  (3,2,3) 60.8
+                // late round 1, on the current kernel: (4,2,3) beats (2,2,5) by 2% on
+                // configs[1] and by 24% on the stress shard (few items per CTA), ties on
+                // 13B churn -> the default (profiles/r01_mha_sweep.md)
                 case 1: return launch_d<128, 4, 3, 2>(a, s);
-                case 3: return launch_d<128, 4, 2, 3>(a, s);
+                case 5: return launch_d<128, 2, 2, 5>(a, s);
                 case 6: return launch_d<128, 2, 2, 4>(a, s);
-                default: return launch_d<128, 2, 2, 5>(a, s);
+                default: return launch_d<128, 4, 2, 3>(a, s);
             }
         default: return cudaErrorInvalidValue;
     }

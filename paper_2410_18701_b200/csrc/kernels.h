@@ -32,13 +32,7 @@ struct DecodeArgs {
     int32_t *tickets;               // [slots][q_heads] (+2 work counters), zero between calls
     int slots, q_heads, kv_heads, head_dim, max_ctx, max_chunks;
     float scale;
-    // MHA head_dim-128 pipeline variant (decode_attention.cu), chosen by the stateful
-    // entry points from the host mirror's work size; -1 = the default.  An explicit
-    // BATON_MHA_VARIANT (sweeps) overrides it.
-    int variant = -1;
 };
-// pipeline variant of the MHA head_dim-128 decode for `items` split-K work items
-int mha_variant_for_items(long long items);
 size_t decode_partial_bytes(int slots, int q_heads, int head_dim, int max_ctx);
 size_t decode_ticket_bytes(int slots, int q_heads);
 bool decode_supported_head_dim(int head_dim);
