@@ -38,6 +38,16 @@ INS_PIECE = 8 << 20       # e2e: bytes per insert H2D piece
 INS_BUDGET = 48 << 20     # e2e: insert H2D bytes issued per step (PCIe ~97 MB per 1.95 ms step; mean need ~32 MB)
 
 
+def _cpu_model():
+    try:
+        for l in open("/proc/cpuinfo"):
+            if l.startswith("model name"):
+                return l.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def _peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -491,7 +501,49 @@ def run_baton(args, rank, world, local_rank):
                "d2h": counters["d2h"] / K_steps}
         release(eng)
 
-    return dict(splice_bytes=splice_bytes, splice_s=splice_s, splice_calls=len(splice_ev),
+    # ================= a8: the window's inserted prompts through the tcgen05 prefill
+    # (P&D decouples it from the decode loop): one varlen launch per
+    # layer over every prompt the window inserts; all layers cost the same, so one
+    # layer is graph-timed.  Reported beside the decode numbers, not part of `value`.
+    prefill = None
+    if rank == 0 and fresh:
+        from paper_2410_18701_b200.baton import baton_prefill_attention_varlen
+        plens = [n for _, n, _ in fresh][:64]
+        T = sum(plens)
+        g = torch.Generator(device=dev).manual_seed(18701)
+        qp = torch.randn((Hq, T, D), device=dev, generator=g).to(torch.bfloat16)
+        kp = torch.randn((Hkv, T, D), device=dev, generator=g).to(torch.bfloat16)
+        vp = torch.randn((Hkv, T, D), device=dev, generator=g).to(torch.bfloat16)
+        op = torch.empty_like(qp)
+        reps = 10
+        for _ in range(2):
+            baton_prefill_attention_varlen(qp, kp, vp, op, plens, Hq, Hkv, D)
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side), torch.cuda.graph(gr, stream=side):
+            for _ in range(reps):
+                baton_prefill_attention_varlen(qp, kp, vp, op, plens, Hq, Hkv, D)
+        gr.replay()
+        torch.cuda.synchronize()
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record()
+        gr.replay()
+        p1.record()
+        torch.cuda.synchronize()
+        us = p0.elapsed_time(p1) * 1e3 / reps
+        flop = sum(4.0 * Hq * D * n * (n + 1) / 2 for n in plens)
+        pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
+        bf16_peak = json.load(open(pk))["bf16_tflops"] if os.path.exists(pk) else 2250.0
+        prefill = {"what": "baton_prefill_attention_varlen (tcgen05) over the window's inserted prompts, "
+                           "one layer, graph-timed", "prompts": len(plens), "tokens": T,
+                   "us_per_layer": us, "tflops": flop / us / 1e6, "peak_tflops": bf16_peak,
+                   "peak_source": "measured" if os.path.exists(pk) else "nominal",
+                   "frac": flop / us / 1e6 / bf16_peak}
+        del qp, kp, vp, op, gr
+
+    return dict(splice_bytes=splice_bytes, splice_s=splice_s, splice_calls=len(splice_ev), prefill=prefill,
                 ms=ms, tokens=tokens, attn_bytes=attn_bytes_total, attn_time_s=attn_time_s,
                 iter_ms=iter_ms,
                 attn_launches=attn_launches, splice_rows=splice_rows, tau=tau, L=L,
@@ -575,7 +627,7 @@ def run_reference(args):
         "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (keyed generator)",
         "config": {"workload": "7b", "t0": args.t0},
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle", "cpu_model": _cpu_model(),
                          "sample": f"O-2 Shard.step (fp64 NumPy), per step 1 of {L} layers x {m} of {live} "
                                    f"live slots (length quantiles) at iteration {args.t0}; {n} timed steps "
                                    f"after {args.warmup} warm-up; tokens/s = {m} / ({L} x step time)"},
@@ -706,10 +758,13 @@ def main():
                                                    max(x[2] for x in r["e2e"]["step_ms"])],
                            "slowest_steps": sorted(((round(x[2], 2), x[0], x[1]) for x in r["e2e"]["step_ms"]),
                                                    reverse=True)[:4]}
+        if r.get("prefill"):
+            line["prefill"] = r["prefill"]
         if world == 1 and not args.no_cpu_baseline:
             t_step, live, L, n, _ = oracle_sample(budget_s=15.0, t0=args.t0)
             line["cpu_baseline"] = {
                 "value": live / (L * t_step), "unit": "tokens/s", "cores": 1, "kind": "oracle",
+                "cpu_model": _cpu_model(),
                 "sample": f"O-2 Shard.step (fp64 NumPy, single thread), 1 of {L} layers, {live} live "
                           f"slots at iteration {args.t0}, {n} steps, extrapolated x{L} layers"}
         print(json.dumps(line))
