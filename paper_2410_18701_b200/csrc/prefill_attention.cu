@@ -262,6 +262,12 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
             const int sb = j & 1;
             const uint32_t tSj = tS + 64 * sb + lane_off;
             mbar_wait(&sm.s_full[sb], (j >> 1) & 1);
+            // one thread observes PV(j-2)'s completion on its barrier: already done (S(j)
+            // was issued after it and its commit covers every earlier MMA), so this never
+            // blocks; it keeps every phase of pv_done waited on (compute-sanitizer
+            // synccheck flags a phase completed with no wait; with all 128 threads
+            // polling it cost ~1%)
+            if (j >= 2 && threadIdx.x == 0) mbar_wait(&sm.pv_done[sb], ((j - 2) >> 1) & 1);
             tc_fence_after();
             const int kbase = j * PF_N;
             const bool diag = kbase + PF_N > off + q0;   // tile touches the causal diagonal

@@ -5,7 +5,7 @@
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out/sanitize
 SMOKE='import __graft_entry__ as g; g.smoke()'
-TESTS="tests/test_gpu_decode.py::test_matches_oracle tests/test_gpu_decode.py::test_gqa_matches_oracle tests/test_gpu_prefill.py::test_prefill_matches_oracle tests/test_gpu_shaping.py::test_w1_shaping_replay"
+TESTS="tests/test_gpu_decode.py::test_matches_oracle tests/test_gpu_decode.py::test_gqa_matches_oracle tests/test_gpu_prefill.py::test_prefill_matches_oracle tests/test_gpu_prefill.py::test_prefill_varlen_matches_oracle tests/test_gpu_shaping.py::test_w1_shaping_replay"
 for tool in memcheck racecheck synccheck initcheck; do
   timeout 900 compute-sanitizer --tool $tool --print-limit 20 python -c "$SMOKE" \
     > gpurun_out/sanitize/smoke_$tool.log 2>&1
