@@ -501,6 +501,30 @@ def run_baton(args, rank, world, local_rank):
                "d2h": counters["d2h"] / K_steps}
         release(eng)
 
+    # ================= full run (steady-state AND full-run tokens/s): the
+    # whole 512-query workload from iteration 0 until the batch drains -- fill, the
+    # overloaded steady state, the tail with no replenishment.  Every step's q/k/v and
+    # every insert's prefilled K/V come from the keyed generator on the device inside
+    # the timed region (standing in for the model's projections and the prefill).
+    full_run = None
+    if world == 1 and not args.no_full_run:
+        engf = Engine(wl, rank=0, world=1, device=dev, use_graph=True)
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        st_f = engf.run()
+        f1.record()
+        torch.cuda.synchronize()
+        ms_f = f0.elapsed_time(f1)
+        tok_f = sum(s.decoded for s in st_f)
+        full_run = {"value": tok_f / (ms_f / 1e3), "unit": "tokens/s", "iterations": len(st_f),
+                    "tokens": tok_f, "queries": len(wl.queries), "ms": ms_f,
+                    "what": "whole workload from iteration 0 to drain, one GPU; per-step q/k/v and "
+                            "inserted K/V generated on the device (keygen) inside the timed region"}
+        del engf, st_f
+        gc.collect()
+        torch.cuda.empty_cache()
+
     # ================= a8: the window's inserted prompts through the tcgen05 prefill
     # (P&D decouples it from the decode loop): one varlen launch per
     # layer over every prompt the window inserts; all layers cost the same, so one
@@ -544,6 +568,7 @@ def run_baton(args, rank, world, local_rank):
         del qp, kp, vp, op, gr
 
     return dict(splice_bytes=splice_bytes, splice_s=splice_s, splice_calls=len(splice_ev), prefill=prefill,
+                full_run=full_run,
                 ms=ms, tokens=tokens, attn_bytes=attn_bytes_total, attn_time_s=attn_time_s,
                 iter_ms=iter_ms,
                 attn_launches=attn_launches, splice_rows=splice_rows, tau=tau, L=L,
@@ -646,6 +671,7 @@ def main():
     ap.add_argument("--t0", type=int, default=T0_DEFAULT)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-full-run", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=20.0)
     args = ap.parse_args()
     if args.warmup < 3:
@@ -760,6 +786,8 @@ def main():
                                                    reverse=True)[:4]}
         if r.get("prefill"):
             line["prefill"] = r["prefill"]
+        if r.get("full_run"):
+            line["full_run"] = r["full_run"]
         if world == 1 and not args.no_cpu_baseline:
             t_step, live, L, n, _ = oracle_sample(budget_s=15.0, t0=args.t0)
             line["cpu_baseline"] = {
