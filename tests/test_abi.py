@@ -55,6 +55,23 @@ def test_host_side_validation():
                                       ctypes.byref(good), 0.1, None, 0, None) == _lib.BATON_E_INVALID
     assert lib.baton_mask_update(None, None) == _lib.BATON_E_INVALID
     assert lib.baton_keygen_history(None, 1, 1, 16, 0, 0, 1, 0, 0, 0, 16, 16, None) == _lib.BATON_E_INVALID
+    # batched prefill: every rejection happens on the host, before any launch
+    fake = ctypes.c_void_p(1 << 20)                    # 16-B aligned, never dereferenced
+    pf = make_shape(1, 1, 8, 8, 128, 16)
+
+    def varlen(cu, n, shape=pf, q=fake, scale=0.1):
+        arr = (ctypes.c_int32 * len(cu))(*cu)
+        return lib.baton_prefill_attention_varlen(q, fake, fake, fake, arr, n, ctypes.byref(shape),
+                                                  scale, None)
+    assert varlen([0, 5], 1, q=None) == _lib.BATON_E_INVALID          # null tensor
+    assert varlen([0], 0) == _lib.BATON_E_INVALID                     # no prompt
+    assert varlen(list(range(66)), 65) == _lib.BATON_E_INVALID        # > 64 prompts
+    assert varlen([1, 5], 1) == _lib.BATON_E_INVALID                  # cu_lens[0] != 0
+    assert varlen([0, 4, 4, 9], 3) == _lib.BATON_E_INVALID            # an empty prompt
+    assert varlen([0, 40 * 128 * 27], 1) == _lib.BATON_E_INVALID      # > 1024 query tiles
+    assert varlen([0, 5], 1, scale=0.0) == _lib.BATON_E_INVALID       # scale must be > 0
+    assert varlen([0, 5], 1, shape=make_shape(1, 1, 8, 8, 64, 16)) == _lib.BATON_E_INVALID  # head_dim
+    assert varlen([0, 5], 1, q=ctypes.c_void_p((1 << 20) + 8)) == _lib.BATON_E_INVALID      # alignment
     assert lib.baton_error_string(_lib.BATON_E_SLOT_BUSY).decode() == "slot busy"
 
 
