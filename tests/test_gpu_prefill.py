@@ -140,3 +140,25 @@ def test_prefill_varlen_errors():
     for lens in ([4, 0, 6], [1] * 65, [10] * 0):
         with pytest.raises((BatonError, ValueError)):
             baton_prefill_attention_varlen(Q, K, V, O, lens, 2, 2, 128)
+
+
+def test_prefill_varlen_max_prompts_bitwise():
+    """The launch limits: 64 packed prompts (ragged, 1..300 tokens, tile-boundary
+    lengths included), every one bit-identical to its own separate launch."""
+    require_cuda()
+    from paper_2410_18701_b200.baton import baton_prefill_attention, baton_prefill_attention_varlen
+    rng = np.random.default_rng(64)
+    lens = [1, 127, 128, 129, 256] + [int(x) for x in rng.integers(1, 300, 59)]
+    Hq, Hkv = 8, 1
+    Q, K, V = _packed(640, Hq, Hkv, lens)
+    O = torch.empty_like(Q)
+    baton_prefill_attention_varlen(Q, K, V, O, lens, Hq, Hkv, 128)
+    s0 = 0
+    for n in lens:
+        sl = slice(s0, s0 + n)
+        o1 = torch.empty((Hq, n, 128), dtype=torch.bfloat16, device="cuda")
+        baton_prefill_attention(Q[:, sl].contiguous(), K[:, sl].contiguous(), V[:, sl].contiguous(), o1, n,
+                                Hq, Hkv, 128)
+        torch.cuda.synchronize()
+        assert np.array_equal(bf16_bits(O[:, sl]), bf16_bits(o1)), n
+        s0 += n
