@@ -249,3 +249,30 @@ def test_policy_stream_replay(seed):
     sys.path.insert(0, os.path.dirname(__file__))
     from test_oracle_policies import _policy_stream
     _replay(_policy_stream(seed))
+
+
+def test_capacity_boundary():
+    """A query can fill its slot up to max_ctx exactly: the full slot decodes over
+    all max_ctx keys (finite output; the empty slot's row is zero, C6), and the step
+    that would write column max_ctx is refused (BATON_E_CAPACITY, C24) and changes
+    nothing."""
+    require_cuda()
+    from paper_2410_18701_b200 import _lib
+    from paper_2410_18701_b200.baton import BatonShard, BatonError
+    sh = BatonShard(1, 2, 2, 2, 16, 64)
+    K = torch.randn((1, 2, 63, 16), device="cuda").to(torch.bfloat16)
+    V = torch.randn_like(K)
+    sh.baton_insert(0, K, V, 63)
+    sh.baton_mask_update()                       # S = 64 = max_ctx, lens[0] = 64
+    m = sh.baton_query()
+    assert m["S"] == 64 and list(m["lens"])[:1] == [64]
+    q = torch.randn((2, 2, 16), device="cuda").to(torch.bfloat16)
+    out = torch.empty_like(q)
+    kn = torch.randn((2, 2, 16), device="cuda").to(torch.bfloat16)
+    sh.baton_decode_layer(0, q, out, kn, kn)     # appends row 63 and attends over 64 keys
+    torch.cuda.synchronize()
+    assert torch.isfinite(out[0].float()).all() and (out[1] == 0).all()
+    with pytest.raises(BatonError) as e:
+        sh.baton_mask_update()
+    assert e.value.code == _lib.BATON_E_CAPACITY
+    assert sh.baton_query()["S"] == 64
