@@ -276,3 +276,25 @@ def test_capacity_boundary():
         sh.baton_mask_update()
     assert e.value.code == _lib.BATON_E_CAPACITY
     assert sh.baton_query()["S"] == 64
+
+
+@pytest.mark.parametrize("hq,hkv,d", [(2, 2, 16), (32, 32, 128), (64, 8, 128)])
+def test_all_slots_empty(hq, hkv, d):
+    """Degenerate batch: no occupied slot.  The step computes nothing and writes zero
+    rows (C6), eager and graph-replayed, for the MHA and the tcgen05 GQA kernels."""
+    require_cuda()
+    from paper_2410_18701_b200.baton import BatonShard
+    sh = BatonShard(2, 4, hq, hkv, d, 64)
+    q = torch.randn((2, 4, hq, d), device="cuda").to(torch.bfloat16)
+    kn = torch.randn((2, 4, hkv, d), device="cuda").to(torch.bfloat16)
+    out = torch.full_like(q, 7.0)
+    sh.baton_decode_step(q, kn, kn, out)
+    torch.cuda.synchronize()
+    assert (out == 0).all()
+    out.fill_(7.0)
+    sh.baton_mask_update()
+    for l in range(2):
+        sh.baton_decode_layer(l, q[l], out[l], kn[l], kn[l])
+    torch.cuda.synchronize()
+    assert (out == 0).all()
+    assert sh.baton_query()["S"] == 2
