@@ -24,7 +24,7 @@ import torch
 from .baton import (BatonShard, baton_keygen_tokens, baton_keygen_history, baton_prefill_attention,
                     baton_prefill_attention_varlen)
 from .comm import gather_completion_flags
-from .scheduler import Planner
+from .scheduler import Planner, local_splice_ops
 
 KIND_Q, KIND_K, KIND_V = 0, 1, 2
 PREFILL_BATCH_MEAN = 256      # batched (varlen) P&D prefill when prompts average <= this many tokens
@@ -301,14 +301,21 @@ class Engine:
         d = pl.plan(flags)
         self.last_decisions = d
         sh = self.shard
-        fin = [pl.local(g) for g, _ in d.finished if pl.rank_of(g) == self.rank]
-        if d.t > 0:
-            # removal + release every iteration (C5); a no-op call enqueues nothing
-            stats.released += sh.baton_remove(fin)
-            stats.removed = len(fin)
-        vic = [(pl.local(g), q, n) for g, q, n in d.victims if pl.rank_of(g) == self.rank]
-        if vic:
-            for b, q, n in vic:
+        ops = local_splice_ops(pl, d, self.rank)
+        ins = []
+        for i, op in enumerate(ops):
+            kind = op[0]
+            if kind == "remove":
+                # removal + release every iteration (C5); a no-op call enqueues nothing.
+                # ops[0] (t > 0) removes the finished rows, later removes free victims
+                stats.released += sh.baton_remove(op[1])
+                if i == 0:
+                    stats.removed = len(op[1])
+                else:
+                    stats.stored += len(op[1])
+            elif kind == "extract":
+                _, b, q = op
+                n = int(sh.baton_query()["lens"][b])       # the library's live length
                 if self.stash_host:
                     shape = (self.wl.layers, self.wl.kv_heads, n, self.wl.head_dim)
                     ko = torch.empty(shape, dtype=torch.bfloat16, pin_memory=True)
@@ -317,14 +324,12 @@ class Engine:
                 else:
                     self.stash[q] = sh.baton_extract(b)
                 stats.extract_rows += n
-            stats.released += sh.baton_remove([b for b, _, _ in vic])
-            stats.stored = len(vic)
-        if d.resize is not None:
-            before = sh.baton_query()
-            o2n = sh.baton_compact(d.resize)
-            stats.compact_rows = int(sum(before["lens"][b] for b in range(self.B) if o2n[b] != b))
-        ins = [(pl.local(g), q, n, home) for g, q, n, home in d.inserts
-               if pl.rank_of(g) == self.rank]
+            elif kind == "compact":
+                before = sh.baton_query()
+                o2n = sh.baton_compact(op[1])
+                stats.compact_rows = int(sum(before["lens"][b] for b in range(self.B) if o2n[b] != b))
+            else:
+                ins = op[1]
         if ins:
             slots, ks, vs, lens = [], [], [], []
             fresh = []                          # synchronous P&D: one batched a8 below

@@ -39,6 +39,10 @@ class Decisions:
     finished: List[Tuple[int, int]] = field(default_factory=list)       # (gslot, qid)
     victims: List[Tuple[int, int, int]] = field(default_factory=list)   # (gslot, qid, length)
     resize: Optional[int] = None                                         # new active per rank
+    # victims[:n_pre_compact] were chosen BEFORE this iteration's compaction (their
+    # gslots are pre-compaction indices: C17 preemption, resize overflow); the rest
+    # (C26 governor, C25 priority preemption) AFTER it, in post-compaction indices
+    n_pre_compact: int = 0
     inserts: List[Tuple[int, int, int, Optional[int]]] = field(default_factory=list)  # (gslot, qid, len, home)
     raw: List[Tuple[int, int, int]] = field(default_factory=list)       # shape: reserved (gslot, qid, l_q)
     prefill: List[Tuple[int, int, int]] = field(default_factory=list)   # shape: prefilled now
@@ -60,6 +64,10 @@ class Planner:
             c = wl.control
             if c.preempt or c.preempt_frac or c.resize:
                 raise ValueError("shape policy: no control events")
+            if wl.governor is not None or any(q.priority for q in wl.queries):
+                # stored K/V re-enter by embedding, which the shaping path does not
+                # have (the oracle Simulator asserts the same)
+                raise ValueError("shape policy: no priorities / governor")
         self.raw = {}                                         # shape: gslot -> prompt length
         self.policy = policy
         self.drained = set()                                  # rtc: finished but resident
@@ -189,6 +197,7 @@ class Planner:
                     stored.append(self._store(g, q, d))
             if self.t in ctl.resize:
                 stored += self._resize(ctl.resize[self.t], d)
+            d.n_pre_compact = len(d.victims)
             gov = self.wl.governor
             if gov is not None:                               # C26
                 for r in range(self.world):
@@ -301,3 +310,38 @@ class Planner:
                 continue
             self.length[g] = e.length
             d.inserts.append((g, e.qid, e.length, e.home))
+
+
+def local_splice_ops(pl, d, rank):
+    """The splice calls rank ``rank`` makes for the decisions ``d`` of planner
+    ``pl``, in execution order (local slot indices):
+
+        ("remove", [b...])            finished rows (+ release; C5) -- every t > 0
+        ("extract", b, qid)           store a victim's K/V
+        ("remove", [b...])            the victims' rows (+ release)
+        ("compact", n_active)         batch shrink/grow (C19)
+        ("extract", b, qid) ... ("remove", [...])   victims chosen after the resize
+        ("insert", [(b, qid, len, home)...])        one batched embed (C7)
+
+    Victims chosen before the compaction (C17 preemption, resize overflow) carry
+    pre-compaction slot indices and are stored before ``compact``; the governor's
+    (C26) and the priority preemption's (C25) are chosen on the compacted batch
+    and are stored after it.  Pure host logic (unit-tested on a host mirror)."""
+    ops = []
+    if d.t > 0:
+        ops.append(("remove", [pl.local(g) for g, _ in d.finished if pl.rank_of(g) == rank]))
+
+    def store(vs):
+        loc = [(pl.local(g), q) for g, q, _ in vs if pl.rank_of(g) == rank]
+        if loc:
+            ops.extend(("extract", b, q) for b, q in loc)
+            ops.append(("remove", [b for b, _ in loc]))
+
+    store(d.victims[:d.n_pre_compact])
+    if d.resize is not None:
+        ops.append(("compact", d.resize))
+    store(d.victims[d.n_pre_compact:])
+    ins = [(pl.local(g), q, n, home) for g, q, n, home in d.inserts if pl.rank_of(g) == rank]
+    if ins:
+        ops.append(("insert", ins))
+    return ops

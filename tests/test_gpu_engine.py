@@ -82,8 +82,10 @@ def test_w1_replay_peaky():
     _replay(w1_workload(scales=SCALES_PEAKY))
 
 
-@pytest.mark.parametrize("seed", list(range(0, 200, 5)))
+@pytest.mark.parametrize("seed", list(range(200)))
 def test_random_stream_replay(seed):
+    """All 200 random event streams of SURVEY §8(c), state checked after every
+    iteration."""
     require_cuda()
     _replay(random_stream(seed))
 
@@ -239,10 +241,11 @@ def test_async_prefill_replay(seed):
     _replay(wl, async_prefill=True, prefill_attention=wl.head_dim == 128, prefill_lookahead=3)
 
 
-@pytest.mark.parametrize("seed", [1, 3, 8])
+@pytest.mark.parametrize("seed", [1, 3, 8, 45, 61, 69, 85, 93])
 def test_policy_stream_replay(seed):
     """§3.3 policies (C25 priority preemption, C26 memory governor): the engine's
-    stores and re-inserts keep the state bit-exact and every output within 1e-2."""
+    stores and re-inserts keep the state bit-exact and every output within 1e-2.
+    Seeds 45-93 store governor / priority victims after a compaction."""
     require_cuda()
     import sys
     import os

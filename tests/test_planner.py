@@ -138,3 +138,78 @@ def test_shape_policy_random_streams(seed):
     wl.max_ctx = 4096
     wl.iterations = -1
     _compare_shape(wl)
+
+
+def _mirror_replay(wl, G):
+    """Apply each rank's splice ops (scheduler.local_splice_ops, the exact call
+    order the engine executes) to a host mirror of the library's slot state and
+    check every call is legal (extract/remove of an occupied slot holding the
+    victim the planner named, insert into an empty slot, no duplicates) and that
+    the mirror ends every iteration equal to the planner's occupancy/lengths."""
+    from paper_2410_18701_b200.scheduler import local_splice_ops
+    pl = Planner(wl, G)
+    B = pl.per_rank
+    occ = [[-1] * B for _ in range(G)]
+    ln = [[0] * B for _ in range(G)]
+    stash = {}
+    while not pl.finished_all():
+        dec = pl.decode_plan() if pl.t > 0 else []
+        for g, q, _ in dec:
+            r, b = pl.rank_of(g), pl.local(g)
+            assert occ[r][b] == q
+            ln[r][b] += 1
+        d = pl.plan()
+        for r in range(G):
+            for op in local_splice_ops(pl, d, r):
+                if op[0] == "remove":
+                    assert len(set(op[1])) == len(op[1]), (d.t, op)
+                    for b in op[1]:
+                        assert occ[r][b] >= 0, (d.t, op)
+                        occ[r][b], ln[r][b] = -1, 0
+                elif op[0] == "extract":
+                    _, b, q = op
+                    assert occ[r][b] == q, (d.t, op, occ[r])      # the victim the planner named
+                    stash[q] = (r, ln[r][b])
+                elif op[0] == "compact":
+                    n = op[1]
+                    for b in range(n, B):
+                        if occ[r][b] >= 0:
+                            f = next(x for x in range(n) if occ[r][x] < 0)
+                            occ[r][f], ln[r][f] = occ[r][b], ln[r][b]
+                            occ[r][b], ln[r][b] = -1, 0
+                else:
+                    for b, q, n, home in op[1]:
+                        assert occ[r][b] < 0, (d.t, op)
+                        if home is not None:
+                            assert stash.pop(q) == (r, n) and home == r   # C20b
+                        occ[r][b], ln[r][b] = q, n
+        assert sum(occ, []) == pl.occupant, d.t
+        assert sum(ln, []) == pl.length, d.t
+    return pl.t
+
+
+@pytest.mark.parametrize("seed", range(100))
+def test_engine_call_order_on_policy_streams(seed):
+    """governor and priority-preemption victims are chosen on the
+    compacted batch, so they must be stored after baton_compact (seeds 45, 61, 69,
+    85, 93 extracted the wrong/empty slot before the fix)."""
+    from test_oracle_policies import _policy_stream
+    wl = _policy_stream(seed)
+    _mirror_replay(wl, wl.gpus)
+
+
+@pytest.mark.parametrize("G", [1, 2, 8])
+def test_engine_call_order_stress(G):
+    wl = config_workload("stress", gpus=G, n_queries=400)
+    wl.iterations = 300
+    _mirror_replay(wl, G)
+
+
+def test_shape_policy_rejects_governor_and_priorities():
+    import dataclasses
+    wl = w1_workload()
+    with pytest.raises(ValueError):
+        Planner(dataclasses.replace(wl, governor=(0.7, 0.5)), 1, policy="shape")
+    qs = [dataclasses.replace(q, priority=1) if q.qid == 3 else q for q in wl.queries]
+    with pytest.raises(ValueError):
+        Planner(dataclasses.replace(wl, queries=qs), 1, policy="shape")
