@@ -73,10 +73,38 @@ __nv_bfloat16 *layer_ptr(void *base, const baton_state *st, int layer) {
     return static_cast<__nv_bfloat16 *>(base) + (size_t)layer * st->layer_elems;
 }
 
+// Transactional host mirror: a mutating call snapshots S/pad/lens/occ after its
+// validation and restores them unless every launch of the call succeeded, so a
+// failing call leaves the host mirror as it was (include/baton.h error contract).
+struct MirrorTxn {
+    baton_state *st;
+    int S;
+    std::vector<int32_t> pad, lens, occ;
+    bool committed = false;
+    explicit MirrorTxn(baton_state *s) : st(s), S(s->S), pad(s->pad), lens(s->lens), occ(s->occ) {}
+    int commit(int r) {
+        committed = r == BATON_OK;
+        return r;
+    }
+    ~MirrorTxn() {
+        if (committed) return;
+        st->S = S;
+        st->pad = pad;
+        st->lens = lens;
+        st->occ = occ;
+    }
+};
+
+// Test-only fault injection (baton_debug_fail_launch): the n-th guarded splice
+// launch from now is refused before it is enqueued, as a failed launch would be.
+thread_local int g_fail_countdown = 0;
+inline bool injected_failure() { return g_fail_countdown > 0 && --g_fail_countdown == 0; }
+#define GUARDED(call) (injected_failure() ? cudaErrorLaunchFailure : (call))
+
 int push_meta(baton_state *st, const std::vector<MaskOp> &ops, cudaStream_t s) {
-    return cuda_status(launch_mask_splice(st->cfg.mask, st->sh.slots, st->sh.max_ctx, ops.data(),
+    return cuda_status(GUARDED(launch_mask_splice(st->cfg.mask, st->sh.slots, st->sh.max_ctx, ops.data(),
                                           (int)ops.size(), st->d_S, st->d_lens, st->d_pad, st->S,
-                                          st->lens.data(), st->pad.data(), s));
+                                          st->lens.data(), st->pad.data(), s)));
 }
 
 }  // namespace
@@ -322,6 +350,7 @@ int baton_shape_step(baton_state *st, int W, int n_new, const int32_t *new_slots
         newlen[b] = new_lens[i];
     }
     if (st->S + W > s.max_ctx) return BATON_E_CAPACITY;
+    MirrorTxn txn(st);
     const int S0 = st->S;
     std::vector<MaskOp> ops;
     std::vector<int32_t> row0(s.slots, -1);
@@ -343,8 +372,8 @@ int baton_shape_step(baton_state *st, int W, int n_new, const int32_t *new_slots
     int r = push_meta(st, ops, cs);
     if (r) return r;
     // the W input tokens' K/V rows (reading C4: the cache grows by W as well)
-    r = cuda_status(launch_shape_append(st->cfg.k_cache, st->cfg.v_cache, k_new, v_new, row0.data(), s.layers,
-                                        s.slots, s.kv_heads, s.head_dim, s.max_ctx, W, cs));
+    r = cuda_status(GUARDED(launch_shape_append(st->cfg.k_cache, st->cfg.v_cache, k_new, v_new, row0.data(), s.layers,
+                                        s.slots, s.kv_heads, s.head_dim, s.max_ctx, W, cs)));
     if (r) return r;
     const size_t qstride = (size_t)s.slots * s.q_heads * W * s.head_dim;
     const float scale = 1.0f / sqrtf((float)s.head_dim);
@@ -355,7 +384,7 @@ int baton_shape_step(baton_state *st, int W, int n_new, const int32_t *new_slots
             s.q_heads, s.kv_heads, s.head_dim, s.max_ctx, st->d_lens, st->d_pad, st->cfg.mask, scale, cs));
         if (r) return r;
     }
-    return BATON_OK;
+    return txn.commit(BATON_OK);
 }
 
 // ---------------------------------------------------------------- a4
@@ -370,6 +399,7 @@ int baton_remove(baton_state *st, const int32_t *slots, int n, int32_t *released
         if (!st->occ[b]) return BATON_E_SLOT_EMPTY;
         seen[b] = 1;
     }
+    MirrorTxn txn(st);
     std::vector<MaskOp> ops;
     for (int i = 0; i < n; ++i) {
         const int b = slots[i];
@@ -388,9 +418,13 @@ int baton_remove(baton_state *st, const int32_t *slots, int n, int32_t *released
             if (st->occ[b]) st->pad[b] -= p;
         st->S -= p;
     }
-    if (released) *released = p;
-    if (ops.empty()) return BATON_OK;   // nothing removed, nothing to release
-    return push_meta(st, ops, as_stream(stream));
+    if (ops.empty()) {   // nothing removed, nothing to release
+        if (released) *released = 0;
+        return txn.commit(BATON_OK);
+    }
+    const int r = txn.commit(push_meta(st, ops, as_stream(stream)));
+    if (released) *released = r == BATON_OK ? p : 0;
+    return r;
 }
 
 // ---------------------------------------------------------------- a5
@@ -411,6 +445,7 @@ int baton_insert_many(baton_state *st, int n, const int32_t *slots, const void *
             return BATON_E_INVALID;
         seen[b] = 1;
     }
+    MirrorTxn txn(st);
     std::vector<MaskOp> ops;
     std::vector<CopyJob> jobs;
     for (int i = 0; i < n; ++i) {
@@ -445,10 +480,10 @@ int baton_insert_many(baton_state *st, int n, const int32_t *slots, const void *
     cudaStream_t cs = as_stream(stream);
     for (size_t i0 = 0; i0 < jobs.size(); i0 += MAX_SPLICE_JOBS) {
         const int nj = (int)std::min(jobs.size() - i0, (size_t)MAX_SPLICE_JOBS);
-        int r = cuda_status(launch_kv_copy(jobs.data() + i0, nj, s.layers, s.kv_heads, s.head_dim, cs));
+        int r = cuda_status(GUARDED(launch_kv_copy(jobs.data() + i0, nj, s.layers, s.kv_heads, s.head_dim, cs)));
         if (r) return r;
     }
-    return push_meta(st, ops, cs);
+    return txn.commit(push_meta(st, ops, cs));
 }
 
 int baton_insert(baton_state *st, int slot, const void *k_pref, const void *v_pref, int len,
@@ -481,7 +516,7 @@ int baton_extract(baton_state *st, int slot, void *k_out, void *v_out, void *str
     j.dst_ls = j.dst_hs * s.kv_heads;
     j.rows = len;
     j.pad_ = 0;
-    return cuda_status(launch_kv_copy(&j, 1, s.layers, s.kv_heads, s.head_dim, as_stream(stream)));
+    return cuda_status(GUARDED(launch_kv_copy(&j, 1, s.layers, s.kv_heads, s.head_dim, as_stream(stream))));
 }
 
 // ---------------------------------------------------------------- a7
@@ -496,6 +531,7 @@ int baton_compact(baton_state *st, int n_active, int32_t *old_to_new, void *stre
         if (b < n_active && !st->occ[b]) ++n_free_lo;
     }
     if (n_occ_hi > n_free_lo) return BATON_E_CAPACITY;
+    MirrorTxn txn(st);
     std::vector<int32_t> src, dst;
     std::vector<CopyJob> jobs;
     std::vector<int32_t> o2n(s.slots);
@@ -525,16 +561,18 @@ int baton_compact(baton_state *st, int n_active, int32_t *old_to_new, void *stre
         st->lens[b] = 0;
         st->pad[b] = 0;
     }
-    if (old_to_new) std::memcpy(old_to_new, o2n.data(), s.slots * 4);
     cudaStream_t cs = as_stream(stream);
     for (size_t i0 = 0; i0 < jobs.size(); i0 += MAX_SPLICE_JOBS) {
         const int nj = (int)std::min(jobs.size() - i0, (size_t)MAX_SPLICE_JOBS);
-        int r = cuda_status(launch_kv_copy(jobs.data() + i0, nj, s.layers, s.kv_heads, s.head_dim, cs));
+        int r = cuda_status(GUARDED(launch_kv_copy(jobs.data() + i0, nj, s.layers, s.kv_heads, s.head_dim, cs)));
         if (r) return r;
     }
-    return cuda_status(launch_mask_move(st->cfg.mask, s.slots, s.max_ctx, src.data(), dst.data(),
-                                        (int)src.size(), st->d_S, st->d_lens, st->d_pad, st->S,
-                                        st->lens.data(), st->pad.data(), cs));
+    const int r = txn.commit(cuda_status(GUARDED(launch_mask_move(st->cfg.mask, s.slots, s.max_ctx, src.data(), dst.data(),
+                                                                  (int)src.size(), st->d_S, st->d_lens, st->d_pad,
+                                                                  st->S, st->lens.data(), st->pad.data(), cs))));
+    // old_to_new is written only when the call succeeded (the mirror rolls back otherwise)
+    if (r == BATON_OK && old_to_new) std::memcpy(old_to_new, o2n.data(), s.slots * 4);
+    return r;
 }
 
 // ---------------------------------------------------------------- a8
@@ -587,6 +625,15 @@ const char *baton_error_string(int code) {
 }
 
 int baton_cuda_error(void) { return g_cuda_error; }
+
+// Test-only (not in include/baton.h): refuse the n-th guarded splice launch
+// (mask splice / mask move / K/V copy / shape append) of this thread from now on
+// (n = 1: the next one; 0 disarms).  Used to check that a failing call leaves the
+// host mirror and the device state unchanged.
+int baton_debug_fail_launch(int n) {
+    g_fail_countdown = n < 0 ? 0 : n;
+    return BATON_OK;
+}
 
 // ---------------------------------------------------------------- harness keygen
 int baton_keygen_tokens(void *out, const int32_t *qids, const int32_t *pos, int layers, int n_slots,

@@ -149,6 +149,40 @@ BATON_DEV uint4 ld_shared_v4(const void *p) {
 // Launch with programmatic stream serialization (PDL): the kernel may start while
 // its predecessor on the stream drains; it calls griddep_wait() before reading
 // the predecessor's results.  Also valid inside stream capture (graph edges).
+// Per-device launch facts.  Function attributes and SM counts are per device, so
+// they are cached per device ordinal (a process may drive several GPUs).
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev < 0 || dev >= kMaxDevices ? 0 : dev;
+}
+inline int device_sms() {
+    static int sms[kMaxDevices] = {};
+    const int dev = current_device();
+    if (!sms[dev]) cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
+    return sms[dev];
+}
+// Raise a kernel's dynamic shared memory limit to `bytes` on the current device,
+// once per (kernel, device) (no-op at <= 48 KB).  Not a stream operation; the
+// launchers call it from their pre-capture dry probes.
+inline cudaError_t ensure_smem_attr_raw(const void *kernel, size_t bytes) {
+    if (bytes <= 48 * 1024) return cudaSuccess;
+    struct Entry { const void *k; int dev; int bytes; };
+    static Entry tab[256];
+    static int n = 0;
+    const int dev = current_device();
+    for (int i = 0; i < n; ++i)
+        if (tab[i].k == kernel && tab[i].dev == dev && tab[i].bytes >= (int)bytes) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess && n < 256) tab[n++] = {kernel, dev, (int)bytes};
+    return e;
+}
+template <typename... KArgs>
+cudaError_t ensure_smem_attr(void (*kernel)(KArgs...), size_t bytes) {
+    return ensure_smem_attr_raw(reinterpret_cast<const void *>(kernel), bytes);
+}
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
                        cudaStream_t s, Args &&...args) {

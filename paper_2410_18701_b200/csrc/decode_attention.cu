@@ -502,19 +502,11 @@ __global__ void __launch_bounds__((CWARPS + 1) * 32, MINB) decode_attention_kern
 
 template <int D, int CW, int ST, int MINB>
 cudaError_t launch_d(const DecodeArgs &a, cudaStream_t s) {
-    static int num_sms = 0;
-    if (!num_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int num_sms = device_sms();
     const size_t smem = sizeof(Smem<D, CW, ST>);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(decode_attention_kernel<D, CW, ST, MINB>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    {
+        cudaError_t e = ensure_smem_attr(decode_attention_kernel<D, CW, ST, MINB>, smem);
         if (e != cudaSuccess) return e;
-        attr_set = true;
     }
     if (a.dry) return cudaSuccess;
     Params p;

@@ -655,12 +655,7 @@ bool gqa_supported(int q_heads, int kv_heads, int head_dim) {
 }
 
 cudaError_t launch_gqa_combine(const DecodeArgs &a, cudaStream_t s) {
-    static int num_sms = 0;
-    if (!num_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int num_sms = device_sms();
     return launch_pdl(decode_combine_kernel, dim3(num_sms), dim3(128), 0, s, a.lens,
                       (const float *)a.partial, static_cast<__nv_bfloat16 *>(a.out), a.slots,
                       a.q_heads, a.max_chunks);
@@ -669,18 +664,11 @@ cudaError_t launch_gqa_combine(const DecodeArgs &a, cudaStream_t s) {
 template <int CW, int KP, int STAGES, int MINB, int RB = 2>
 cudaError_t launch_gqa_v(const DecodeArgs &a, cudaStream_t s) {
     constexpr int TILE = CW * KP, THREADS = (CW + 1) * 32;
-    static int num_sms = 0;
-    if (!num_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int num_sms = device_sms();
     const size_t smem = sizeof(Smem<CW, KP, STAGES, RB>) + 1024;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(decode_gqa_kernel<CW, KP, STAGES, RB, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    {
+        cudaError_t e = ensure_smem_attr(decode_gqa_kernel<CW, KP, STAGES, RB, MINB>, smem);
         if (e != cudaSuccess) return e;
-        attr = true;
     }
     if (a.dry) return cudaSuccess;
     Params p;

@@ -578,18 +578,11 @@ decode_gqa_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_cons
 }  // namespace
 
 cudaError_t launch_decode_gqa_tc(const DecodeArgs &a, cudaStream_t s, bool fused) {
-    static int num_sms = 0;
-    if (!num_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int num_sms = device_sms();
     const size_t smem = sizeof(TSmem) + 1024;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(decode_gqa_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    {
+        cudaError_t e = ensure_smem_attr(decode_gqa_tc_kernel, smem);
         if (e != cudaSuccess) return e;
-        attr = true;
     }
     if (a.dry) return cudaSuccess;
     TParams p;

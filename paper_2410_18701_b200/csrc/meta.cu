@@ -56,41 +56,53 @@ struct MaskSpliceParams {
     MaskOp ops[MAX_MASK_OPS];
 };
 
-// One CTA per mask row; the row is staged in shared memory and the op list is
-// applied in order (each op is a whole-row transform):
+// One CTA per mask row.  The op list is a composition of whole-row transforms
+// applied in order:
 //   ZERO_ROW    P:L105  the finished query's row := 0
 //   SHIFT_LEFT  P:L124  release: column j takes column j+p, tail filled with 0
 //   SHIFT_RIGHT P:L137  left expansion by e: column j takes j-e, front filled with 0
 //   SET_ROW     P:L137  embedded query: 0 on [0, pad), 1 on [pad, S)
+//   SET_CELL    NEXT-1  one column := 1
+// Every output column is resolved on its own by walking the list BACKWARDS: a
+// shift maps the column to its source column (or to the fill 0), a row op of this
+// row fixes the value.  A column that survives every op takes the ORIGINAL row's
+// value at its source column.  So the original row is staged once in shared memory
+// (max_ctx bytes; the launcher opts in above 48 KB) and no per-op pass or barrier
+// is needed.
 __global__ void mask_splice_kernel(const __grid_constant__ MaskSpliceParams p) {
     extern __shared__ uint8_t row_buf[];
-    uint8_t *cur = row_buf;
-    uint8_t *nxt = row_buf + p.max_ctx;
     const int b = blockIdx.x;
     uint8_t *row = p.mask + (size_t)b * p.max_ctx;
-    for (int j = threadIdx.x; j < p.max_ctx; j += blockDim.x) cur[j] = row[j];
+    for (int j = threadIdx.x * 16; j < p.max_ctx; j += blockDim.x * 16)      // max_ctx % 16 == 0
+        *reinterpret_cast<uint4 *>(row_buf + j) = *reinterpret_cast<const uint4 *>(row + j);
     __syncthreads();
-    for (int i = 0; i < p.nops; ++i) {
-        const MaskOp op = p.ops[i];
-        if ((op.kind == MOP_ZERO_ROW || op.kind == MOP_SET_ROW || op.kind == MOP_SET_CELL) && op.slot != b)
-            continue;
-        for (int j = threadIdx.x; j < p.max_ctx; j += blockDim.x) {
-            uint8_t val;
+    for (int j = threadIdx.x; j < p.max_ctx; j += blockDim.x) {
+        int c = j;
+        int val = -1;
+        for (int i = p.nops - 1; i >= 0 && val < 0; --i) {
+            const MaskOp op = p.ops[i];
             switch (op.kind) {
-                case MOP_ZERO_ROW: val = 0; break;
-                case MOP_SHIFT_LEFT: val = (j + op.a < p.max_ctx) ? cur[j + op.a] : 0; break;
-                case MOP_SHIFT_RIGHT: val = (j >= op.a) ? cur[j - op.a] : 0; break;
-                case MOP_SET_CELL: val = (j == op.a) ? 1 : cur[j]; break;
-                default: val = (j >= op.a && j < op.b) ? 1 : 0; break;
+                case MOP_ZERO_ROW:
+                    if (op.slot == b) val = 0;
+                    break;
+                case MOP_SHIFT_LEFT:
+                    c += op.a;
+                    if (c >= p.max_ctx) val = 0;
+                    break;
+                case MOP_SHIFT_RIGHT:
+                    if (c < op.a) val = 0;
+                    else c -= op.a;
+                    break;
+                case MOP_SET_CELL:
+                    if (op.slot == b && c == op.a) val = 1;
+                    break;
+                default:   // MOP_SET_ROW
+                    if (op.slot == b) val = (c >= op.a && c < op.b) ? 1 : 0;
+                    break;
             }
-            nxt[j] = val;
         }
-        __syncthreads();
-        uint8_t *t = cur;
-        cur = nxt;
-        nxt = t;
+        row[j] = (uint8_t)(val < 0 ? row_buf[c] : val);
     }
-    for (int j = threadIdx.x; j < p.max_ctx; j += blockDim.x) row[j] = cur[j];
     if (b == 0) {
         for (int s = threadIdx.x; s < p.slots; s += blockDim.x) {
             p.d_lens[s] = p.lens[s];
@@ -166,7 +178,9 @@ cudaError_t launch_mask_splice(uint8_t *mask, int slots, int max_ctx, const Mask
         p.pad[i] = pad[i];
     }
     for (int i = 0; i < nops; ++i) p.ops[i] = ops[i];
-    mask_splice_kernel<<<slots, 256, 2 * max_ctx, s>>>(p);
+    cudaError_t e = ensure_smem_attr(mask_splice_kernel, (size_t)max_ctx);
+    if (e != cudaSuccess) return e;
+    mask_splice_kernel<<<slots, 256, max_ctx, s>>>(p);
     return cudaGetLastError();
 }
 

@@ -65,6 +65,11 @@ struct __align__(1024) PfSmem {
 
 using namespace tc;
 
+// Debug counter (baton_debug_prefill_rescales): warps that took the lazy-rescale
+// branch (O rows rescaled in TMEM).  One relaxed atomic per such warp-tile; the
+// branch is rare by design (the reference max moves by > rescale_t log2 units).
+__device__ unsigned long long g_pf_rescales = 0;
+
 // packed fp32x2 FMA / add (SASS FFMA2 / FADD2): half the issue slots of the scalar ops
 BATON_DEV float2 ffma2(float2 a, float2 b, float2 c) {
     uint64_t A, B, C, D;
@@ -331,6 +336,7 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
                 // before S(j-1), which this warp group already read: at most one phase behind)
                 mbar_wait(&sm.pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
                 tc_fence_after();
+                if (lane == 0) atomicAdd(&g_pf_rescales, 1ull);
                 {
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
@@ -408,24 +414,30 @@ bool make_map(CUtensorMap *m, const void *base, int heads, int len, int box_rows
 bool prefill_supported(int head_dim) { return head_dim == PF_D; }
 
 namespace {
+float g_rescale_override = -1.f;   // baton_debug_prefill_rescale_t
+// lazy-rescale threshold in log2 units: BATON_PF_RESCALE_T, default 8 (0 = rescale
+// whenever the row max moves)
+float pf_rescale_t() {
+    if (g_rescale_override >= 0.f) return g_rescale_override;
+    static float t = -1.f;
+    if (t < 0.f) {
+        const char *e = getenv("BATON_PF_RESCALE_T");
+        t = e ? (float)atof(e) : 8.f;
+        if (t < 0.f) t = 0.f;
+    }
+    return t;
+}
+
 cudaError_t launch_pf(const CUtensorMap &mq, const CUtensorMap &mk, const CUtensorMap &mv, const PfParams &p,
                       int slots, cudaStream_t s) {
     const size_t smem = sizeof(PfSmem) + 1024;
-    static float rescale_t = -1.f;   // BATON_PF_RESCALE_T (0 = rescale whenever the max moves)
-    if (rescale_t < 0.f) {
-        const char *e = getenv("BATON_PF_RESCALE_T");
-        rescale_t = e ? (float)atof(e) : 8.f;
-        if (rescale_t < 0.f) rescale_t = 0.f;
-    }
     PfParams pp = p;
-    pp.rescale_t = rescale_t;
-    static bool attr[2] = {false, false};
+    pp.rescale_t = pf_rescale_t();
     const bool ext = p.lens != nullptr;
-    if (!attr[ext]) {
-        cudaError_t e = cudaFuncSetAttribute(ext ? prefill_attention_kernel<true> : prefill_attention_kernel<false>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    {
+        cudaError_t e = ext ? ensure_smem_attr(prefill_attention_kernel<true>, smem)
+                            : ensure_smem_attr(prefill_attention_kernel<false>, smem);
         if (e != cudaSuccess) return e;
-        attr[ext] = true;
     }
     if (ext)
         prefill_attention_kernel<true><<<p.n_mtiles * p.Hq * slots, PF_THREADS, smem, s>>>(mq, mk, mv, pp);
@@ -512,3 +524,21 @@ cudaError_t launch_extend_attention(const void *q, const void *k_layer, const vo
 }
 
 }  // namespace baton
+
+// Debug only (not part of include/baton.h).  baton_debug_prefill_rescales: the
+// number of warp-tiles that rescaled O since the last reset (reset != 0 zeroes it;
+// synchronous).  baton_debug_prefill_rescale_t: override the lazy-rescale
+// threshold (log2 units; < 0 restores BATON_PF_RESCALE_T / the default 8).
+extern "C" long long baton_debug_prefill_rescales(int reset) {
+    unsigned long long v = 0;
+    if (cudaMemcpyFromSymbol(&v, baton::g_pf_rescales, sizeof(v)) != cudaSuccess) return -1;
+    if (reset) {
+        const unsigned long long z = 0;
+        if (cudaMemcpyToSymbol(baton::g_pf_rescales, &z, sizeof(z)) != cudaSuccess) return -1;
+    }
+    return (long long)v;
+}
+extern "C" int baton_debug_prefill_rescale_t(float t) {
+    baton::g_rescale_override = t;
+    return 0;
+}
