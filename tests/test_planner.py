@@ -40,7 +40,7 @@ def test_w1():
     assert _compare(w1_workload()) == 19
 
 
-@pytest.mark.parametrize("seed", range(0, 200, 5))
+@pytest.mark.parametrize("seed", range(200))
 def test_random_streams(seed):
     _compare(random_stream(seed))
 
