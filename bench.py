@@ -246,34 +246,37 @@ class Window:
             baton_keygen_tokens(self.k_all[i], dq, dp, L, B, Hkv, D, 1, 0, wl.seed, wl.scales[1])
             baton_keygen_tokens(self.v_all[i], dq, dp, L, B, Hkv, D, 2, 0, wl.seed, wl.scales[2])
         # prefilled K/V of the window's fresh inserts: each query's own keyed history
-        # while they fit in the pool budget; beyond that (13b churn: ~0.9 GB of K/V per
-        # iteration) a ring of already-generated buffers is reused -- the insert moves
-        # the same bytes, the values belong to an earlier query
+        # when they all fit in the pool budget; otherwise (13b churn: ~0.9 GB of K/V
+        # per iteration) a ring of P buffers sized for the window's longest prompt,
+        # buffer i % P serving insert i as a contiguous [L][Hkv][n][D] prefix view: the
+        # insert moves the same bytes, the values are keyed rows of an earlier query
+        # (finite, the same distribution)
         tok_bytes = 2 * L * Hkv * D * 2
         # room for the pool: what is free now, less the engine's K/V cache (allocated by
         # each pass after this) and a 12 GiB margin (warm-start staging, stash, e2e)
         cap = (wl.max_ctx + 15) // 16 * 16
         cache = 2 * L * B * Hkv * cap * D * 2
         budget = min(POOL_BYTES, max(2 << 30, torch.cuda.mem_get_info(dev)[0] - cache - (12 << 30)))
-        self.pref, pool, used = {}, [], 0
+        self.pref = {}
         self.pool_reused = 0
-        for q, n, _ in self.fresh:
-            if used + n * tok_bytes <= budget:
-                Kp = torch.empty((L, Hkv, n, D), dtype=torch.bfloat16, device=dev)
-                Vp = torch.empty_like(Kp)
-                baton_keygen_history(Kp, L, Hkv, D, q, 0, n, 1, wl.seed, wl.scales[1])
-                baton_keygen_history(Vp, L, Hkv, D, q, 0, n, 2, wl.seed, wl.scales[2])
-                used += n * tok_bytes
-                self.pref[q] = (Kp, Vp)
-                pool.append((Kp, Vp))
-                continue
-            i = next((i for i, (a, _) in enumerate(pool) if a.shape[2] >= n), None)
-            if i is None:
-                raise SystemExit("prefilled K/V pool: no buffer long enough")
-            src = pool.pop(i)
-            pool.append(src)                              # least recently used first
-            self.pref[q] = tuple(t.view(-1)[:L * Hkv * n * D].view(L, Hkv, n, D) for t in src)
-            self.pool_reused += 1
+
+        def hist(q, n):
+            Kp = torch.empty((L, Hkv, n, D), dtype=torch.bfloat16, device=dev)
+            Vp = torch.empty_like(Kp)
+            baton_keygen_history(Kp, L, Hkv, D, q, 0, n, 1, wl.seed, wl.scales[1])
+            baton_keygen_history(Vp, L, Hkv, D, q, 0, n, 2, wl.seed, wl.scales[2])
+            return Kp, Vp
+
+        if sum(n for _, n, _ in self.fresh) * tok_bytes <= budget:
+            for q, n, _ in self.fresh:
+                self.pref[q] = hist(q, n)
+        elif self.fresh:
+            nmax = max(n for _, n, _ in self.fresh)
+            P = int(max(1, min(len(self.fresh), budget // (nmax * tok_bytes))))
+            ring = [hist(q, nmax) for q, _, _ in self.fresh[:P]]
+            for i, (q, n, _) in enumerate(self.fresh):
+                self.pref[q] = tuple(t.view(-1)[:L * Hkv * n * D].view(L, Hkv, n, D) for t in ring[i % P])
+            self.pool_reused = max(0, len(self.fresh) - P)
         torch.cuda.synchronize()
 
     def token_dev(self, t, dec):
@@ -342,7 +345,7 @@ class Ctx:
             del kv
         for e in pl.queue:
             if e.home == rank:
-                eng.stash[e.qid] = hist(e.qid, e.length)
+                eng.stash.put(e.qid, *hist(e.qid, e.length))
         torch.cuda.synchronize()
         return eng
 
@@ -652,15 +655,14 @@ def run_full(ctx):
     return out
 
 
-def run_prefill(ctx, win):
-    """a8: the window's inserted prompts through the tcgen05 prefill (P&D decouples it
-    from the decode loop): one varlen launch per layer over them; all
-    layers cost the same, so one layer is graph-timed.  Beside `value`, not in it."""
+def run_prefill(ctx, plens):
+    """a8: the windows' inserted prompts (the first 64) through the tcgen05 prefill (P&D
+    decouples it from the decode loop): one varlen launch per layer over
+    them; all layers cost the same, so one layer is graph-timed.  Beside `value`."""
     import torch
     from paper_2410_18701_b200.baton import baton_prefill_attention_varlen
     wl, dev = ctx.wl, ctx.dev
     Hq, Hkv, D = wl.q_heads, wl.kv_heads, wl.head_dim
-    plens = [n for _, n, _ in win.fresh][:64]
     T = sum(plens)
     g = torch.Generator(device=dev).manual_seed(18701)
     qp = torch.randn((Hq, T, D), device=dev, generator=g).to(torch.bfloat16)
@@ -688,8 +690,8 @@ def run_prefill(ctx, win):
     flop = sum(4.0 * Hq * D * n * (n + 1) / 2 for n in plens)
     pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
     bf16_peak = json.load(open(pk))["bf16_tflops"] if os.path.exists(pk) else 2250.0
-    out = {"what": "baton_prefill_attention_varlen (tcgen05) over the median window's inserted "
-                   "prompts, one layer, graph-timed", "prompts": len(plens), "tokens": T,
+    out = {"what": "baton_prefill_attention_varlen (tcgen05) over the windows' inserted "
+                   "prompts (first 64), one layer, graph-timed", "prompts": len(plens), "tokens": T,
            "us_per_layer": us, "tflops": flop / us / 1e6, "peak_tflops": bf16_peak,
            "peak_source": "measured" if os.path.exists(pk) else "nominal",
            "frac": flop / us / 1e6 / bf16_peak}
@@ -706,21 +708,16 @@ def run_baton(args, rank, world, local_rank):
     clocks.start()
     time.sleep(0.3)
     wins = []
-    prefill_fresh = None
     for t0 in starts:
         win = Window(ctx, t0)
         wins.append(run_window(ctx, win, clocks))
-        wins[-1]["fresh"] = [(n, t) for _, n, t in win.fresh]
-        if t0 == starts[len(starts) // 2] and rank == 0 and win.fresh:
-            prefill_fresh = win
-        else:
-            win.free()
+        wins[-1]["fresh"] = [n for _, n, _ in win.fresh]
+        win.free()
         _release(win)
     clk = clocks.stop()
     full_run = run_full(ctx) if (world == 1 and not args.no_full_run) else None
-    prefill = run_prefill(ctx, prefill_fresh) if prefill_fresh is not None else None
-    if prefill_fresh is not None:
-        prefill_fresh.free()
+    plens = sum((w["fresh"] for w in wins), [])[:64]
+    prefill = run_prefill(ctx, plens) if (rank == 0 and plens) else None
     return dict(wins=wins, steady=steady, clocks=clk, full_run=full_run, prefill=prefill,
                 scaling=ctx.scaling, wl=ctx.wl)
 
@@ -886,7 +883,9 @@ def summarize(args, r, world, red):
                      "live_slots_per_step_rank0": w["tokens"] / args.steps,
                      "inserts": w["inserted"], "stored": w["stored"],
                      "attn_frac": (w["attn_bytes"] / w["attn_time_s"] / 1e9 / peak) if w["attn_time_s"] else None,
-                     **({"e2e": w["e2e_all"] / (w["e2e_ms_max"] / 1e3)} if "e2e" in w else {})}
+                     **({"e2e": w["e2e_all"] / (w["e2e_ms_max"] / 1e3),
+                         "e2e_step_ms_p50_max": [statistics.median(w["e2e"]["step_ms"]),
+                                                 max(w["e2e"]["step_ms"])]} if "e2e" in w else {})}
                     for i, w in enumerate(wins)],
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
@@ -928,12 +927,12 @@ def summarize(args, r, world, red):
     if r.get("full_run"):
         line["full_run"] = r["full_run"]
     if world == 1 and not args.no_cpu_baseline:
-        t0 = wm["t0"]
+        t0 = wins[len(wins) // 2]["t0"]         # the middle window's start, as --impl reference
         t_step, m, Lw, n, live, mlen = oracle_sample(args.config, t0, n_slots=8, budget_s=15.0)
         cb = {"value": m / (Lw * t_step), "unit": "tokens/s", "cores": 1, "kind": "oracle",
               "cpu_model": _cpu_model(),
               "sample": f"O-2 Shard.step (fp64 NumPy, 1 thread), 1 of {Lw} layers x {m} of {live} live "
-                        f"slots (length quantiles, mean {mlen:.0f}) at iteration {t0} (the median "
+                        f"slots (length quantiles, mean {mlen:.0f}) at iteration {t0} (the middle "
                         f"window's start), {n} steps, tokens/s = {m} / ({Lw} x step time) -- the same "
                         f"sample as --impl reference"}
         if not args.no_all_cores:

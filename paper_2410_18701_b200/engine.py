@@ -24,6 +24,7 @@ import torch
 from .baton import (BatonShard, baton_keygen_tokens, baton_keygen_history, baton_prefill_attention,
                     baton_prefill_attention_varlen)
 from .comm import gather_completion_flags
+from .kvstore import HybridKVStore
 from .scheduler import Planner, local_splice_ops
 
 KIND_Q, KIND_K, KIND_V = 0, 1, 2
@@ -47,19 +48,28 @@ class StepStats:
     prefill_rows: int = 0       # shape policy: prompt tokens prefilled in the batch
     bubble_rows: int = 0        # shape policy: padding input tokens computed
     S: int = 0                  # shared logical length after the iteration (host mirror)
+    completed: int = 0          # queries whose last token was decoded in this iteration
+    live_slots: int = 0         # occupied slots after the iteration
+    kv_live_rows: int = 0       # sum of lens over occupied slots after the iteration
 
 
 class Engine:
     def __init__(self, wl, rank=0, world=1, device=None, group=None, keep_outputs=False,
                  keep_layers=None, token_source=None, prefill_source=None, use_graph=True,
                  stash_host=False, policy="baton", prefill_attention=False, async_prefill=False,
-                 prefill_lookahead=None):
+                 prefill_lookahead=None, prefill_grouping=None, trace=False,
+                 stash_hbm_bytes=None, pins=None):
+        """prefill_grouping: "length" -- a8 of several fresh prompts runs in batches of
+        similar length, one varlen launch each (the PD method's prefill, P:L220;
+        default for policy "pd"); None -- batched only when the prompts are short.
+        trace: record a CUDA event after every iteration (per-iteration device time
+        for the JSONL log, ``write_log``)."""
         self.wl = wl
         self.rank = rank
         self.world = world
         self.group = group
         self.device = torch.device(device or "cuda")
-        self.planner = Planner(wl, world, policy=policy)
+        self.planner = Planner(wl, world, policy=policy, pins=pins)
         self.B = self.planner.per_rank
         # libbaton requires max_ctx % 16 == 0 (16-B aligned mask rows for the bulk
         # copies); a larger capacity changes no result (C24 caps l_q + A anyway)
@@ -73,7 +83,6 @@ class Engine:
         self.out = torch.zeros((L, B, wl.q_heads, D), dtype=torch.bfloat16, device=self.device)
         self.d_qid = torch.full((B,), -1, dtype=torch.int32, device=self.device)
         self.d_pos = torch.zeros((B,), dtype=torch.int32, device=self.device)
-        self.stash: Dict[int, Tuple[torch.Tensor, torch.Tensor]] = {}
         self.keep_outputs = keep_outputs
         self.keep_layers = keep_layers
         self.outputs: Dict[Tuple[int, int], np.ndarray] = {}
@@ -95,8 +104,19 @@ class Engine:
         self.staging = {(self.q.data_ptr(), self.k_new.data_ptr(), self.v_new.data_ptr())}
         # P:L147 "moved to the host memory": stored K/V in pinned host memory (the
         # extract/insert copy kernels read/write it over PCIe), else an HBM stash
+        # P:L144/P:L147/P:L335: stored K/V in HBM (stash_host=False), in pinned host
+        # memory (True: extract/insert copy kernels write/read it over PCIe), or the
+        # prefetchable hybrid ("hybrid": HBM up to stash_hbm_bytes, then host; host
+        # entries near the queue head prefetched back to HBM ahead of re-insert)
         self.stash_host = stash_host
+        hybrid = stash_host == "hybrid"
+        self.stash = HybridKVStore(self.shard, self.device,
+                                   hbm_budget=stash_hbm_bytes if hybrid else (0 if stash_host else None),
+                                   host=bool(stash_host), prefetch=hybrid)
         self.last_decisions = None
+        self.prefill_grouping = prefill_grouping or ("length" if policy == "pd" else None)
+        self.trace = trace
+        self.trace_events = []
 
     def register_staging(self, q, k, v):
         """Declare a fixed (q, k_new, v_new) buffer set a token source may return
@@ -135,60 +155,13 @@ class Engine:
         return K, V
 
     def _prefill_attn(self, qid, n, K, V):
-        """a8 over every layer of a fresh query's prompt (output discarded)."""
-        wl = self.wl
-        Q = torch.empty((wl.layers, wl.q_heads, n, wl.head_dim), dtype=torch.bfloat16, device=self.device)
-        baton_keygen_history(Q, wl.layers, wl.q_heads, wl.head_dim, qid, 0, n, KIND_Q, wl.seed,
-                             wl.scales[0])
-        O = torch.empty_like(Q)
-        for l in range(wl.layers):
-            baton_prefill_attention(Q[l], K[l], V[l], O[l], n, wl.q_heads, wl.kv_heads, wl.head_dim)
+        prefill_attention_one(self.wl, self.device, qid, n, K, V)
 
-    @staticmethod
-    def _batchable(items):
-        return len(items) > 1 and sum(n for _, n, _, _ in items) <= PREFILL_BATCH_MEAN * len(items)
+    def _batchable(self, items):
+        return batchable(items, self.prefill_grouping)
 
     def _prefill_attn_batch(self, items):
-        """a8 for several fresh queries at once (output discarded): per layer ONE
-        baton_prefill_attention_varlen launch over their prompts packed along the token
-        axis (NEXT-2).  The packed q/k/v come from the same keyed generator as the
-        per-query prefill (identical values), written straight into the packed layout."""
-        # Batching pays where launches dominate (short prompts: 3x for eight 30-200-token
-        # prompts, scripts/probes/prefill_batch_probe.py).  Long prompts keep one
-        # launch per query and layer: packing them would regenerate their K/V (the
-        # keyed generator runs at ~250 GB/s), which costs more than the launches saved.
-        if not self._batchable(items):
-            for it in items:
-                self._prefill_attn(*it)
-            return
-        wl = self.wl
-        L, D = wl.layers, wl.head_dim
-        groups, cur, tiles = [], [], 0          # launch limits: 64 prompts, 1024 query tiles
-        for it in items:
-            t = -(-it[1] // 128)
-            if cur and (len(cur) == 64 or tiles + t > 1024):
-                groups.append(cur)
-                cur, tiles = [], 0
-            cur.append(it)
-            tiles += t
-        groups.append(cur)
-        for grp in groups:
-            T = sum(n for _, n, _, _ in grp)
-            bufs = {}
-            for kind, H, sc in ((KIND_Q, wl.q_heads, wl.scales[0]), (KIND_K, wl.kv_heads, wl.scales[1]),
-                                (KIND_V, wl.kv_heads, wl.scales[2])):
-                t = torch.empty((L, H, T, D), dtype=torch.bfloat16, device=self.device)
-                s0 = 0
-                for qid, n, _, _ in grp:
-                    baton_keygen_history(t[:, :, s0:], L, H, D, qid, 0, n, kind, wl.seed, sc,
-                                         head_stride=T * D, layer_stride=H * T * D)
-                    s0 += n
-                bufs[kind] = t
-            O = torch.empty_like(bufs[KIND_Q])
-            lens = [n for _, n, _, _ in grp]
-            for l in range(L):
-                baton_prefill_attention_varlen(bufs[KIND_Q][l], bufs[KIND_K][l], bufs[KIND_V][l], O[l], lens,
-                                               wl.q_heads, wl.kv_heads, D)
+        prefill_attention_batch(self.wl, self.device, items, self.prefill_grouping)
 
     # ---------------------------------------------------------------- one iteration
     def done(self):
@@ -243,6 +216,10 @@ class Engine:
         return dec
 
     def decode(self, stats):
+        with torch.cuda.nvtx.range("baton.decode"):
+            return self._decode(stats)
+
+    def _decode(self, stats):
         """a1 + per layer a2/a3 for the slots the planner says are live."""
         pl = self.planner
         dec = [(pl.local(g), q, p) for g, q, p in pl.decode_plan() if pl.rank_of(g) == self.rank]
@@ -297,9 +274,28 @@ class Engine:
             self.decode(stats)
             local = pl.local_completion_flags(self.rank)
             # completion flags + occupancy summary of every rank
-            flags = self._gather_flags(local) if self.world > 1 else None
+            if self.world > 1:
+                with torch.cuda.nvtx.range("baton.allgather"):
+                    flags = self._gather_flags(local)
         d = pl.plan(flags)
         self.last_decisions = d
+        stats.completed = sum(1 for g, _ in d.completed if pl.rank_of(g) == self.rank)
+        with torch.cuda.nvtx.range("baton.splice"):
+            self._splice(d, stats)
+        if self.async_prefill:
+            self._prefetch()
+        stats.S = self.shard.S
+        mine = [(g, q) for g, q in pl.live() if pl.rank_of(g) == self.rank]
+        stats.live_slots = len(mine)
+        stats.kv_live_rows = sum(pl.length[g] for g, _ in mine)
+        if self.trace:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            self.trace_events.append(ev)
+        return stats
+
+    def _splice(self, d, stats):
+        pl = self.planner
         sh = self.shard
         ops = local_splice_ops(pl, d, self.rank)
         ins = []
@@ -315,15 +311,7 @@ class Engine:
                     stats.stored += len(op[1])
             elif kind == "extract":
                 _, b, q = op
-                n = int(sh.baton_query()["lens"][b])       # the library's live length
-                if self.stash_host:
-                    shape = (self.wl.layers, self.wl.kv_heads, n, self.wl.head_dim)
-                    ko = torch.empty(shape, dtype=torch.bfloat16, pin_memory=True)
-                    vo = torch.empty(shape, dtype=torch.bfloat16, pin_memory=True)
-                    self.stash[q] = sh.baton_extract(b, ko, vo)
-                else:
-                    self.stash[q] = sh.baton_extract(b)
-                stats.extract_rows += n
+                stats.extract_rows += self.stash.store(b, q)     # the library's live length
             elif kind == "compact":
                 before = sh.baton_query()
                 o2n = sh.baton_compact(op[1])
@@ -335,7 +323,7 @@ class Engine:
             fresh = []                          # synchronous P&D: one batched a8 below
             for b, q, n, home in ins:
                 if home is not None:
-                    K, V = self.stash.pop(q)
+                    K, V = self.stash.take(q)
                 elif q in self.prefetched:
                     K, V, ev = self.prefetched.pop(q)
                     torch.cuda.current_stream(self.device).wait_event(ev)
@@ -353,12 +341,14 @@ class Engine:
             if fresh:
                 self._prefill_attn_batch(fresh)
             sh.baton_insert_many(slots, ks, vs, lens)
+            self.stash.after_insert()
             stats.inserted = len(ins)
             stats.insert_rows = sum(lens)
-        if self.async_prefill:
-            self._prefetch()
-        stats.S = sh.S
-        return stats
+        if len(self.stash):
+            # hybrid store: start the H2D of host-resident stored queries that come
+            # up next in the queue's service order (this rank's only, C20b)
+            self.stash.prefetch([pl.queue[i].qid for i in pl._order()
+                                 if pl.queue[i].home == self.rank])
 
     def _prefetch(self):
         """Launch the prefill of the next queued fresh queries on the side stream."""
@@ -387,8 +377,117 @@ class Engine:
 
     def run(self, max_iters=None):
         all_stats = []
+        if self.trace:
+            self.trace_start = torch.cuda.Event(enable_timing=True)
+            self.trace_start.record()
+            self.trace_events = []
         while not self.done():
             all_stats.append(self.iteration())
             if max_iters is not None and len(all_stats) >= max_iters:
                 break
         return all_stats
+
+    def log_records(self, stats):
+        """Per-iteration records (SURVEY.md §5 metrics log; the Fig. 6-8 traces of
+        P:L299-309): live slots, S, sum of live lengths, K/V bytes moved by the
+        splice, decoded / idle / completed counts and, when traced, the device time
+        at the end of the iteration.  Synchronises when traced."""
+        wl = self.wl
+        tau_l = 2 * wl.kv_heads * wl.head_dim * 2 * wl.layers      # K+V bytes per token, all layers
+        t_ms = None
+        if self.trace and self.trace_events:
+            torch.cuda.synchronize(self.device)
+            t_ms = [self.trace_start.elapsed_time(e) for e in self.trace_events[-len(stats):]]
+        recs = []
+        for i, s in enumerate(stats):
+            r = {"t": s.t, "decoded": s.decoded, "idle": s.idle, "completed": s.completed,
+                 "inserted": s.inserted, "removed": s.removed, "stored": s.stored,
+                 "live_slots": s.live_slots, "S": s.S, "kv_live_rows": s.kv_live_rows,
+                 "kv_live_bytes": s.kv_live_rows * tau_l,
+                 "kv_dense_bytes": self.B * s.S * tau_l,   # the paper's dense [B][S] tensors
+                 "live_rows_read": s.live_rows,
+                 "splice_bytes": 2 * (s.insert_rows + s.extract_rows + s.compact_rows) * tau_l,
+                 "width": s.width, "prefill_rows": s.prefill_rows, "bubble_rows": s.bubble_rows}
+            if t_ms is not None:
+                r["t_ms"] = t_ms[i]
+            recs.append(r)
+        return recs
+
+    def write_log(self, path, stats):
+        """The per-iteration records as JSON lines."""
+        import json
+        with open(path, "w") as f:
+            for r in self.log_records(stats):
+                f.write(json.dumps(r) + "\n")
+
+
+def prefill_groups(items, by_length=False, ratio=1.25, max_prompts=64, max_tiles=1024):
+    """Split fresh prompts (qid, n, ...) into varlen prefill launches (at most 64
+    prompts and 1024 query tiles each).  by_length: the PD method's grouping
+    (P:L220 "queries with similar sequence lengths will be grouped into a batch";
+    P:L335 "the similarity of length principle") -- sorted by length, a new group
+    whenever a prompt exceeds the group's shortest by more than `ratio`."""
+    order = sorted(items, key=lambda it: it[1]) if by_length else list(items)
+    groups, cur, tiles = [], [], 0
+    for it in order:
+        t = -(-it[1] // 128)
+        if cur and (len(cur) == max_prompts or tiles + t > max_tiles
+                    or (by_length and it[1] > ratio * cur[0][1])):
+            groups.append(cur)
+            cur, tiles = [], 0
+        cur.append(it)
+        tiles += t
+    if cur:
+        groups.append(cur)
+    return groups
+
+
+def prefill_attention_one(wl, device, qid, n, K, V):
+    """a8 over every layer of a fresh query's prompt (output discarded): q from the
+    keyed generator (the model's projection stand-in), K/V the query's prefilled K/V."""
+    Q = torch.empty((wl.layers, wl.q_heads, n, wl.head_dim), dtype=torch.bfloat16, device=device)
+    baton_keygen_history(Q, wl.layers, wl.q_heads, wl.head_dim, qid, 0, n, KIND_Q, wl.seed,
+                         wl.scales[0])
+    O = torch.empty_like(Q)
+    for l in range(wl.layers):
+        baton_prefill_attention(Q[l], K[l], V[l], O[l], n, wl.q_heads, wl.kv_heads, wl.head_dim)
+
+
+def batchable(items, grouping=None):
+    if grouping == "length":
+        return len(items) > 1
+    return len(items) > 1 and sum(it[1] for it in items) <= PREFILL_BATCH_MEAN * len(items)
+
+
+def prefill_attention_batch(wl, device, items, grouping=None):
+    """a8 for several fresh queries (qid, n, K, V) at once (output discarded): per
+    layer ONE baton_prefill_attention_varlen launch per group of prompts packed along
+    the token axis (NEXT-2; grouping "length": the PD method's similar-length groups).
+    The packed q/k/v come from the same keyed generator as the per-query prefill
+    (identical values), written straight into the packed layout."""
+    # Batching pays where launches dominate (short prompts: 3x for eight 30-200-token
+    # prompts, scripts/probes/prefill_batch_probe.py).  Without length grouping, long
+    # prompts keep one launch per query and layer: packing them regenerates their K/V
+    # (the keyed generator runs at ~250 GB/s), which costs more than the launches saved.
+    if not batchable(items, grouping):
+        for it in items:
+            prefill_attention_one(wl, device, *it)
+        return
+    L, D = wl.layers, wl.head_dim
+    for grp in prefill_groups(items, by_length=grouping == "length"):
+        T = sum(n for _, n, _, _ in grp)
+        bufs = {}
+        for kind, H, sc in ((KIND_Q, wl.q_heads, wl.scales[0]), (KIND_K, wl.kv_heads, wl.scales[1]),
+                            (KIND_V, wl.kv_heads, wl.scales[2])):
+            t = torch.empty((L, H, T, D), dtype=torch.bfloat16, device=device)
+            s0 = 0
+            for qid, n, _, _ in grp:
+                baton_keygen_history(t[:, :, s0:], L, H, D, qid, 0, n, kind, wl.seed, sc,
+                                     head_stride=T * D, layer_stride=H * T * D)
+                s0 += n
+            bufs[kind] = t
+        O = torch.empty_like(bufs[KIND_Q])
+        lens = [n for _, n, _, _ in grp]
+        for l in range(L):
+            baton_prefill_attention_varlen(bufs[KIND_Q][l], bufs[KIND_K][l], bufs[KIND_V][l], O[l], lens,
+                                           wl.q_heads, wl.kv_heads, D)

@@ -30,6 +30,11 @@ class QueueEntry:
     qid: int
     length: int                 # prefilled / stored K/V length
     home: Optional[int] = None  # rank holding stored K/V (None = fresh query)
+    pin: Optional[int] = None   # fresh query prefilled remotely: the rank its K/V went to (C20c)
+
+    def rank(self):
+        """The only rank this entry may enter (None: any)."""
+        return self.home if self.home is not None else self.pin
 
 
 @dataclass
@@ -46,10 +51,11 @@ class Decisions:
     inserts: List[Tuple[int, int, int, Optional[int]]] = field(default_factory=list)  # (gslot, qid, len, home)
     raw: List[Tuple[int, int, int]] = field(default_factory=list)       # shape: reserved (gslot, qid, l_q)
     prefill: List[Tuple[int, int, int]] = field(default_factory=list)   # shape: prefilled now
+    completed: List[Tuple[int, int]] = field(default_factory=list)  # (gslot, qid): last token just decoded
 
 
 class Planner:
-    def __init__(self, wl, world=1, policy="baton"):
+    def __init__(self, wl, world=1, policy="baton", pins=None):
         """policy "baton": relay race (remove on completion, insert at once);
         "rtc": the paper's run-to-completion Benchmark -- a finished query
         keeps its slot and keeps decoding (idle EOS tokens) until every query of
@@ -57,9 +63,26 @@ class Planner:
         "shape": relay race WITHOUT P&D (vector shaping, NEXT-1) -- a
         new query takes its slot raw and is prefilled inside the batch in the
         next iteration (baton_shape_step), whose input width is the longest such
-        prompt; its A decode iterations follow.  No control events."""
-        if policy not in ("baton", "rtc", "shape"):
+        prompt; its A decode iterations follow.  No control events.
+        The paper's two comparison methods (NEXT-4), on the same kernels:
+        "benchmark": the transformers batch-wise strategy -- run-to-completion, and
+        the batch's prompts are prefilled together inside the batch, left-padded to
+        the longest (a shaped iteration in which every row is new);
+        "pd": P&D decoupling without the relay race -- run-to-completion decode
+        batches of randomly combined (FCFS) queries whose prompts were prefilled
+        separately in batches of similar length (the engine groups them).
+        pins: {qid: rank} for fresh queries prefilled on a separate prefill rank and
+        handed to that decode rank (NEXT-2, handoff.py): such a query may only take a
+        slot of its rank (reading C20c, the fresh-query analogue of C20b)."""
+        if policy not in ("baton", "rtc", "shape", "benchmark", "pd"):
             raise ValueError(policy)
+        self.rtc = policy in ("rtc", "benchmark", "pd")       # run-to-completion batches
+        self.raw_insert = policy in ("shape", "benchmark")     # prefilled inside the batch
+        if self.raw_insert or self.rtc:
+            c = wl.control
+            if policy != "shape" and (c.preempt or c.preempt_frac or c.resize or wl.governor is not None
+                                      or any(q.priority for q in wl.queries)):
+                raise ValueError(f"{policy} policy: no control events / priorities / governor")
         if policy == "shape":
             c = wl.control
             if c.preempt or c.preempt_frac or c.resize:
@@ -68,6 +91,7 @@ class Planner:
                 # stored K/V re-enter by embedding, which the shaping path does not
                 # have (the oracle Simulator asserts the same)
                 raise ValueError("shape policy: no priorities / governor")
+        self.pins = dict(pins or {})
         self.raw = {}                                         # shape: gslot -> prompt length
         self.policy = policy
         self.drained = set()                                  # rtc: finished but resident
@@ -174,7 +198,8 @@ class Planner:
                     self.done_tokens[q] >= self.meta[q].A)
                 if done:
                     d.finished.append((g, q))
-            if self.policy == "rtc":
+            d.completed = [(g, q) for g, q in d.finished if q not in self.drained]
+            if self.rtc:
                 self.drained.update(q for _, q in d.finished)
                 if any(q not in self.drained for _, q in self.live()):
                     d.finished = []                           # the batch runs on
@@ -257,7 +282,7 @@ class Planner:
                and self.pending[self.next_arrival].arrival <= self.t):
             q = self.pending[self.next_arrival]
             self.ticket[q.qid] = len(self.ticket) + 1
-            self.queue.append(QueueEntry(q.qid, q.l_q, None))
+            self.queue.append(QueueEntry(q.qid, q.l_q, None, self.pins.get(q.qid)))
             self.next_arrival += 1
 
     def _priority_preempt(self, d):
@@ -267,11 +292,11 @@ class Planner:
         if not self.queue:
             return
         e0 = self.queue[self._order()[0]]
-        if any((e0.home is None or self.rank_of(g) == e0.home) and self._admissible(self.rank_of(g), e0.length)
+        if any((e0.rank() is None or self.rank_of(g) == e0.rank()) and self._admissible(self.rank_of(g), e0.length)
                for g in self._free()):
             return
         live = [(g, q) for g, q in self.live()
-                if (e0.home is None or self.rank_of(g) == e0.home) and self.local(g) < self.active
+                if (e0.rank() is None or self.rank_of(g) == e0.rank()) and self.local(g) < self.active
                 and self.prio[q] < self.prio[e0.qid]]
         if not live:
             return
@@ -279,7 +304,7 @@ class Planner:
         self._requeue([self._store(g, q, d)])
 
     def _fill(self, d):
-        if self.policy == "rtc" and self.live():
+        if self.rtc and self.live():
             return                                            # batch still running
         if self.t > 0 and self.policy == "baton":
             self._priority_preempt(d)
@@ -291,7 +316,7 @@ class Planner:
             for idx in self._order():
                 e = self.queue[idx]
                 for g in free:
-                    if (e.home is None or self.rank_of(g) == e.home) and self._admissible(self.rank_of(g), e.length):
+                    if (e.rank() is None or self.rank_of(g) == e.rank()) and self._admissible(self.rank_of(g), e.length):
                         chosen = (idx, g)
                         break
                 if chosen:
@@ -303,7 +328,7 @@ class Planner:
             del self.queue[idx]
             self.occupant[g] = e.qid
             self.entered[e.qid] = self.t
-            if self.policy == "shape":                        # raw: prefilled next iteration
+            if self.raw_insert:                               # raw: prefilled next iteration
                 self.length[g] = 0
                 self.raw[g] = e.length
                 d.raw.append((g, e.qid, e.length))

@@ -96,6 +96,54 @@ def test_run_to_completion_policy():
     assert base.t < pl.t            # the relay race finishes the same work sooner
 
 
+@pytest.mark.parametrize("policy", ["benchmark", "pd"])
+def test_paper_baseline_policies(policy):
+    """NEXT-4, the paper's two comparison methods as planner policies.
+    Both run decode batches to completion (P:L65) and only refill an empty batch;
+    "benchmark" places the batch's queries raw (prefilled together inside the batch,
+    padded to the longest prompt: one shaped iteration with every row new), "pd"
+    embeds separately prefilled queries (the same decisions as "rtc").  Every query
+    yields exactly its A tokens and is reported complete exactly once (a
+    response returns as soon as it is done)."""
+    from baton_inputs import Workload, Query
+    A = [10, 2, 3, 9, 2, 4, 8, 1, 2]
+    qs = [Query(i, 0, 5 + i, A[i]) for i in range(9)]
+    wl = Workload("rtc", qs, layers=1, q_heads=2, kv_heads=2, head_dim=16, slots=3, max_ctx=64)
+    pl, ref = Planner(wl, 1, policy=policy), Planner(wl, 1, policy="rtc")
+    useful, completed, shaped = 0, [], []
+    while not pl.finished_all():
+        d = pl.plan()
+        useful += len(d.decode) - pl.idle_decodes(d.decode)
+        completed += [q for _, q in d.completed]
+        if d.prefill:
+            shaped.append(sorted(q for _, q, _ in d.prefill))
+            assert not d.decode                    # every row of the batch is new
+        if policy == "pd":
+            r = ref.plan()
+            assert (d.decode, d.finished, d.inserts) == (r.decode, r.finished, r.inserts)
+        else:
+            assert not d.inserts
+            if d.raw:
+                assert len(pl.live()) == len(d.raw)  # only into an empty batch
+    assert useful == sum(A) and sorted(completed) == list(range(9))
+    if policy == "benchmark":
+        assert shaped == [[0, 1, 2], [3, 4, 5], [6, 7, 8]]
+    with pytest.raises(ValueError):
+        w2 = random_stream(3)                      # preemption events: relay race only
+        Planner(w2, 1, policy=policy)
+
+
+def test_completed_once_per_query_relay():
+    wl = random_stream(5)
+    pl = Planner(wl, 1)
+    done = []
+    while not pl.finished_all():
+        d = pl.plan()
+        done += [q for _, q in d.completed]
+    assert len(done) == len(set(done))
+    assert set(done) <= {q.qid for q in wl.queries}
+
+
 def _compare_shape(wl, G=None):
     """Planner policy "shape" (product) == Simulator policy "shape" (oracle)."""
     G = G or wl.gpus
