@@ -1,11 +1,15 @@
 """Build libbaton.so in-tree with nvcc for sm_100a (no JIT, no torch extension).
 
-    python -m paper_2410_18701_b200.build [--verbose]
+    python -m paper_2410_18701_b200.build [--verbose] [--force] [--experiments]
 
 Compiles every csrc/*.cu with
     -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo
 and links them (static cudart) into paper_2410_18701_b200/libbaton.so, which the
-ctypes binding (_lib.py) loads.  Rebuilds only when a source or header is newer.
+ctypes binding (_lib.py) loads.  Rebuilds only when a source or header is newer, or
+when the build mode changed.  --experiments (or BATON_EXPERIMENTS=1) also compiles
+csrc/experiments/*.cu with -DBATON_EXPERIMENTS=1: the round-1 sweep variants
+(BATON_MHA_VARIANT / BATON_GQA_VARIANT) and the globaltimer debug timelines used by
+scripts/trace_*.py and scripts/sweep_*.sh.  The product build has neither.
 """
 import glob
 import os
@@ -25,12 +29,16 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-re
          "-I" + os.path.join(ROOT, "include")]
 
 
-def _sources():
-    return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+def _sources(experiments=False):
+    srcs = glob.glob(os.path.join(CSRC, "*.cu"))
+    if experiments:
+        srcs += glob.glob(os.path.join(CSRC, "experiments", "*.cu"))
+    return sorted(srcs)
 
 
 def _headers():
     return (glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh"))
+            + glob.glob(os.path.join(CSRC, "experiments", "*.h"))
             + glob.glob(os.path.join(ROOT, "include", "*.h")))
 
 
@@ -38,21 +46,28 @@ def _newest(paths):
     return max(os.path.getmtime(p) for p in paths) if paths else 0.0
 
 
-def build(verbose=False, force=False):
-    srcs = _sources()
+def build(verbose=False, force=False, experiments=None):
+    if experiments is None:
+        experiments = os.environ.get("BATON_EXPERIMENTS", "0") == "1"
+    mode = "experiments" if experiments else "product"
+    stamp = LIB + ".mode"
+    old_mode = open(stamp).read().strip() if os.path.exists(stamp) else "product"
+    srcs = _sources(experiments)
     hdr_time = _newest(_headers())
-    if (not force and os.path.exists(LIB)
+    if (not force and os.path.exists(LIB) and old_mode == mode
             and os.path.getmtime(LIB) >= max(_newest(srcs), hdr_time, os.path.getmtime(__file__))):
         return LIB
-    os.makedirs(BUILD, exist_ok=True)
+    build_dir = BUILD + ("-exp" if experiments else "")
+    os.makedirs(build_dir, exist_ok=True)
+    flags = FLAGS + (["-DBATON_EXPERIMENTS=1"] if experiments else [])
 
     def compile_one(src):
-        obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+        obj = os.path.join(build_dir, os.path.basename(src) + ".o")
         if (not force and os.path.exists(obj)
                 and os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_time,
                                                  os.path.getmtime(__file__))):
             return obj, ""
-        cmd = [NVCC, *ARCH, *FLAGS, "-Xptxas", "-v", "-c", src, "-o", obj]
+        cmd = [NVCC, *ARCH, *flags, "-Xptxas", "-v", "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
@@ -71,8 +86,11 @@ def build(verbose=False, force=False):
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
     os.replace(tmp, LIB)
+    with open(stamp, "w") as f:
+        f.write(mode + "\n")
     return LIB
 
 
 if __name__ == "__main__":
-    print(build(verbose="--verbose" in sys.argv, force="--force" in sys.argv))
+    print(build(verbose="--verbose" in sys.argv, force="--force" in sys.argv,
+                experiments=True if "--experiments" in sys.argv else None))

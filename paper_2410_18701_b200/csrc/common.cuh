@@ -1,6 +1,13 @@
 // common.cuh -- sm_100a device helpers shared by the libbaton kernels:
 // mbarrier + bulk-copy (TMA engine, cp.async.bulk) PTX wrappers and bf16 unpacking.
 #pragma once
+// Experiment builds (python -m paper_2410_18701_b200.build --experiments) add the
+// round-1 sweep variants and the globaltimer debug timelines; the product build
+// compiles neither.
+#ifndef BATON_EXPERIMENTS
+#define BATON_EXPERIMENTS 0
+#endif
+
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>

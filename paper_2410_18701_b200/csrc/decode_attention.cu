@@ -34,7 +34,7 @@ namespace baton {
 // writes slot l % MT_L.  Per CTA: [0] enter [1] work list built [2] consumer exit
 // [3] items [4] smid [5] producer past the wait; per item k < 6: [8+4k] w, [9+4k]
 // first copy issued, [10+4k] first tile ready, [11+4k] epilogue done.
-constexpr int MT_L = 8, MT_CTAS = 1024, MT_W = 32;
+constexpr int MT_L = BATON_EXPERIMENTS ? 8 : 1, MT_CTAS = BATON_EXPERIMENTS ? 1024 : 1, MT_W = 32;
 __device__ int g_mtrace_on;
 __device__ long long g_mtrace[MT_L][MT_CTAS][MT_W];
 static int g_mtrace_launch = 0;
@@ -108,7 +108,7 @@ __global__ void __launch_bounds__((CWARPS + 1) * 32, MINB) decode_attention_kern
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const bool trace = g_mtrace_on && blockIdx.x < MT_CTAS;
+    const bool trace = BATON_EXPERIMENTS && g_mtrace_on && blockIdx.x < MT_CTAS;
     long long *tr = g_mtrace[p.trace_slot][trace ? blockIdx.x : 0];
     if (trace && threadIdx.x == 0) {
         tr[0] = mtimer();
@@ -537,14 +537,18 @@ cudaError_t launch_d(const DecodeArgs &a, cudaStream_t s) {
 }
 
 // head_dim 128 pipeline variants (consumer warps, ring stages, CTAs per SM), chosen
-// by BATON_MHA_VARIANT for sweeps; 0 is the default.
+// by BATON_MHA_VARIANT for sweeps in experiment builds; 0 is the default.
 int mha_variant() {
+#if BATON_EXPERIMENTS
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("BATON_MHA_VARIANT");
         v = e ? atoi(e) : 0;
     }
     return v;
+#else
+    return 0;
+#endif
 }
 
 }  // namespace
@@ -571,9 +575,11 @@ cudaError_t launch_decode_attention(const DecodeArgs &a, cudaStream_t s) {
                 // late round 1, on the current kernel: (4,2,3) beats (2,2,5) by 2% on
                 // configs[1] and by 24% on the stress shard (few items per CTA), ties on
                 // 13B churn -> the default (profiles/r01_mha_sweep.md)
+#if BATON_EXPERIMENTS
                 case 1: return launch_d<128, 4, 3, 2>(a, s);
                 case 5: return launch_d<128, 2, 2, 5>(a, s);
                 case 6: return launch_d<128, 2, 2, 4>(a, s);
+#endif
                 default: return launch_d<128, 4, 2, 3>(a, s);
             }
         default: return cudaErrorInvalidValue;
@@ -585,6 +591,12 @@ cudaError_t launch_decode_attention(const DecodeArgs &a, cudaStream_t s) {
 // Debug only (not part of include/baton.h): MHA decode timeline on/off + copy out
 // ([MT_L][MT_CTAS][MT_W] int64, see g_mtrace).
 extern "C" int baton_debug_mha_trace(int on, void *host, size_t bytes) {
+#if !BATON_EXPERIMENTS
+    (void)on;
+    (void)host;
+    (void)bytes;
+    return -1;   // timelines exist in experiment builds only
+#endif
     if (host) {
         if (cudaMemcpyFromSymbol(host, baton::g_mtrace, bytes < sizeof(baton::g_mtrace) ? bytes : sizeof(baton::g_mtrace)) != cudaSuccess)
             return -1;

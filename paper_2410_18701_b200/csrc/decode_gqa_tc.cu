@@ -41,7 +41,7 @@ namespace baton {
 // Debug timeline (off unless baton_debug_gqa_tc_trace(1, ...)): per CTA [0] enter,
 // [1] exit; per tile j < 16: [4+4j] MMA issued S(j), [5+4j] softmax holds S(j),
 // [6+4j] softmax published P(j), [7+4j] MMA issued P.V(j).
-constexpr int TT_CTAS = 160, TT_W = 68;
+constexpr int TT_CTAS = BATON_EXPERIMENTS ? 160 : 1, TT_W = 68;
 __device__ int g_tt_on;
 __device__ long long g_tt[TT_CTAS][TT_W];
 
@@ -136,7 +136,7 @@ decode_gqa_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_cons
     extern __shared__ uint8_t smem_raw[];
     TSmem &sm = *reinterpret_cast<TSmem *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const bool trace = g_tt_on && blockIdx.x < TT_CTAS;
+    const bool trace = BATON_EXPERIMENTS && g_tt_on && blockIdx.x < TT_CTAS;
     long long *tr = g_tt[trace ? blockIdx.x : 0];
     if (trace && threadIdx.x == 0) tr[0] = tt_now();
 
@@ -622,6 +622,12 @@ cudaError_t launch_decode_gqa_tc(const DecodeArgs &a, cudaStream_t s, bool fused
 }  // namespace baton
 
 extern "C" int baton_debug_gqa_tc_trace(int on, void *host, size_t bytes) {
+#if !BATON_EXPERIMENTS
+    (void)on;
+    (void)host;
+    (void)bytes;
+    return -1;   // timelines exist in experiment builds only
+#endif
     if (host) {
         if (cudaMemcpyFromSymbol(host, baton::g_tt, bytes < sizeof(baton::g_tt) ? bytes : sizeof(baton::g_tt)) !=
             cudaSuccess)

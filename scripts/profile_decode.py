@@ -5,7 +5,10 @@
 Builds one 7B-shaped shard (L layers, default 2), embeds every live query of the
 t0 state with its keyed history through baton_insert_many, runs one mask update,
 then launches baton_decode_attention N times per layer and reports the per-launch
-time (CUDA events) and algorithmic GB/s.  Used under ncu for the profiles/."""
+time (CUDA events) and algorithmic GB/s.  Used under ncu for the profiles/.
+Needs an experiment build (python -m paper_2410_18701_b200.build --experiments):
+the product library has no debug timelines.
+"""
 import argparse
 import json
 import math

@@ -2,6 +2,8 @@
 # GQA pipeline variants in the engine path (70B shard, decode-step graphs) + parity
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
+# the sweep variants and timelines exist in experiment builds only
+python -m paper_2410_18701_b200.build --experiments > /dev/null
 : > gpurun_out/sweep_gqa_engine.log
 for v in ${VARIANTS:-0 6 7 8}; do
   echo "variant $v" >> gpurun_out/sweep_gqa_engine.log

@@ -3,7 +3,10 @@
 per launch (layer) the first CTA entry, the median/last time the work list was
 built, the first tile ready, and the last CTA exit, relative to the first entry.
 
-    python scripts/trace_engine.py [--out gpurun_out/engine_trace.json]"""
+    python scripts/trace_engine.py [--out gpurun_out/engine_trace.json]
+Needs an experiment build (python -m paper_2410_18701_b200.build --experiments):
+the product library has no debug timelines.
+"""
 import argparse
 import ctypes
 import json

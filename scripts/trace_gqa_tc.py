@@ -1,5 +1,8 @@
 """Per-tile timeline of the tcgen05 GQA decode kernel (BATON_GQA_VARIANT=20) on the
-70B shard, K/V resident in L2 (one layer, stateless launches)."""
+70B shard, K/V resident in L2 (one layer, stateless launches).
+Needs an experiment build (python -m paper_2410_18701_b200.build --experiments):
+the product library has no debug timelines.
+"""
 import ctypes
 import json
 import os
