@@ -51,7 +51,7 @@ sys.path.insert(0, ROOT)
 INS_AHEAD = 16            # e2e: steps of lookahead for the prefilled K/V H2D of upcoming inserts
 INS_PIECE = 8 << 20       # e2e: bytes per insert H2D piece
 INS_BUDGET = 48 << 20     # e2e: insert H2D bytes issued per step (PCIe ~97 MB per 1.95 ms step; mean need ~32 MB)
-POOL_BYTES = 48 << 30     # prefilled K/V held in HBM for a window (beyond it: recycled buffers)
+POOL_BYTES = 32 << 30     # prefilled K/V held in HBM for a window (beyond it: recycled buffers)
 
 CONFIG_TEXT = {
     "7b": "Llama-2-7B-shaped attention, 32 layers x 32 heads x d128, bf16 KV, 32 slots/GPU, "
@@ -226,6 +226,7 @@ class Window:
     def __init__(self, ctx, t0):
         import torch
         from paper_2410_18701_b200.baton import baton_keygen_tokens, baton_keygen_history
+        _release()                   # cached blocks of earlier passes count as free below
         self.ctx, self.t0 = ctx, t0
         wl, dev, rank = ctx.wl, ctx.dev, ctx.rank
         L, Hq, Hkv, D = wl.layers, wl.q_heads, wl.kv_heads, wl.head_dim
@@ -253,10 +254,10 @@ class Window:
         # (finite, the same distribution)
         tok_bytes = 2 * L * Hkv * D * 2
         # room for the pool: what is free now, less the engine's K/V cache (allocated by
-        # each pass after this) and a 12 GiB margin (warm-start staging, stash, e2e)
+        # each pass after this) and a 24 GiB margin (warm-start staging, stash, e2e)
         cap = (wl.max_ctx + 15) // 16 * 16
         cache = 2 * L * B * Hkv * cap * D * 2
-        budget = min(POOL_BYTES, max(2 << 30, torch.cuda.mem_get_info(dev)[0] - cache - (12 << 30)))
+        budget = min(POOL_BYTES, max(2 << 30, torch.cuda.mem_get_info(dev)[0] - cache - (24 << 30)))
         self.pref = {}
         self.pool_reused = 0
 
@@ -324,6 +325,7 @@ class Ctx:
         from paper_2410_18701_b200.baton import baton_keygen_history
         wl, dev, rank = self.wl, self.dev, self.rank
         L, Hkv, D = wl.layers, wl.kv_heads, wl.head_dim
+        _release()                   # whatever the previous pass left cached
         eng = Engine(wl, rank=rank, world=self.world, device=dev, group=self.group,
                      token_source=token_source, prefill_source=prefill_source, use_graph=True)
         eng.planner = self.planner_at(t0)
@@ -351,6 +353,8 @@ class Ctx:
 
 
 def _release(*objs):
+    """Drop the references passed in (the caller must not hold others) and return the
+    freed blocks to the driver, so the next pass's cache allocation finds room."""
     import torch
     del objs
     gc.collect()
@@ -393,8 +397,8 @@ def run_window(ctx, win, clocks):
     ms = e0.elapsed_time(e1)
     iter_ms = [a.elapsed_time(b) for a, b in zip([e0] + marks[:-1], marks)]
     gather_us = 1e6 * eng.gather_s / max(1, eng.gathers)
-    _release(eng)
     eng = None
+    _release()
 
     tokens = sum(s.decoded for s in st)
     live_rows = sum(s.live_rows for s in st)      # sum of lens over decoding slots
@@ -450,8 +454,8 @@ def run_window(ctx, win, clocks):
     splice_s = sum(a.elapsed_time(b) for a, b, _ in splice_ev) / 1e3
     sh.baton_decode_step, sh.baton_insert_many = orig, orig_ins
     del sh, orig, orig_ins, timed_step, timed_insert
-    _release(eng)
     eng = None
+    _release()
 
     res = dict(t0=t0, ms=ms, tokens=tokens, live_rows=live_rows, attn_bytes=attn_bytes,
                attn_time_s=sum(graph_ms) / 1e3, attn_launches=L * len(graph_ms),
@@ -626,8 +630,8 @@ def run_e2e(ctx, win, B):
     out = {"ms": ms2, "host_ms": host_ms, "step_ms": step_ms,
            "tokens": sum(s.decoded for s in st2), "h2d": counters["h2d"] / K_steps,
            "d2h": counters["d2h"] / K_steps, "inserts_h2d": ins_h2d}
-    del eng
-    _release(q_h, k_h, v_h, pref_h, sets, res_dev, res_h)
+    eng = q_h = k_h = v_h = pref_h = sets = res_dev = res_h = None
+    _release()
     return out
 
 
@@ -651,7 +655,8 @@ def run_full(ctx):
            "mean_live_len": sum(s.live_rows for s in st_f) / max(1, tok_f),
            "what": "whole workload from iteration 0 to drain, one GPU; per-step q/k/v and "
                    "inserted K/V generated on the device (keygen) inside the timed region"}
-    _release(engf, st_f)
+    engf = st_f = None
+    _release()
     return out
 
 
@@ -695,7 +700,8 @@ def run_prefill(ctx, plens):
            "us_per_layer": us, "tflops": flop / us / 1e6, "peak_tflops": bf16_peak,
            "peak_source": "measured" if os.path.exists(pk) else "nominal",
            "frac": flop / us / 1e6 / bf16_peak}
-    _release(qp, kp, vp, op, gr)
+    qp = kp = vp = op = gr = None
+    _release()
     return out
 
 
@@ -713,7 +719,8 @@ def run_baton(args, rank, world, local_rank):
         wins.append(run_window(ctx, win, clocks))
         wins[-1]["fresh"] = [n for _, n, _ in win.fresh]
         win.free()
-        _release(win)
+        win = None
+        _release()
     clk = clocks.stop()
     full_run = run_full(ctx) if (world == 1 and not args.no_full_run) else None
     plens = sum((w["fresh"] for w in wins), [])[:64]

@@ -114,4 +114,10 @@ cudaError_t launch_keygen_history(void *out, int layers, int heads, int head_dim
                                   int pos_begin, int n, int kind, uint64_t seed, int scale_exp,
                                   int64_t head_stride, int64_t layer_stride, cudaStream_t s);
 
+// a8 prefill in the FA4 layout (prefill_fa4.cu): n prompts packed along the token axis
+cudaError_t launch_prefill_fa4_varlen(const void *q, const void *k, const void *v, void *out,
+                                      const int32_t *cu_lens, int n, int q_heads, int kv_heads,
+                                      float scale, float rescale_t, cudaStream_t s);
+long long fa4_rescale_count(bool reset);
+
 }  // namespace baton

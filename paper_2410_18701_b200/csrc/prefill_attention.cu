@@ -449,10 +449,28 @@ cudaError_t launch_pf(const CUtensorMap &mq, const CUtensorMap &mk, const CUtens
 
 int prefill_varlen_max_prompts() { return VL_MAXP; }
 
+namespace {
+// the FA4-layout kernel (prefill_fa4.cu) is the prefill; experiment builds can select
+// this file's round-1 kernel with BATON_PF_KERNEL=1 for A/B runs
+bool use_fa4() {
+#if BATON_EXPERIMENTS
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("BATON_PF_KERNEL");
+        v = e ? atoi(e) : 0;
+    }
+    return v == 0;
+#else
+    return true;
+#endif
+}
+}  // namespace
+
 cudaError_t launch_prefill_attention_varlen(const void *q, const void *k, const void *v, void *out,
                                             const int32_t *cu_lens, int n, int q_heads, int kv_heads,
                                             int head_dim, float scale, cudaStream_t s) {
     if (head_dim != PF_D || n < 1 || n > VL_MAXP || cu_lens[0] != 0) return cudaErrorInvalidValue;
+    if (use_fa4()) return launch_prefill_fa4_varlen(q, k, v, out, cu_lens, n, q_heads, kv_heads, scale, pf_rescale_t(), s);
     PfParams p{};
     // (prompt, query tile) entries, heaviest first (key tiles up to the diagonal),
     // ties by prompt then tile: a longest-processing-time order over all prompts
@@ -536,7 +554,8 @@ extern "C" long long baton_debug_prefill_rescales(int reset) {
         const unsigned long long z = 0;
         if (cudaMemcpyToSymbol(baton::g_pf_rescales, &z, sizeof(z)) != cudaSuccess) return -1;
     }
-    return (long long)v;
+    const long long f = baton::fa4_rescale_count(reset != 0);
+    return f < 0 ? -1 : (long long)v + f;
 }
 extern "C" int baton_debug_prefill_rescale_t(float t) {
     baton::g_rescale_override = t;

@@ -1,11 +1,9 @@
 """NEXT-3 measured: the stress workload's stored K/V in HBM, in pinned host memory,
 or in the prefetchable hybrid store.
 
-    python scripts/bench_hybrid.py [--iters N] [--budget-frac F]
+    python scripts/bench_hybrid.py [--iters N] [--budget-frac F] [--workloads priority,stress]
 
-One GPU's shard of configs[4] (7B shape, 32 slots, active 2 -> 32, 25% of the live
-queries stored every 16 iterations and re-inserted at the queue head), run from
-iteration 0 for N iterations under each store:
+Two workloads (shard_workload), run from iteration 0 under each store:
 
   hbm     every stored query's K/V in HBM (baton_extract HBM -> HBM)
   host    every stored query's K/V in pinned host memory: the extract kernel writes
@@ -28,15 +26,26 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-from baton_inputs import config_workload                      # noqa: E402
+from baton_inputs import config_workload, Query               # noqa: E402
 from paper_2410_18701_b200.engine import Engine               # noqa: E402
 
 
-def shard_workload():
-    wl = config_workload("stress", gpus=8)
-    wl.slots, wl.gpus, wl.active = 32, 1, 2
-    wl.control.resize = {t: n // 8 for t, n in wl.control.resize.items()}
-    wl.queries = wl.queries[:400]
+def shard_workload(kind):
+    """stress: one GPU's shard of configs[4] -- 25% of the live queries stored every 16
+    iterations and re-inserted at the queue head, i.e. at once (nothing to prefetch).
+    priority: the 7B batch (32 slots, D1 mix, Poisson 0.08/iteration, overloaded) with
+    every fifth query urgent (priority 1, reading C25): an urgent arrival that finds no
+    free slot stores the newest low-priority query, which then waits behind the urgent
+    queue -- stored K/V that sit in the store for a while, the case prefetch is for."""
+    if kind == "stress":
+        wl = config_workload("stress", gpus=8)
+        wl.slots, wl.gpus, wl.active = 32, 1, 2
+        wl.control.resize = {t: n // 8 for t, n in wl.control.resize.items()}
+        wl.queries = wl.queries[:400]
+        return wl
+    wl = config_workload("7b")
+    wl.queries = [Query(q.qid, q.arrival, q.l_q, q.A, q.kind, 1 if q.qid % 5 == 4 else 0)
+                  for q in wl.queries]
     return wl
 
 
@@ -58,8 +67,8 @@ def pcie_peak():
     return out
 
 
-def run(mode, iters, budget):
-    wl = shard_workload()
+def run(kind, mode, iters, budget):
+    wl = shard_workload(kind)
     wl.iterations = iters
     kw = {"hbm": {}, "host": {"stash_host": True},
           "hybrid": {"stash_host": "hybrid", "stash_hbm_bytes": budget}}[mode]
@@ -103,22 +112,27 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=640)
     ap.add_argument("--budget-frac", type=float, default=0.25)
+    ap.add_argument("--workloads", default="priority,stress")
     args = ap.parse_args()
     peak = pcie_peak()
     print(json.dumps({"pcie_cudaMemcpy_GBps": peak}), flush=True)
-    base = run("hbm", args.iters, None)
-    print(json.dumps(base), flush=True)
-    budget = int(args.budget_frac * base["peak_stored_bytes"])
-    for mode in ("host", "hybrid"):
-        r = run(mode, args.iters, budget)
-        r["hbm_budget_bytes"] = budget if mode == "hybrid" else None
-        if r["extract_to_host_GBps"]:
-            r["extract_to_host_frac_of_d2h_peak"] = r["extract_to_host_GBps"] / peak["d2h"]
-        if r["prefetch_h2d_GBps"]:
-            r["prefetch_frac_of_h2d_peak"] = r["prefetch_h2d_GBps"] / peak["h2d"]
-        r["tok_per_s_over_hbm"] = r["tok_per_s"] / base["tok_per_s"]
-        print(json.dumps(r), flush=True)
-        torch.cuda.empty_cache()
+    for kind in args.workloads.split(","):
+        iters = args.iters if kind == "stress" else 3 * args.iters
+        base = run(kind, "hbm", iters, None)
+        base["workload"] = kind
+        print(json.dumps(base), flush=True)
+        budget = int(args.budget_frac * base["peak_stored_bytes"])
+        for mode in ("host", "hybrid"):
+            r = run(kind, mode, iters, budget)
+            r["workload"] = kind
+            r["hbm_budget_bytes"] = budget if mode == "hybrid" else None
+            if r["extract_to_host_GBps"]:
+                r["extract_to_host_frac_of_d2h_peak"] = r["extract_to_host_GBps"] / peak["d2h"]
+            if r["prefetch_h2d_GBps"]:
+                r["prefetch_frac_of_h2d_peak"] = r["prefetch_h2d_GBps"] / peak["h2d"]
+            r["tok_per_s_over_hbm"] = r["tok_per_s"] / base["tok_per_s"]
+            print(json.dumps(r), flush=True)
+            torch.cuda.empty_cache()
 
 
 if __name__ == "__main__":

@@ -48,7 +48,8 @@ def _worker(rank, port, name, out_q):
             srv.serve()
             torch.cuda.synchronize()
             out_q.put((0, len(srv.sent), None))
-            return
+            dist.barrier()                      # gloo sends of small tensors complete when
+            return                              # buffered: stay until the decode rank is done
         from paper_2410_18701_b200.engine import Engine
         from oracle import Simulator
         from test_gpu_engine import _check_state
@@ -68,8 +69,11 @@ def _worker(rank, port, name, out_q):
             assert worst <= ATTN_RTOL
             out_q.put((1, len(recv.received), worst))
         except Exception as e:                  # report, and let the prefill rank finish
+            import traceback
+            traceback.print_exc()
             out_q.put((1, -1, repr(e)[:2000]))
         recv.drain()
+        dist.barrier()
     finally:
         dist.destroy_process_group()
 

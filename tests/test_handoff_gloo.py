@@ -57,6 +57,7 @@ def _worker(rank, world, port, out_q):
                                 chunk=5, max_inflight=6)
             srv.serve()
             out_q.put((rank, [q for q, _ in srv.sent], srv.bytes))
+            dist.barrier()
             return
         me = rank - 1
         recv = HandoffReceiver(wl, me, pins, src=0, lookahead=3)
@@ -77,7 +78,9 @@ def _worker(rank, world, port, out_q):
                 ok &= np.array_equal(V.view(torch.int16).numpy(), _bits(wl, KIND_V, q, n))
                 inserted.append(q)
         mine = [q.qid for q in admission_order(wl) if pins[q.qid] == me]
+        recv.drain()
         out_q.put((rank, inserted, ok, mine, trace))
+        dist.barrier()
     finally:
         dist.destroy_process_group()
 
