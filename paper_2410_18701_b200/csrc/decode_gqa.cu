@@ -104,7 +104,96 @@ __global__ void __launch_bounds__(128) decode_combine_kernel(const int32_t *__re
     }
 }
 
+// The same merge, started before the attention grid completes: a CTA owns whole
+// (slot, kv group)s -- 4 warps x 2 pairs = the group's 8 q heads -- and polls the
+// group's ticket (chunks published by the attention kernel's P.V issuers, release
+// -> acquire) instead of waiting for the grid, so the merges run under the attention
+// tail.  The CTA resets the ticket once all 4 warps have merged the group.  Resident
+// beside the attention CTA (128 threads x 72 registers fit next to 384 x 144).
+__global__ void __launch_bounds__(128) decode_combine_spin_kernel(const int32_t *__restrict__ lens,
+                                                                  const float *__restrict__ partial,
+                                                                  int32_t *tickets,
+                                                                  __nv_bfloat16 *__restrict__ out, int B,
+                                                                  int Hq, int max_chunks) {
+    griddep_launch_dependents();
+    const int lane = threadIdx.x & 31, hl = lane & 15, w = threadIdx.x >> 5;
+    const int groups = B * (Hq / GS);
+    constexpr int R = D + PREC_PAD, NB = 8;
+    for (int gi = blockIdx.x; gi < groups; gi += gridDim.x) {
+        const int b = gi / (Hq / GS);
+        const int L = lens[b];
+        const int nch = (L + CHUNK - 1) / CHUNK;
+        if (nch <= 1) continue;                                   // uniform over the CTA
+        const int bh0 = gi * GS;
+        int32_t *tk = tickets + bh0;
+        if (lane == 0) {
+            const long long t0 = clock64();
+            while (ld_acquire_gpu(tk) < nch) {
+                __nanosleep(256);
+                if (clock64() - t0 > 60000000000LL) {   // ~30 s: a missing publish traps, not hangs
+                    printf("baton watchdog: combine waits on ticket %d (%d of %d)\n", bh0, *tk, nch);
+                    __trap();
+                }
+            }
+        }
+        __syncwarp();
+        const int pair = bh0 + 2 * w + (lane >> 4);
+        const float *pp = partial + (size_t)pair * max_chunks * R + hl * 8;
+        float Mc = -INFINITY, Lc = 0.f, Oc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        for (int c0 = 0; c0 < nch; c0 += NB) {
+            float m[NB], l[NB];
+            float4 va[NB], vb[NB];
+#pragma unroll
+            for (int j = 0; j < NB; ++j) {
+                const bool ok = c0 + j < nch;
+                const float *r = pp + (ok ? c0 + j : c0) * R;
+                m[j] = ok ? __ldcg(r - hl * 8 + D) : -INFINITY;
+                l[j] = ok ? __ldcg(r - hl * 8 + D + 1) : 0.f;
+                va[j] = __ldcg(reinterpret_cast<const float4 *>(r));
+                vb[j] = __ldcg(reinterpret_cast<const float4 *>(r + 4));
+            }
+            float Mn = Mc;
+#pragma unroll
+            for (int j = 0; j < NB; ++j) Mn = fmaxf(Mn, m[j]);
+            const float al = (Mc == -INFINITY) ? 0.f : ex2(Mc - Mn);
+            Lc *= al;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) Oc[i] *= al;
+#pragma unroll
+            for (int j = 0; j < NB; ++j) {
+                const float f = (m[j] == -INFINITY) ? 0.f : ex2(m[j] - Mn);
+                Lc = fmaf(f, l[j], Lc);
+                Oc[0] = fmaf(f, va[j].x, Oc[0]);
+                Oc[1] = fmaf(f, va[j].y, Oc[1]);
+                Oc[2] = fmaf(f, va[j].z, Oc[2]);
+                Oc[3] = fmaf(f, va[j].w, Oc[3]);
+                Oc[4] = fmaf(f, vb[j].x, Oc[4]);
+                Oc[5] = fmaf(f, vb[j].y, Oc[5]);
+                Oc[6] = fmaf(f, vb[j].z, Oc[6]);
+                Oc[7] = fmaf(f, vb[j].w, Oc[7]);
+            }
+            Mc = Mn;
+        }
+        const float inv = Lc > 0.f ? 1.f / Lc : 0.f;
+        uint4 wv;
+        wv.x = pack_bf16(Oc[0] * inv, Oc[1] * inv);
+        wv.y = pack_bf16(Oc[2] * inv, Oc[3] * inv);
+        wv.z = pack_bf16(Oc[4] * inv, Oc[5] * inv);
+        wv.w = pack_bf16(Oc[6] * inv, Oc[7] * inv);
+        *reinterpret_cast<uint4 *>(out + (size_t)pair * D + hl * 8) = wv;
+        __syncthreads();                                          // all 8 heads observed the ticket
+        if (threadIdx.x == 0) *tk = 0;                            // ready for the next launch
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_gqa_combine_spin(const DecodeArgs &a, cudaStream_t s) {
+    const int num_sms = device_sms();
+    return launch_pdl(decode_combine_spin_kernel, dim3(num_sms), dim3(128), 0, s, a.lens,
+                      (const float *)a.partial, a.tickets, static_cast<__nv_bfloat16 *>(a.out), a.slots,
+                      a.q_heads, a.max_chunks);
+}
 
 bool gqa_supported(int q_heads, int kv_heads, int head_dim) {
     return head_dim == D && kv_heads > 0 && q_heads == GS * kv_heads;
@@ -133,6 +222,16 @@ cudaError_t launch_decode_gqa(const DecodeArgs &a, cudaStream_t s) {
         v = e ? atoi(e) : 20;
     }
     if (v == 21 && a.max_chunks <= 32) return launch_decode_gqa_tc(a, s, true);
+    // 22: the attention launch alone, no split-K merge (WRONG outputs for multi-chunk
+    // queries; measures what the combine hop costs in the decode-step chain)
+    if (v == 22) return launch_decode_gqa_tc(a, s, false);
+    // 23: published tickets + a combine that merges each (slot, kv group) as soon as it
+    // is complete, under the attention tail
+    if (v == 23) {
+        cudaError_t e = launch_decode_gqa_tc(a, s, false, true);
+        if (e != cudaSuccess || a.dry) return e;
+        return launch_gqa_combine_spin(a, s);
+    }
     if (v != 20 && v != 21) return launch_gqa_experiment(v, a, s);
 #endif
     cudaError_t e = launch_decode_gqa_tc(a, s, false);

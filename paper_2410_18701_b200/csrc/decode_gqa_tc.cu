@@ -55,6 +55,7 @@ BATON_DEV long long tt_now() {
 
 constexpr int D = 128, GS = 8, NH = 16;      // UMMA N = 16 heads (8 real)
 constexpr int TK = 128;                      // keys per tile
+constexpr int TAIL = 32;                     // rows per TMA box of a short (last) tile
 constexpr int STAGES = 3;
 constexpr int KREG = TK * 128;               // 16 KB: a 64-dim half of a K or V tile
 constexpr int QREG = NH * 128;               // 2 KB: a 64-dim half of the q tile
@@ -76,6 +77,7 @@ struct __align__(1024) TStage {
 
 struct PvEntry {
     int32_t stage, flags;
+    int32_t bh0, multi;                      // publish: (slot, kv group) ticket of a split item's last tile
 };
 
 struct __align__(1024) TSmem {
@@ -84,6 +86,7 @@ struct __align__(1024) TSmem {
     uint8_t p[2][2 * PREG];                  // P^T per group
     uint64_t full[STAGES], empty[STAGES], q_empty[2];
     uint64_t s_full[2][2], s_free[2][2], p_full[2], o_done[2];   // [group][S buffer] / [group]
+    uint64_t pub[2];                         // publish: the group's partials are written
     TDesc gq[2][2];                          // the group's tile queue, per S buffer
     PvEntry pvq[2][4];                       // the P.V issuer's queue, per group
     WorkSched ws;
@@ -108,6 +111,8 @@ struct TParams {
     float scale_log2;
     bool early;
     bool fused;                              // in-kernel split-K merge (no combine launch)
+    bool publish;                            // count published chunks per (slot, kv group) for a
+                                             // combine that merges as soon as a group is complete
 };
 
 BATON_DEV void tma_2d(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar) {
@@ -132,7 +137,8 @@ BATON_DEV uint32_t swz(int r, int c, int reg) {
 // so the next layer's CTA can enter while this layer drains (PDL early phase)
 __global__ void __maxnreg__(144)
 decode_gqa_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
-                     const __grid_constant__ CUtensorMap qmap, const TParams p) {
+                     const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap32,
+                     const __grid_constant__ CUtensorMap vmap32, const TParams p) {
     extern __shared__ uint8_t smem_raw[];
     TSmem &sm = *reinterpret_cast<TSmem *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -149,6 +155,7 @@ decode_gqa_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_cons
             mbar_init(&sm.q_empty[g], 1);
             mbar_init(&sm.p_full[g], 128);
             mbar_init(&sm.o_done[g], 1);
+            mbar_init(&sm.pub[g], 128);
             for (int b2 = 0; b2 < 2; ++b2) {
                 mbar_init(&sm.s_full[g][b2], 2);      // S MMAs done + queue entry written
                 mbar_init(&sm.s_free[g][b2], 128);
@@ -179,6 +186,8 @@ decode_gqa_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_cons
             prefetch_tmap(&kmap);
             prefetch_tmap(&vmap);
             prefetch_tmap(&qmap);
+            prefetch_tmap(&kmap32);
+            prefetch_tmap(&vmap32);
             const int total = sched_total(sm.ws, p.Hkv);
             int stage = 0, b = 0, item = 0, issued = 0;
             uint32_t phase = 0;
@@ -215,7 +224,10 @@ decode_gqa_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_cons
                     mbar_wait(&sm.empty[stage], phase ^ 1);
                     if (t == 0) mbar_wait(&sm.q_empty[par], ((item >> 1) & 1) ^ 1);   // S of item-2 done
                     TStage &st = sm.st[stage];
-                    uint32_t bytes = 4 * KREG;
+                    // a tile cut short by lens is fetched in 32-row boxes: at most 31 rows
+                    // past lens, not up to 127 (rows past nr are masked, their V zeroed)
+                    const int nbox = nr == TK ? 0 : (nr + TAIL - 1) / TAIL;
+                    uint32_t bytes = nbox ? 4u * nbox * TAIL * 128 : 4 * KREG;
                     int moff = 0;
                     uint32_t mbytes = 0;
                     const uint8_t *msrc = nullptr;
@@ -244,10 +256,20 @@ decode_gqa_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_cons
                     st.desc.stage = stage;
                     mbar_arrive_expect_tx(&sm.full[stage], bytes);
                     const int row = row_base + t * TK;
-                    tma_2d(st.k, &kmap, 0, row, &sm.full[stage]);
-                    tma_2d(st.k + KREG, &kmap, 64, row, &sm.full[stage]);
-                    tma_2d(st.v, &vmap, 0, row, &sm.full[stage]);
-                    tma_2d(st.v + KREG, &vmap, 64, row, &sm.full[stage]);
+                    if (nbox == 0) {
+                        tma_2d(st.k, &kmap, 0, row, &sm.full[stage]);
+                        tma_2d(st.k + KREG, &kmap, 64, row, &sm.full[stage]);
+                        tma_2d(st.v, &vmap, 0, row, &sm.full[stage]);
+                        tma_2d(st.v + KREG, &vmap, 64, row, &sm.full[stage]);
+                    } else {
+                        for (int i = 0; i < nbox; ++i) {   // 4 KB pieces, 1024-B aligned: same swizzle
+                            const uint32_t o = i * TAIL * 128;
+                            tma_2d(st.k + o, &kmap32, 0, row + i * TAIL, &sm.full[stage]);
+                            tma_2d(st.k + KREG + o, &kmap32, 64, row + i * TAIL, &sm.full[stage]);
+                            tma_2d(st.v + o, &vmap32, 0, row + i * TAIL, &sm.full[stage]);
+                            tma_2d(st.v + KREG + o, &vmap32, 64, row + i * TAIL, &sm.full[stage]);
+                        }
+                    }
                     if (mbytes) bulk_g2s(st.mask, msrc, mbytes, &sm.full[stage]);
                     if (app_tile) {   // always after the wait (flush above)
                         const size_t nb = ((size_t)b * p.Hkv + g) * D;
@@ -332,7 +354,8 @@ decode_gqa_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_cons
                 umma_commit(&sm.s_full[g][sb]);
                 if (d.flags & F_LAST) umma_commit(&sm.q_empty[g]);
                 sm.gq[g][sb] = d;
-                sm.pvq[g][n & 3] = PvEntry{d.stage, d.flags};
+                sm.pvq[g][n & 3] = PvEntry{d.stage, d.flags, d.b * p.Hq + d.g * GS,
+                                           (d.flags & F_LAST) && d.nchunks > 1};
                 mbar_arrive(&sm.s_full[g][sb]);            // release: the queue entries
                 if (trace && g == 0 && n < 16) tr[4 + 4 * n] = tt_now();
                 cnt[g] = n + 1;
@@ -348,10 +371,25 @@ decode_gqa_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_cons
             const int g = warp - 10;
             constexpr uint32_t idO = idesc_bf16_ab(D, NH, 1, 0);    // A = V (MN-major), B = P^T (K-major)
             const uint32_t tO = tmem + 64 + 16 * g, pa = smem_u32(sm.p[g]);
+            // publish mode: a split item's ticket is released after this group's softmax
+            // threads wrote its partials (pub barrier) -- deferred until the next P.V is
+            // issued, so the release's wait for those writes overlaps tensor work
+            int pending = -1;
+            uint32_t pub_phase = 0;
+            auto publish = [&]() {
+                if (pending < 0) return;
+                mbar_wait(&sm.pub[g], pub_phase);
+                pub_phase ^= 1;
+                red_add_release_gpu(p.tickets + pending, 1);
+                pending = -1;
+            };
             for (int n = 0;; ++n) {
                 mbar_wait(&sm.p_full[g], n & 1);
                 const PvEntry e = sm.pvq[g][n & 3];
-                if (e.flags & F_END) break;
+                if (e.flags & F_END) {
+                    publish();
+                    break;
+                }
                 tc_fence_after();
                 const uint32_t va = smem_u32(sm.st[e.stage].v);
 #pragma unroll
@@ -362,6 +400,10 @@ decode_gqa_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_cons
                 umma_commit(&sm.o_done[g]);
                 umma_commit(&sm.empty[e.stage]);
                 if (trace && g == 0 && n < 16) tr[7 + 4 * n] = tt_now();
+                if (p.publish) {
+                    publish();
+                    if (e.multi) pending = e.bh0;
+                }
             }
         }
     } else if (warp < 8) {
@@ -497,6 +539,7 @@ decode_gqa_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_cons
                             pp[D + 1] = lt[h];
                         }
                     }
+                    if (p.publish) mbar_arrive(&sm.pub[grp]);   // release.cta: the PV issuer publishes
                     if (p.fused) {
                         // in-kernel split-K merge: the group that draws the last ticket of
                         // (slot, kv group) merges the chunks in ascending order.  The
@@ -577,7 +620,7 @@ decode_gqa_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_cons
 
 }  // namespace
 
-cudaError_t launch_decode_gqa_tc(const DecodeArgs &a, cudaStream_t s, bool fused) {
+cudaError_t launch_decode_gqa_tc(const DecodeArgs &a, cudaStream_t s, bool fused, bool publish) {
     const int num_sms = device_sms();
     const size_t smem = sizeof(TSmem) + 1024;
     {
@@ -599,6 +642,7 @@ cudaError_t launch_decode_gqa_tc(const DecodeArgs &a, cudaStream_t s, bool fused
     p.partial = a.partial;
     p.tickets = a.tickets;
     p.fused = fused;
+    p.publish = publish && !fused;
     if (fused && a.max_chunks > 32) return cudaErrorInvalidValue;   // see TSmem::mf
     p.B = a.slots;
     p.Hq = a.q_heads;
@@ -607,16 +651,18 @@ cudaError_t launch_decode_gqa_tc(const DecodeArgs &a, cudaStream_t s, bool fused
     p.max_chunks = a.max_chunks;
     p.scale_log2 = a.scale * 1.4426950408889634f;
     p.early = a.early;
-    CUtensorMap km, vm, qm;
+    CUtensorMap km, vm, qm, km32, vm32;
     const uint64_t dims[2] = {(uint64_t)D, (uint64_t)a.slots * a.kv_heads * a.max_ctx};
     const uint64_t strides[1] = {(uint64_t)D * 2};
     const uint32_t box[2] = {64, TK};
     const uint64_t qdims[2] = {(uint64_t)D, (uint64_t)a.slots * a.q_heads};
     const uint32_t qbox[2] = {64, NH};
+    const uint32_t box32[2] = {64, TAIL};
     if (!encode_bf16_map(&km, a.k, 2, dims, strides, box) || !encode_bf16_map(&vm, a.v, 2, dims, strides, box) ||
-        !encode_bf16_map(&qm, a.q, 2, qdims, strides, qbox))
+        !encode_bf16_map(&qm, a.q, 2, qdims, strides, qbox) ||
+        !encode_bf16_map(&km32, a.k, 2, dims, strides, box32) || !encode_bf16_map(&vm32, a.v, 2, dims, strides, box32))
         return cudaErrorInvalidValue;
-    return launch_pdl(decode_gqa_tc_kernel, dim3(num_sms), dim3(THREADS), smem, s, km, vm, qm, p);
+    return launch_pdl(decode_gqa_tc_kernel, dim3(num_sms), dim3(THREADS), smem, s, km, vm, qm, km32, vm32, p);
 }
 
 }  // namespace baton

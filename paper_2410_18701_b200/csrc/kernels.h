@@ -41,7 +41,8 @@ cudaError_t launch_decode_attention(const DecodeArgs &a, cudaStream_t s);
 bool gqa_supported(int q_heads, int kv_heads, int head_dim);
 cudaError_t launch_decode_gqa(const DecodeArgs &a, cudaStream_t s);
 // tcgen05 variants: 20 = separate combine kernel, 21 = fused in-kernel merge
-cudaError_t launch_decode_gqa_tc(const DecodeArgs &a, cudaStream_t s, bool fused);
+cudaError_t launch_decode_gqa_tc(const DecodeArgs &a, cudaStream_t s, bool fused, bool publish = false);
+cudaError_t launch_gqa_combine_spin(const DecodeArgs &a, cudaStream_t s);
 cudaError_t launch_gqa_combine(const DecodeArgs &a, cudaStream_t s);
 
 // ------------------------------------------------------------ metadata / mask

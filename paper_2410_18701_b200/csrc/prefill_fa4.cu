@@ -128,7 +128,8 @@ BATON_DEV Work decode_work(const FaParams &p, int w) {
     return k;
 }
 
-__global__ void __maxnreg__(200)
+// 10 warps: SM sub-partitions 0/1 hold 3 of them, so at most 16384 / 96 = 170 registers
+__global__ void __launch_bounds__(FTHREADS, 1)
 prefill_fa4_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                    const __grid_constant__ CUtensorMap tm_v, const FaParams p) {
     extern __shared__ uint8_t smem_raw[];
@@ -283,32 +284,29 @@ prefill_fa4_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
             for (int j = 0; j < n; ++j, ++ns) {
                 mbar_wait(&sm.s_full[grp], ns & 1);
                 tc_fence_after();
-                uint32_t r[4][32];
+                // two passes over the S row in TMEM (32 columns at a time, so at most one
+                // chunk of scores is live): the row max, then exp2 / pack / P store.
+                // Diagonal tile: keys c > lim are causally masked (-inf).
+                const bool diag = j == n - 1;
+                const int lim = qi - j * FN;
+                float a0 = -INFINITY, a1 = -INFINITY;
 #pragma unroll
-                for (int c = 0; c < 4; ++c) tmem_ld32(tS + 32 * c, r[c]);
-                tmem_wait_ld();
-                if (j == n - 1) {                        // the diagonal tile: causal -inf
-                    const int lim = qi - j * FN;         // keys c <= lim live
+                for (int c4 = 0; c4 < 4; ++c4) {
+                    uint32_t r[32];
+                    tmem_ld32(tS + 32 * c4, r);
+                    tmem_wait_ld();
+                    if (diag) {
 #pragma unroll
-                    for (int c = 0; c < FN; ++c)
-                        if (c > lim) r[c >> 5][c & 31] = __float_as_uint(-INFINITY);
+                        for (int i = 0; i < 32; ++i)
+                            if (32 * c4 + i > lim) r[i] = __float_as_uint(-INFINITY);
+                    }
+#pragma unroll
+                    for (int i = 0; i < 32; i += 4) {   // 3-input FMNMX3, two chains
+                        a0 = fmax3(a0, __uint_as_float(r[i]), __uint_as_float(r[i + 1]));
+                        a1 = fmax3(a1, __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
+                    }
                 }
-                float mx;
-                {   // row max by 3-input FMNMX3: 128 -> 43 -> 15 -> 5 -> 1
-                    float t[43];
-#pragma unroll
-                    for (int c = 0; c < 42; ++c)
-                        t[c] = fmax3(__uint_as_float(r[(3 * c) >> 5][(3 * c) & 31]),
-                                     __uint_as_float(r[(3 * c + 1) >> 5][(3 * c + 1) & 31]),
-                                     __uint_as_float(r[(3 * c + 2) >> 5][(3 * c + 2) & 31]));
-                    t[42] = fmaxf(__uint_as_float(r[3][30]), __uint_as_float(r[3][31]));
-#pragma unroll
-                    for (int c = 0; c < 14; ++c) t[c] = fmax3(t[3 * c], t[3 * c + 1], t[3 * c + 2]);
-                    t[14] = t[42];
-#pragma unroll
-                    for (int c = 0; c < 5; ++c) t[c] = fmax3(t[3 * c], t[3 * c + 1], t[3 * c + 2]);
-                    mx = fmax3(fmax3(t[0], t[1], t[2]), t[3], t[4]);
-                }
+                float mx = fmaxf(a0, a1);
                 mx *= p.scale_log2;                      // -inf stays -inf
                 // lazy rescale (see the header); a row with only masked keys so far keeps
                 // exp2 finite: ex2(-inf - 0) = 0
@@ -317,13 +315,22 @@ prefill_fa4_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
                 const float alpha = ex2(m - mref);
                 const float2 nr2 = make_float2(-mref, -mref);
                 float2 rs2 = make_float2(0.f, 0.f);
+                // P -> TMEM columns [0,64) of S_grp; chunk c4 writes columns 16c4.. that
+                // chunks <= c4 already read
 #pragma unroll
-                for (int c4 = 0; c4 < 4; ++c4) {         // P -> TMEM columns [0,64) of S_grp, 16 per chunk
+                for (int c4 = 0; c4 < 4; ++c4) {
+                    uint32_t r[32];
+                    tmem_ld32(tS + 32 * c4, r);
+                    tmem_wait_ld();
+                    if (diag) {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            if (32 * c4 + i > lim) r[i] = __float_as_uint(-INFINITY);
+                    }
                     uint32_t pk[16];
 #pragma unroll
                     for (int i = 0; i < 32; i += 2) {
-                        float2 a = ffma2(make_float2(__uint_as_float(r[c4][i]), __uint_as_float(r[c4][i + 1])),
-                                         sc2, nr2);
+                        float2 a = ffma2(make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), sc2, nr2);
                         a.x = ex2(a.x);
                         a.y = ex2(a.y);
                         const __nv_bfloat162 b = __floats2bfloat162_rn(a.x, a.y);

@@ -13,3 +13,4 @@ ncu --set full --clock-control none -k regex:prefill_fa4 -c 1 -o gpurun_out/fa4_
 timeout 900 python -m pytest tests/test_gpu_handoff.py -q -x > gpurun_out/handoff_tests.log 2>&1; echo "rc=$?" >> gpurun_out/handoff_tests.log
 timeout 900 python bench.py --config 13b --no-cpu-baseline > gpurun_out/bench_13b.log 2>&1; echo "rc=$?" >> gpurun_out/bench_13b.log
 timeout 900 python scripts/bench_hybrid.py > gpurun_out/hybrid2.log 2>&1; echo "rc=$?" >> gpurun_out/hybrid2.log
+bash scripts/ab_gqa_r02.sh
