@@ -12,8 +12,9 @@ will be promptly re-inserted"; under memory pressure stored queries are
 
 Host-resident entries are PREFETCHED back into HBM on a copy stream ahead of
 their re-insert: every iteration the engine passes the planner's service order
-of the waiting queue, and the first ``lookahead`` host entries whose size fits
-the free HBM budget start an async H2D copy.  The re-insert then reads HBM
+of the waiting queue, and host entries among its first ``lookahead`` stored
+queries start an async H2D copy into staging buffers while the staging budget
+allows.  The re-insert then reads HBM
 (``baton_insert`` after waiting on that copy's event only); an entry not (yet)
 prefetched is inserted from host memory directly, as before.  Placement never
 changes a byte: the re-inserted rows are the extracted rows (tested bit-exact).
@@ -40,9 +41,13 @@ class Entry:
 
 
 class HybridKVStore:
-    def __init__(self, shard, device, hbm_budget=None, host=True, prefetch=True, lookahead=8):
+    def __init__(self, shard, device, hbm_budget=None, host=True, prefetch=True, lookahead=8,
+                 staging_budget=4 << 30):
         """hbm_budget: bytes of stored K/V kept in HBM (None = unlimited, i.e. the
-        plain HBM stash; 0 with host=True = every store spills to the host)."""
+        plain HBM stash; 0 with host=True = every store spills to the host).
+        staging_budget: HBM for prefetched host entries in flight to their re-insert
+        (separate from hbm_budget: a spilled query may be larger than the whole stash
+        budget, and the re-insert needs its bytes in HBM anyway)."""
         self.shard = shard
         self.device = device
         self.hbm_budget = hbm_budget
@@ -51,6 +56,8 @@ class HybridKVStore:
         self.lookahead = lookahead
         self.entries: Dict[int, Entry] = {}
         self.hbm_used = 0
+        self.staging_budget = staging_budget
+        self.staging_used = 0
         self.stored_bytes = self.peak_stored_bytes = 0       # all placements
         self.copy_stream = torch.cuda.Stream(device=device) if self.prefetch_on else None
         self._inflight: List[tuple] = []     # (event, tensors) kept alive until read
@@ -110,7 +117,7 @@ class HybridKVStore:
             seen += 1
             if seen > self.lookahead:
                 break
-            if e.where != "host" or not self._fits(e.nbytes):
+            if e.where != "host" or self.staging_used + e.nbytes > self.staging_budget:
                 continue
             # allocated on the decode stream (its caching-allocator pool); the copy
             # stream waits for everything enqueued there so far -- the extract that
@@ -133,7 +140,7 @@ class HybridKVStore:
                     self.timing.append((t0, ev, e.nbytes))
             e.host = (e.K, e.V)
             e.K, e.V, e.where, e.ready = Kd, Vd, "prefetching", ev
-            self.hbm_used += e.nbytes
+            self.staging_used += e.nbytes
             self.stats["prefetched"] += 1
             self.stats["prefetch_bytes"] += e.nbytes
 
@@ -152,7 +159,9 @@ class HybridKVStore:
         if e.where == "prefetching":
             cur.wait_event(e.ready)
             self._inflight.append((e.ready, e.host))
-        self.hbm_used -= e.nbytes
+            self.staging_used -= e.nbytes
+        else:
+            self.hbm_used -= e.nbytes
         self.stats["inserted_from_hbm"] += 1
         return e.K, e.V
 
