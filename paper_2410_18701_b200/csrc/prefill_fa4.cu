@@ -18,7 +18,7 @@
 //     cycles); both Q tiles of the pair share every K/V tile (K/V smem traffic and L2
 //     reads halved per FLOP);
 //   * TMEM (512 columns): S0 | S1 | O0 | O1, 128 columns each.  P_i overwrites the
-//     first 64 columns of S_i as bf16 pairs and feeds O_i += P_i V as the TMEM (A)
+//     upper 64 columns of S_i as bf16 pairs and feeds O_i += P_i V as the TMEM (A)
 //     operand ("TS" form);
 //   * two softmax warpgroups (warps 0-3: Q tile 0, warps 4-7: Q tile 1), thread =
 //     query row = TMEM lane, ping-ponged: the MMA issuer (warp 9) issues
@@ -31,11 +31,12 @@
 //   * warp 8: TMA producer -- Q tiles (2 x 32 KB), K and V tiles (32 KB each) through
 //     2-stage rings, cp.async.bulk.tensor with mbarrier tx-counts.  The next work
 //     item's Q and K/V stream in while this item's last tiles and epilogue run.
-//   Softmax per row and 128-key tile: 4 tcgen05.ld x32, causal -inf only on the
-//   diagonal tile, the row max by 3-input FMNMX3, lazy rescale (P <= 2^rescale_t
-//   against a reference max that moves only by more than rescale_t, O rescaled in
-//   TMEM on those tiles), exponent FFMA2 + ex2 per key, bf16x2 packs straight into
-//   TMEM (tcgen05.st x16), fp32 row sum by FADD2.  Epilogue: O_i / l -> bf16 rows.
+//   Softmax per row and 128-key tile: three tcgen05.ld round trips of 64 columns
+//   (the 10-warp CTA leaves 168 registers a thread), causal -inf only on the diagonal
+//   tile, the row max by 3-input FMNMX3, lazy rescale (P <= 2^rescale_t against a
+//   reference max that moves only by more than rescale_t, O rescaled in TMEM on those
+//   tiles), exponent FFMA2 + ex2 per key, bf16x2 packs straight into TMEM
+//   (tcgen05.st x32), fp32 row sum by FADD2.  Epilogue: O_i / l -> bf16 rows.
 #include <cuda.h>
 
 #include <algorithm>
@@ -218,7 +219,7 @@ prefill_fa4_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
                 const uint32_t va = smem_u32(sm.v[s]);
 #pragma unroll
                 for (int k = 0; k < 8; ++k)        // K = 128 keys in steps of 16 (8 TMEM columns of bf16 pairs)
-                    umma_f16_ts(tmem + 256 + 128 * i, tmem + 128 * i + 8 * k,
+                    umma_f16_ts(tmem + 256 + 128 * i, tmem + 128 * i + 64 + 8 * k,
                                 smem_desc(va + k * 2048, FKV_REG, 1024), idO, (j > 0 || k > 0));
             };
             auto wait_k = [&](int j) {
@@ -284,29 +285,40 @@ prefill_fa4_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
             for (int j = 0; j < n; ++j, ++ns) {
                 mbar_wait(&sm.s_full[grp], ns & 1);
                 tc_fence_after();
-                // two passes over the S row in TMEM (32 columns at a time, so at most one
-                // chunk of scores is live): the row max, then exp2 / pack / P store.
-                // Diagonal tile: keys c > lim are causally masked (-inf).
+                // The S row in TMEM, 64 columns per tcgen05.ld round trip (at most 64
+                // scores + 32 packed P live in registers): (1) columns 0-63, then 64-127,
+                // for the row max; (2) exp2 / pack of keys 64-127 (still in registers) ->
+                // P columns 96-127; reload keys 0-63, exp2 / pack -> P columns 64-95.  P
+                // (key 2c in the low half of column 64 + c) only overwrites scores that are
+                // already in registers.  Diagonal tile: keys c > lim causally masked (-inf).
                 const bool diag = j == n - 1;
                 const int lim = qi - j * FN;
-                float a0 = -INFINITY, a1 = -INFINITY;
-#pragma unroll
-                for (int c4 = 0; c4 < 4; ++c4) {
-                    uint32_t r[32];
-                    tmem_ld32(tS + 32 * c4, r);
+                uint32_t ra[32], rb[32];
+                auto load2 = [&](int c0) {
+                    tmem_ld32(tS + c0, ra);
+                    tmem_ld32(tS + c0 + 32, rb);
                     tmem_wait_ld();
                     if (diag) {
 #pragma unroll
-                        for (int i = 0; i < 32; ++i)
-                            if (32 * c4 + i > lim) r[i] = __float_as_uint(-INFINITY);
+                        for (int i = 0; i < 32; ++i) {
+                            if (c0 + i > lim) ra[i] = __float_as_uint(-INFINITY);
+                            if (c0 + 32 + i > lim) rb[i] = __float_as_uint(-INFINITY);
+                        }
                     }
+                };
+                auto max2 = [&](float acc) {
+                    float a0 = acc, a1 = -INFINITY;
 #pragma unroll
-                    for (int i = 0; i < 32; i += 4) {   // 3-input FMNMX3, two chains
-                        a0 = fmax3(a0, __uint_as_float(r[i]), __uint_as_float(r[i + 1]));
-                        a1 = fmax3(a1, __uint_as_float(r[i + 2]), __uint_as_float(r[i + 3]));
+                    for (int i = 0; i < 32; i += 2) {   // 3-input FMNMX3, two chains
+                        a0 = fmax3(a0, __uint_as_float(ra[i]), __uint_as_float(ra[i + 1]));
+                        a1 = fmax3(a1, __uint_as_float(rb[i]), __uint_as_float(rb[i + 1]));
                     }
-                }
-                float mx = fmaxf(a0, a1);
+                    return fmaxf(a0, a1);
+                };
+                load2(0);
+                float mx = max2(-INFINITY);
+                load2(64);
+                mx = max2(mx);
                 mx *= p.scale_log2;                      // -inf stays -inf
                 // lazy rescale (see the header); a row with only masked keys so far keeps
                 // exp2 finite: ex2(-inf - 0) = 0
@@ -315,29 +327,28 @@ prefill_fa4_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
                 const float alpha = ex2(m - mref);
                 const float2 nr2 = make_float2(-mref, -mref);
                 float2 rs2 = make_float2(0.f, 0.f);
-                // P -> TMEM columns [0,64) of S_grp; chunk c4 writes columns 16c4.. that
-                // chunks <= c4 already read
+                auto pack2 = [&](uint32_t (&pk)[32]) {
 #pragma unroll
-                for (int c4 = 0; c4 < 4; ++c4) {
-                    uint32_t r[32];
-                    tmem_ld32(tS + 32 * c4, r);
-                    tmem_wait_ld();
-                    if (diag) {
-#pragma unroll
-                        for (int i = 0; i < 32; ++i)
-                            if (32 * c4 + i > lim) r[i] = __float_as_uint(-INFINITY);
-                    }
-                    uint32_t pk[16];
-#pragma unroll
-                    for (int i = 0; i < 32; i += 2) {
-                        float2 a = ffma2(make_float2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), sc2, nr2);
+                    for (int i = 0; i < 64; i += 2) {
+                        const uint32_t x0 = i < 32 ? ra[i] : rb[i - 32], x1 = i < 32 ? ra[i + 1] : rb[i - 31];
+                        float2 a = ffma2(make_float2(__uint_as_float(x0), __uint_as_float(x1)), sc2, nr2);
                         a.x = ex2(a.x);
                         a.y = ex2(a.y);
                         const __nv_bfloat162 b = __floats2bfloat162_rn(a.x, a.y);
                         rs2 = fadd2(rs2, a);
                         pk[i / 2] = *reinterpret_cast<const uint32_t *>(&b);
                     }
-                    tmem_st16(tS + 16 * c4, pk);
+                };
+                {
+                    uint32_t pk[32];
+                    pack2(pk);                           // keys 64-127
+                    tmem_st32(tS + 96, pk);
+                }
+                load2(0);
+                {
+                    uint32_t pk[32];
+                    pack2(pk);                           // keys 0-63
+                    tmem_st32(tS + 64, pk);
                 }
                 l = l * alpha + (rs2.x + rs2.y);
                 m = m_new;

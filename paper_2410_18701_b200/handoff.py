@@ -105,7 +105,7 @@ class PrefillServer:
         for i in range(0, len(order), self.chunk):
             part = order[i:i + self.chunk]
             items = [(q.qid, q.l_q) + tuple(self.kv_source(q.qid, q.l_q)) for q in part]
-            if self.attention:
+            if self.attention and self.wl.head_dim == 128:   # a8 is built for head_dim 128
                 prefill_attention_batch(self.wl, self.device, items, grouping="length")
             for qid, n, K, V in items:
                 dst = self.decode_ranks[self.pins[qid]]

@@ -89,7 +89,7 @@ def test_handoff_replay_bit_exact(name):
         p.start()
     res = {}
     for _ in procs:
-        r = q.get(timeout=600)
+        r = q.get(timeout=300)
         res[r[0]] = r[1:]
     for p in procs:
         p.join(timeout=60)
