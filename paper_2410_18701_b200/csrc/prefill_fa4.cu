@@ -227,41 +227,76 @@ prefill_fa4_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
                 mbar_wait(&sm.k_full[t & 1], (t >> 1) & 1);
                 tc_fence_after();
             };
+            // Event-driven: P.V (and the next S) of whichever group published its P
+            // first -- a strict 0,1,0,1 order would hold one group's MMAs behind the
+            // other group's softmax.  K(j) / V(j) are released once every group that
+            // uses them issued its S(j) / P.V(j).
             for (int w = blockIdx.x; w < p.n_work; w += gridDim.x) {
                 const Work wk = decode_work(p, w);
                 const int nk = wk.has1 ? wk.n1 : wk.n0;
+                const int n[2] = {wk.n0, wk.n1};
                 mbar_wait(&sm.q_full[0], nq[0] & 1);
                 if (wk.has1) mbar_wait(&sm.q_full[1], nq[1] & 1);
                 wait_k(0);
                 issue_s(0, 0, wk.n0);
                 if (wk.has1) issue_s(1, 0, wk.n1);
                 umma_commit(&sm.k_empty[kc & 1]);
-                for (int j = 0; j < nk; ++j) {
-                    const int vs = (kc + j) & 1, vph = ((kc + j) >> 1) & 1;
-                    bool v_waited = false, k_waited = false;
-                    for (int i = 0; i < 2; ++i) {
-                        const int ni = i == 0 ? wk.n0 : wk.n1;
-                        if (j >= ni) continue;
-                        mbar_wait(&sm.p_full[i], np[i] & 1);      // P_i(j) in TMEM, O_i rescaled
-                        ++np[i];
-                        if (j == 0 && nq[i] > 0) mbar_wait(&sm.o_free[i], (nq[i] - 1) & 1);   // epilogue read O_i
-                        if (!v_waited) {
-                            mbar_wait(&sm.v_full[vs], vph);
-                            v_waited = true;
+                int next[2] = {0, wk.has1 ? 0 : n[1]};     // next P.V per group
+                int k_ready = 0, v_ready = -1;              // K(<= k_ready), V(<= v_ready) waited
+                int s_cnt[4] = {0, 0, 0, 0}, v_cnt[4] = {0, 0, 0, 0};   // per j & 3: S / P.V issued
+                int last = 1;
+                while (next[0] < n[0] || next[1] < n[1]) {
+                    // a group is ready when its P is published and the V / next K tile it
+                    // needs are loaded (never block here: one group may be a tile ahead, and
+                    // the stage it needs frees only when the other group moves on)
+                    auto ready = [&](int c) {
+                        if (next[c] >= n[c] || !mbar_test_wait(&sm.p_full[c], np[c] & 1)) return false;
+                        const int j = next[c];
+                        if (j > v_ready && !mbar_test_wait(&sm.v_full[(kc + j) & 1], ((kc + j) >> 1) & 1))
+                            return false;
+                        if (j + 1 < n[c] && j + 1 > k_ready &&
+                            !mbar_test_wait(&sm.k_full[(kc + j + 1) & 1], ((kc + j + 1) >> 1) & 1))
+                            return false;
+                        return true;
+                    };
+                    int i = -1;
+                    for (int t = 1; t <= 2 && i < 0; ++t) {   // round robin over ready groups
+                        const int c = (last + t) & 1;
+                        if (ready(c)) i = c;
+                    }
+                    if (i < 0) {
+                        __nanosleep(32);
+                        continue;
+                    }
+                    last = i;
+                    const int j = next[i]++;
+                    ++np[i];
+                    if (j == 0 && nq[i] > 0) mbar_wait(&sm.o_free[i], (nq[i] - 1) & 1);   // epilogue read O_i
+                    if (j > v_ready) {
+                        const int t = kc + j;
+                        mbar_wait(&sm.v_full[t & 1], (t >> 1) & 1);
+                        v_ready = j;
+                    }
+                    tc_fence_after();
+                    issue_pv(i, j);
+                    if (j == n[i] - 1) umma_commit(&sm.o_done[i]);
+                    const int v_need = (j < n[0]) + (j < n[1]);
+                    if (++v_cnt[j & 3] == v_need) {          // V(j) consumed by every group
+                        v_cnt[j & 3] = 0;
+                        umma_commit(&sm.v_empty[(kc + j) & 1]);
+                    }
+                    if (j + 1 < n[i]) {
+                        if (j + 1 > k_ready) {
+                            wait_k(j + 1);
+                            k_ready = j + 1;
                         }
-                        tc_fence_after();
-                        issue_pv(i, j);
-                        if (j == ni - 1) umma_commit(&sm.o_done[i]);
-                        if (j + 1 < ni) {
-                            if (!k_waited) {
-                                wait_k(j + 1);
-                                k_waited = true;
-                            }
-                            issue_s(i, j + 1, ni);
+                        issue_s(i, j + 1, n[i]);
+                        const int k_need = (j + 1 < n[0]) + (j + 1 < n[1]);
+                        if (++s_cnt[(j + 1) & 3] == k_need) {   // K(j+1) consumed
+                            s_cnt[(j + 1) & 3] = 0;
+                            umma_commit(&sm.k_empty[(kc + j + 1) & 1]);
                         }
                     }
-                    umma_commit(&sm.v_empty[vs]);                  // both P.V of V(j) issued
-                    if (k_waited) umma_commit(&sm.k_empty[(kc + j + 1) & 1]);   // both S of K(j+1)
                 }
                 ++nq[0];
                 if (wk.has1) ++nq[1];
@@ -285,12 +320,16 @@ prefill_fa4_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
             for (int j = 0; j < n; ++j, ++ns) {
                 mbar_wait(&sm.s_full[grp], ns & 1);
                 tc_fence_after();
-                // The S row in TMEM, 64 columns per tcgen05.ld round trip (at most 64
-                // scores + 32 packed P live in registers): (1) columns 0-63, then 64-127,
-                // for the row max; (2) exp2 / pack of keys 64-127 (still in registers) ->
-                // P columns 96-127; reload keys 0-63, exp2 / pack -> P columns 64-95.  P
-                // (key 2c in the low half of column 64 + c) only overwrites scores that are
-                // already in registers.  Diagonal tile: keys c > lim causally masked (-inf).
+                // The S row in TMEM is read 64 columns per tcgen05.ld round trip (at most 64
+                // scores + 32 packed P live in registers).  P (key 2c in the low half of
+                // column 64 + c) only overwrites scores already in registers: keys 64-127
+                // go first (-> P columns 96-127), then keys 0-63 (-> P columns 64-95).
+                // Diagonal tile: keys c > lim causally masked (-inf).
+                //   fast path (the reference max m is set): exponentials against m while
+                //   the chunk max is checked; a chunk whose max exceeds m + rescale_t in
+                //   any lane of the warp moves the reference (keys 64-127: nothing stored
+                //   yet, recompute; keys 0-63: also rescale the stored P of 64-127);
+                //   first tile of a work item: the row max first (two passes).
                 const bool diag = j == n - 1;
                 const int lim = qi - j * FN;
                 uint32_t ra[32], rb[32];
@@ -315,19 +354,8 @@ prefill_fa4_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
                     }
                     return fmaxf(a0, a1);
                 };
-                load2(0);
-                float mx = max2(-INFINITY);
-                load2(64);
-                mx = max2(mx);
-                mx *= p.scale_log2;                      // -inf stays -inf
-                // lazy rescale (see the header); a row with only masked keys so far keeps
-                // exp2 finite: ex2(-inf - 0) = 0
-                const float m_new = (mx > m + p.rescale_t || m == -INFINITY) ? fmaxf(m, mx) : m;
-                const float mref = (m_new == -INFINITY) ? 0.f : m_new;
-                const float alpha = ex2(m - mref);
-                const float2 nr2 = make_float2(-mref, -mref);
-                float2 rs2 = make_float2(0.f, 0.f);
-                auto pack2 = [&](uint32_t (&pk)[32]) {
+                auto pack2 = [&](uint32_t (&pk)[32], float mref, float2 &rs2) {
+                    const float2 nr2 = make_float2(-mref, -mref);
 #pragma unroll
                     for (int i = 0; i < 64; i += 2) {
                         const uint32_t x0 = i < 32 ? ra[i] : rb[i - 32], x1 = i < 32 ? ra[i + 1] : rb[i - 31];
@@ -339,19 +367,77 @@ prefill_fa4_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
                         pk[i / 2] = *reinterpret_cast<const uint32_t *>(&b);
                     }
                 };
-                {
+                // the new reference for a chunk max mx (log2 units): moves only past m + t
+                auto move_ref = [&](float mx) {
+                    return (mx > m + p.rescale_t || m == -INFINITY) ? fmaxf(m, mx) : m;
+                };
+                float alpha = 1.f;                       // O and l scale of this tile
+                float2 rs2 = make_float2(0.f, 0.f);
+                float mref = m;
+                if (m == -INFINITY) {                    // first tile: the row max first
+                    load2(0);
+                    float mx = max2(-INFINITY);
+                    load2(64);
+                    mx = max2(mx) * p.scale_log2;        // -inf stays -inf
+                    const float m_new = move_ref(mx);
+                    mref = (m_new == -INFINITY) ? 0.f : m_new;   // keeps exp2 finite
+                    alpha = ex2(m - mref);
+                    m = m_new;
                     uint32_t pk[32];
-                    pack2(pk);                           // keys 64-127
+                    pack2(pk, mref, rs2);                // keys 64-127
+                    tmem_st32(tS + 96, pk);
+                } else {
+                    load2(64);
+                    uint32_t pk[32];
+                    pack2(pk, mref, rs2);                // keys 64-127 against m
+                    const float mx = max2(-INFINITY) * p.scale_log2;
+                    if (__any_sync(FULL_MASK, mx > m + p.rescale_t)) {
+                        const float m_new = move_ref(mx);
+                        mref = m_new;
+                        alpha = ex2(m - mref);
+                        m = m_new;
+                        rs2 = make_float2(0.f, 0.f);
+                        pack2(pk, mref, rs2);            // recompute against the new reference
+                    }
                     tmem_st32(tS + 96, pk);
                 }
                 load2(0);
                 {
                     uint32_t pk[32];
-                    pack2(pk);                           // keys 0-63
+                    const float mref0 = mref;
+                    pack2(pk, mref, rs2);                // keys 0-63
+                    const float mx = max2(-INFINITY) * p.scale_log2;
+                    if (__any_sync(FULL_MASK, mx > m + p.rescale_t)) {
+                        // the reference moves after keys 64-127 were stored: rescale them
+                        const float m_new = move_ref(mx);
+                        const float f = ex2(mref0 - m_new);   // 1 in the lanes that keep m
+                        mref = m_new;
+                        alpha *= f;
+                        m = m_new;
+                        rs2 = make_float2(rs2.x * 0.f, rs2.y * 0.f);
+                        {
+                            uint32_t ph[32];
+                            tmem_ld32(tS + 96, ph);
+                            tmem_wait_ld();
+                            float2 r2 = make_float2(0.f, 0.f);
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) {
+                                __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162 *>(&ph[i]);
+                                float2 v = __bfloat1622float2(b);
+                                v.x *= f;
+                                v.y *= f;
+                                r2 = fadd2(r2, v);
+                                b = __floats2bfloat162_rn(v.x, v.y);
+                                ph[i] = *reinterpret_cast<const uint32_t *>(&b);
+                            }
+                            tmem_st32(tS + 96, ph);
+                            rs2 = r2;                    // keys 64-127 (bf16-rounded sums)
+                        }
+                        pack2(pk, mref, rs2);            // keys 0-63 against the new reference
+                    }
                     tmem_st32(tS + 64, pk);
                 }
                 l = l * alpha + (rs2.x + rs2.y);
-                m = m_new;
                 // O_grp rescale: holding S(j) means PV(j-1) is complete (issued before S(j))
                 if (j > 0 && __any_sync(FULL_MASK, alpha != 1.f)) {
                     if (lane == 0) atomicAdd(&g_fa4_rescales, 1ull);
