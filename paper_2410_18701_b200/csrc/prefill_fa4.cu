@@ -264,10 +264,7 @@ prefill_fa4_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
                         const int c = (last + t) & 1;
                         if (ready(c)) i = c;
                     }
-                    if (i < 0) {
-                        __nanosleep(32);
-                        continue;
-                    }
+                    if (i < 0) continue;                     // spin (test_wait does not suspend)
                     last = i;
                     const int j = next[i]++;
                     ++np[i];
