@@ -1,5 +1,10 @@
 // prefill_fa4.cu -- a8 prefill attention, the FA4 layout on the 5th-gen tensor cores.
 //
+// EXPERIMENT BUILD ONLY (BATON_EXPERIMENTS=1, BATON_PF_KERNEL=2): passes every prefill /
+// varlen / shaping parity test, but measured slower than the round-1 kernel
+// (prefill_attention.cu) on every prompt shape -- DESIGN.md §6.3 has the numbers and
+// the ncu reading (the softmax waits for S: S_i(j+1) can only follow PV_i(j)).
+//
 // What it computes ("all original queries ... are initially prefilled";
 // P:L215 asynchronous P&D): causal softmax(Q K^T / sqrt(D)) V of each new prompt over
 // its own tokens -- row i is the textbook SDPA of query token i over keys
@@ -42,10 +47,10 @@
 #include <algorithm>
 #include <cstdlib>
 
-#include "common.cuh"
-#include "kernels.h"
-#include "tcgen05.cuh"
-#include "tma.h"
+#include "../common.cuh"
+#include "../kernels.h"
+#include "../tcgen05.cuh"
+#include "../tma.h"
 
 namespace baton {
 

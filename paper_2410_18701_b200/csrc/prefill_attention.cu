@@ -450,18 +450,19 @@ cudaError_t launch_pf(const CUtensorMap &mq, const CUtensorMap &mk, const CUtens
 int prefill_varlen_max_prompts() { return VL_MAXP; }
 
 namespace {
-// the FA4-layout kernel (prefill_fa4.cu) is the prefill; experiment builds can select
-// this file's round-1 kernel with BATON_PF_KERNEL=1 for A/B runs
+// The FA4-layout kernel (prefill_fa4.cu) is an experiment: measured slower than this
+// file's kernel on every prompt shape, so the product prefill is
+// this file's kernel; experiment builds select FA4 with BATON_PF_KERNEL=2
 bool use_fa4() {
 #if BATON_EXPERIMENTS
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("BATON_PF_KERNEL");
-        v = e ? atoi(e) : 0;
+        v = e ? atoi(e) : 1;
     }
-    return v == 0;
+    return v == 2;
 #else
-    return true;
+    return false;
 #endif
 }
 }  // namespace
@@ -470,7 +471,9 @@ cudaError_t launch_prefill_attention_varlen(const void *q, const void *k, const 
                                             const int32_t *cu_lens, int n, int q_heads, int kv_heads,
                                             int head_dim, float scale, cudaStream_t s) {
     if (head_dim != PF_D || n < 1 || n > VL_MAXP || cu_lens[0] != 0) return cudaErrorInvalidValue;
+#if BATON_EXPERIMENTS
     if (use_fa4()) return launch_prefill_fa4_varlen(q, k, v, out, cu_lens, n, q_heads, kv_heads, scale, pf_rescale_t(), s);
+#endif
     PfParams p{};
     // (prompt, query tile) entries, heaviest first (key tiles up to the diagonal),
     // ties by prompt then tile: a longest-processing-time order over all prompts
@@ -554,8 +557,12 @@ extern "C" long long baton_debug_prefill_rescales(int reset) {
         const unsigned long long z = 0;
         if (cudaMemcpyToSymbol(baton::g_pf_rescales, &z, sizeof(z)) != cudaSuccess) return -1;
     }
+#if BATON_EXPERIMENTS
     const long long f = baton::fa4_rescale_count(reset != 0);
     return f < 0 ? -1 : (long long)v + f;
+#else
+    return (long long)v;
+#endif
 }
 extern "C" int baton_debug_prefill_rescale_t(float t) {
     baton::g_rescale_override = t;
