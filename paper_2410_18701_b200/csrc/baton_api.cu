@@ -26,6 +26,7 @@ struct baton_state {
     int32_t *d_S = nullptr, *d_lens = nullptr, *d_pad = nullptr;
     int32_t *tickets = nullptr;
     float *partial = nullptr;
+    float *partial2 = nullptr;    // the decode step's second split-K buffer (deferred GQA merge)
     int max_chunks = 0;
     size_t layer_elems = 0;   // elements of one layer of the K (or V) cache
     bool prev_decode = false; // the shard's last launch was a decode kernel (DecodeArgs::early)
@@ -118,7 +119,9 @@ size_t baton_decode_workspace_bytes(const baton_shape *s) {
 
 size_t baton_workspace_bytes(const baton_shape *s) {
     if (!shape_ok(s)) return 0;
-    return meta_bytes(s) + baton_decode_workspace_bytes(s);
+    // + a second partial buffer: consecutive layers of a decode step alternate them
+    return meta_bytes(s) + baton_decode_workspace_bytes(s) +
+           align256(decode_partial_bytes(s->slots, s->q_heads, s->head_dim, s->max_ctx));
 }
 
 int baton_create(const baton_config *cfg, void *stream, baton_state **out) {
@@ -144,6 +147,7 @@ int baton_create(const baton_config *cfg, void *stream, baton_state **out) {
     st->d_pad = st->d_lens + s.slots;
     st->tickets = reinterpret_cast<int32_t *>(ws + meta_bytes(&s));
     st->partial = reinterpret_cast<float *>(ws + meta_bytes(&s) + ticket_region(&s));
+    st->partial2 = reinterpret_cast<float *>(ws + meta_bytes(&s) + baton_decode_workspace_bytes(&s));
     st->max_chunks = ceil_div(s.max_ctx, CHUNK);
     st->layer_elems = (size_t)s.slots * s.kv_heads * s.max_ctx * s.head_dim;
     cudaStream_t cs = as_stream(stream);
@@ -303,14 +307,30 @@ int baton_decode_step(baton_state *st, const void *q, const void *k_new, const v
         if ((e = cudaStreamBeginCapture(st->cap_stream, cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
             return cuda_status(e);
         e = launch_mask_update(st->cfg.mask, st->d_S, st->d_lens, s.slots, s.max_ctx, st->cap_stream);
+        // GQA: layer l's split-K merge runs at the start of layer l+1's launch (buffers
+        // alternate by layer), so no combine kernel sits in the layer chain; one
+        // combine after the last layer
+        const bool defer = gqa_supported(s.q_heads, s.kv_heads, s.head_dim);
+        DecodeArgs last{};
         for (int l = 0; l < s.layers && e == cudaSuccess; ++l) {
             const __nv_bfloat16 *ql = static_cast<const __nv_bfloat16 *>(q) + l * qstride;
             const __nv_bfloat16 *kl = static_cast<const __nv_bfloat16 *>(k_new) + l * kstride;
             const __nv_bfloat16 *vl = static_cast<const __nv_bfloat16 *>(v_new) + l * kstride;
             __nv_bfloat16 *ol = static_cast<__nv_bfloat16 *>(out) + l * qstride;
             // layer 0 follows the mask update (writes lens): no early prefetch
-            e = launch_decode_attention(layer_args(st, l, ql, kl, vl, ol, l > 0), st->cap_stream);
+            DecodeArgs a = layer_args(st, l, ql, kl, vl, ol, l > 0);
+            if (defer) {
+                a.defer_merge = true;
+                a.partial = (l & 1) ? st->partial2 : st->partial;
+                if (l > 0) {
+                    a.prev_partial = last.partial;
+                    a.prev_out = last.out;
+                }
+            }
+            e = launch_decode_attention(a, st->cap_stream);
+            last = a;
         }
+        if (defer && e == cudaSuccess && s.layers > 0) e = launch_gqa_combine(last, st->cap_stream);
         cudaGraph_t g = nullptr;
         const cudaError_t e2 = cudaStreamEndCapture(st->cap_stream, &g);
         if (e == cudaSuccess) e = e2;

@@ -16,6 +16,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "gqa_merge.cuh"
 #include "sched.cuh"
 #include "tma.h"
 
@@ -33,10 +34,9 @@ BATON_DEV uint32_t pack_bf16(float lo, float hi) {
 
 // Split-K merge for multi-chunk queries.  Grid = one 4-warp CTA per SM (a GQA CTA
 // keeps two warps on one SM sub-partition; more combine warps resident there would
-// block the next layer's CTA from entering until the combine drains).  A warp merges
-// two (slot, q head) pairs at a time, 16 lanes x 8 dims each; chunks in ascending
-// order, eight per round trip (online max).  Single-chunk queries were written by
-// the attention kernel.
+// block the next layer's CTA from entering until the combine drains).  The merge
+// itself is gqa_merge_pairs (gqa_merge.cuh), shared with the decode-step path that
+// runs it at the start of the next layer's launch.
 __global__ void __launch_bounds__(128) decode_combine_kernel(const int32_t *__restrict__ lens,
                                                              const float *__restrict__ partial,
                                                              __nv_bfloat16 *__restrict__ out, int B,
@@ -46,62 +46,9 @@ __global__ void __launch_bounds__(128) decode_combine_kernel(const int32_t *__re
     // Safe because that phase reads only lens/pad/mask and cache rows other than
     // lens-1, which neither launch writes; everything it writes waits for us.
     griddep_launch_dependents();
-    const int lane = threadIdx.x & 31, hl = lane & 15;
-    int gw = blockIdx.x * 4 + (threadIdx.x >> 5);
-    const int nw = gridDim.x * 4;
-    const int npairs = B * Hq;
-    constexpr int R = D + PREC_PAD, NB = 8;
-    // lens is stable since the mask update: read the first pair's before the wait
-    int pair = gw * 2 + (lane >> 4);
-    int L = pair < npairs ? lens[pair / Hq] : 0;
     griddep_wait();
-    for (; gw * 2 < npairs; gw += nw, pair = gw * 2 + (lane >> 4), L = pair < npairs ? lens[pair / Hq] : 0) {
-        const int nch = (L + CHUNK - 1) / CHUNK;
-        if (pair >= npairs || nch <= 1) continue;
-        const float *pp = partial + (size_t)pair * max_chunks * R + hl * 8;
-        float Mc = -INFINITY, Lc = 0.f, Oc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        for (int c0 = 0; c0 < nch; c0 += NB) {
-            float m[NB], l[NB];
-            float4 va[NB], vb[NB];
-#pragma unroll
-            for (int j = 0; j < NB; ++j) {
-                const bool ok = c0 + j < nch;
-                const float *r = pp + (ok ? c0 + j : c0) * R;
-                m[j] = ok ? __ldcg(r - hl * 8 + D) : -INFINITY;
-                l[j] = ok ? __ldcg(r - hl * 8 + D + 1) : 0.f;
-                va[j] = __ldcg(reinterpret_cast<const float4 *>(r));
-                vb[j] = __ldcg(reinterpret_cast<const float4 *>(r + 4));
-            }
-            float Mn = Mc;
-#pragma unroll
-            for (int j = 0; j < NB; ++j) Mn = fmaxf(Mn, m[j]);
-            const float al = (Mc == -INFINITY) ? 0.f : ex2(Mc - Mn);
-            Lc *= al;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) Oc[i] *= al;
-#pragma unroll
-            for (int j = 0; j < NB; ++j) {
-                const float f = (m[j] == -INFINITY) ? 0.f : ex2(m[j] - Mn);
-                Lc = fmaf(f, l[j], Lc);
-                Oc[0] = fmaf(f, va[j].x, Oc[0]);
-                Oc[1] = fmaf(f, va[j].y, Oc[1]);
-                Oc[2] = fmaf(f, va[j].z, Oc[2]);
-                Oc[3] = fmaf(f, va[j].w, Oc[3]);
-                Oc[4] = fmaf(f, vb[j].x, Oc[4]);
-                Oc[5] = fmaf(f, vb[j].y, Oc[5]);
-                Oc[6] = fmaf(f, vb[j].z, Oc[6]);
-                Oc[7] = fmaf(f, vb[j].w, Oc[7]);
-            }
-            Mc = Mn;
-        }
-        const float inv = Lc > 0.f ? 1.f / Lc : 0.f;
-        uint4 w;
-        w.x = pack_bf16(Oc[0] * inv, Oc[1] * inv);
-        w.y = pack_bf16(Oc[2] * inv, Oc[3] * inv);
-        w.z = pack_bf16(Oc[4] * inv, Oc[5] * inv);
-        w.w = pack_bf16(Oc[6] * inv, Oc[7] * inv);
-        *reinterpret_cast<uint4 *>(out + (size_t)pair * D + hl * 8) = w;
-    }
+    gqa_merge_pairs(lens, partial, out, B, Hq, max_chunks, blockIdx.x * 4 + (threadIdx.x >> 5),
+                    gridDim.x * 4, threadIdx.x & 31);
 }
 
 // The same merge, started before the attention grid completes: a CTA owns whole
@@ -235,7 +182,7 @@ cudaError_t launch_decode_gqa(const DecodeArgs &a, cudaStream_t s) {
     if (v != 20 && v != 21) return launch_gqa_experiment(v, a, s);
 #endif
     cudaError_t e = launch_decode_gqa_tc(a, s, false);
-    if (e != cudaSuccess || a.dry) return e;
+    if (e != cudaSuccess || a.dry || a.defer_merge) return e;
     return launch_gqa_combine(a, s);
 }
 

@@ -31,6 +31,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "gqa_merge.cuh"
 #include "kernels.h"
 #include "sched.cuh"
 #include "tcgen05.cuh"
@@ -111,6 +112,8 @@ struct TParams {
     float scale_log2;
     bool early;
     bool fused;                              // in-kernel split-K merge (no combine launch)
+    const float *prev_partial;               // decode step: merge the previous layer's split-K
+    __nv_bfloat16 *prev_out;                 // partials at the start (DecodeArgs::defer_merge)
     bool publish;                            // count published chunks per (slot, kv group) for a
                                              // combine that merges as soon as a group is complete
 };
@@ -413,6 +416,11 @@ decode_gqa_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_cons
             griddep_wait();
             griddep_launch_dependents();
         }
+        // decode step: the previous layer's split-K merge (its partials are complete and
+        // visible once griddepcontrol.wait returned) while this layer's first K/V stream in
+        if (p.prev_partial)
+            gqa_merge_pairs(p.lens, p.prev_partial, p.prev_out, p.B, p.Hq, p.max_chunks,
+                            blockIdx.x * 8 + warp, gridDim.x * 8, lane);
         for (int b = blockIdx.x; b < p.B; b += gridDim.x) {   // empty slots -> zero rows (C6)
             if (p.lens[b] <= 0) {
                 uint4 *o = reinterpret_cast<uint4 *>(p.out + (size_t)b * p.Hq * D);
@@ -642,6 +650,8 @@ cudaError_t launch_decode_gqa_tc(const DecodeArgs &a, cudaStream_t s, bool fused
     p.partial = a.partial;
     p.tickets = a.tickets;
     p.fused = fused;
+    p.prev_partial = a.prev_partial;
+    p.prev_out = static_cast<__nv_bfloat16 *>(a.prev_out);
     p.publish = publish && !fused;
     if (fused && a.max_chunks > 32) return cudaErrorInvalidValue;   // see TSmem::mf
     p.B = a.slots;

@@ -32,6 +32,13 @@ struct DecodeArgs {
     int32_t *tickets;               // [slots][q_heads] (+2 work counters), zero between calls
     int slots, q_heads, kv_heads, head_dim, max_ctx, max_chunks;
     float scale;
+    // decode-step graph, GQA: this launch leaves the split-K merge of its multi-chunk
+    // queries to the next launch (no combine kernel in the layer chain), and merges
+    // the previous layer's (prev_partial -> prev_out) at its own start, while its first
+    // K/V tiles stream in.  The step's last layer is followed by one combine.
+    bool defer_merge = false;
+    const float *prev_partial = nullptr;
+    void *prev_out = nullptr;
 };
 size_t decode_partial_bytes(int slots, int q_heads, int head_dim, int max_ctx);
 size_t decode_ticket_bytes(int slots, int q_heads);
