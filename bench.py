@@ -348,6 +348,8 @@ class Ctx:
         for e in pl.queue:
             if e.home == rank:
                 eng.stash.put(e.qid, *hist(e.qid, e.length))
+        if eng.device_flags:
+            eng._sync_targets()          # device completion targets of the embedded queries
         torch.cuda.synchronize()
         return eng
 

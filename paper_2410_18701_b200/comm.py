@@ -8,9 +8,13 @@ tests) gives every rank the same view, and the replicated planner
 (scheduler.py) then takes identical insert/remove decisions without a
 broadcast.
 
-The flags are known on the host when the decode of the iteration has been
-*enqueued*, so the all-gather runs on its own stream: it does not wait for the
-decode kernels, and the host blocks only for the (tiny) collective itself.
+By default (Engine device_flags, world > 1) each rank computes its flags ON THE
+DEVICE after the decode -- a slot's live length reached its target, the stand-in
+for the model's EOS, which a real model also only knows on the device -- and the
+all-gather runs on the decode stream behind it; the host planner waits for the
+gathered flags (one small D2H per iteration).  With host bookkeeping instead
+(device_flags=False) the flags are known when the decode is enqueued, and the
+gather runs on its own stream without waiting for the decode.
 """
 import torch
 import torch.distributed as dist
@@ -26,9 +30,23 @@ def _comm_stream(device):
 
 
 def gather_completion_flags(local_flags, world, group=None, device=None):
+    """local_flags: a list (host bookkeeping) or an int32 device tensor computed on the
+    current stream after the decode (Engine device_flags).  Returns every rank's flags
+    as a list, in rank order."""
     if world == 1:
-        return list(local_flags)
+        return local_flags.tolist() if torch.is_tensor(local_flags) else list(local_flags)
     backend = dist.get_backend(group)
+    if torch.is_tensor(local_flags):
+        if backend == "nccl":
+            # on the current (decode) stream: the gather runs after the decode, NCCL
+            # over NVLink, then one small D2H that the host planner waits for
+            out = torch.empty(world * local_flags.numel(), dtype=torch.int32, device=local_flags.device)
+            dist.all_gather_into_tensor(out, local_flags.contiguous(), group=group)
+            return out.cpu().tolist()
+        t = local_flags.cpu()
+        parts = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(parts, t, group=group)
+        return torch.cat(parts).tolist()
     if backend == "nccl" and device is not None:
         with torch.cuda.stream(_comm_stream(device)):
             t = torch.tensor(local_flags, dtype=torch.int32, device=device)

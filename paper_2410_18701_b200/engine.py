@@ -58,12 +58,18 @@ class Engine:
                  keep_layers=None, token_source=None, prefill_source=None, use_graph=True,
                  stash_host=False, policy="baton", prefill_attention=False, async_prefill=False,
                  prefill_lookahead=None, prefill_grouping=None, trace=False,
-                 stash_hbm_bytes=None, pins=None):
+                 stash_hbm_bytes=None, pins=None, device_flags=None):
         """prefill_grouping: "length" -- a8 of several fresh prompts runs in batches of
         similar length, one varlen launch each (the PD method's prefill, P:L220;
         default for policy "pd"); None -- batched only when the prompts are short.
         trace: record a CUDA event after every iteration (per-iteration device time
-        for the JSONL log, ``write_log``)."""
+        for the JSONL log, ``write_log``).
+        device_flags (default: on when world > 1): each rank's completion flags are
+        computed on the device from the live lengths after the decode (lens >= the
+        slot's target length l_q + A, the stand-in for the model's EOS) and all-gathered
+        from there; the replicated planner then decides on what the ranks' devices
+        reported.  Off: the planner's own bookkeeping (identical decisions, no exchange
+        needed on one GPU)."""
         self.wl = wl
         self.rank = rank
         self.world = world
@@ -117,6 +123,9 @@ class Engine:
         self.prefill_grouping = prefill_grouping or ("length" if policy == "pd" else None)
         self.trace = trace
         self.trace_events = []
+        self.device_flags = (world > 1) if device_flags is None else device_flags
+        self.d_target = torch.zeros((self.B,), dtype=torch.int32, device=self.device)
+        self._target_host = [0] * self.B
 
     def register_staging(self, q, k, v):
         """Declare a fixed (q, k_new, v_new) buffer set a token source may return
@@ -266,15 +275,31 @@ class Engine:
         self.gathers += 1
         return out
 
+    def _device_flags(self):
+        """This rank's completion flags on the device, after the decode: the slot's live
+        length reached its target (l_q + A)."""
+        return ((self.shard.d_lens >= self.d_target) & (self.d_target > 0)).to(torch.int32)
+
+    def _sync_targets(self):
+        """The device copy of each local slot's target length, after the splice."""
+        pl = self.planner
+        tgt = [0] * self.B
+        for g, q in pl.live():
+            if pl.rank_of(g) == self.rank and g not in pl.raw:
+                tgt[pl.local(g)] = pl.meta[q].l_q + pl.meta[q].A
+        if tgt != self._target_host:
+            self._target_host = tgt
+            self.d_target.copy_(torch.tensor(tgt, dtype=torch.int32), non_blocking=True)
+
     def iteration(self):
         pl = self.planner
         stats = StepStats(pl.t)
         flags = None
         if pl.t > 0:
             self.decode(stats)
-            local = pl.local_completion_flags(self.rank)
-            # completion flags + occupancy summary of every rank
+            # completion flags of every rank (SURVEY.md §8(e))
             if self.world > 1:
+                local = self._device_flags() if self.device_flags else pl.local_completion_flags(self.rank)
                 with torch.cuda.nvtx.range("baton.allgather"):
                     flags = self._gather_flags(local)
         d = pl.plan(flags)
@@ -282,6 +307,8 @@ class Engine:
         stats.completed = sum(1 for g, _ in d.completed if pl.rank_of(g) == self.rank)
         with torch.cuda.nvtx.range("baton.splice"):
             self._splice(d, stats)
+        if self.device_flags:
+            self._sync_targets()
         if self.async_prefill:
             self._prefetch()
         stats.S = self.shard.S
