@@ -81,6 +81,11 @@ BATON_DEV float2 ffma2(float2 a, float2 b, float2 c) {
     asm("mov.b64 {%0,%1}, %2;" : "=f"(d.x), "=f"(d.y) : "l"(D));
     return d;
 }
+BATON_DEV float fmax3(float a, float b, float c) {   // SASS FMNMX3
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
 BATON_DEV float2 fadd2(float2 a, float2 b) {
     uint64_t A, B, D;
     asm("mov.b64 %0, {%1,%2};" : "=l"(A) : "f"(a.x), "f"(a.y));
@@ -285,7 +290,6 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
             // Masked keys become -inf in the RAW scores; the scale (> 0) is folded into
             // the exponent (one FFMA + ex2 per key) and the row max is taken raw.  Tiles
             // off the diagonal (and prefill has no mask) skip the per-key tests.
-            float mx = -INFINITY;
             if (diag || ext) {
 #pragma unroll
                 for (int c = 0; c < 2; ++c)
@@ -293,13 +297,19 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
                     for (int i = 0; i < 32; ++i) {
                         const bool dead = (diag && kbase + c * 32 + i > off + qi) || (ext && mk[c * 32 + i] == 0);
                         if (dead) r[c][i] = __float_as_uint(-INFINITY);
-                        mx = fmaxf(mx, __uint_as_float(r[c][i]));
                     }
-            } else {
+            }
+            float mx;
+            {   // row max: 3-input FMNMX3 in four independent chains
+                float a0 = -INFINITY, a1 = -INFINITY, a2 = -INFINITY, a3 = -INFINITY;
 #pragma unroll
-                for (int c = 0; c < 2; ++c)
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(r[c][i]));
+                for (int i = 0; i < 32; i += 4) {
+                    a0 = fmax3(a0, __uint_as_float(r[0][i]), __uint_as_float(r[0][i + 1]));
+                    a1 = fmax3(a1, __uint_as_float(r[0][i + 2]), __uint_as_float(r[0][i + 3]));
+                    a2 = fmax3(a2, __uint_as_float(r[1][i]), __uint_as_float(r[1][i + 1]));
+                    a3 = fmax3(a3, __uint_as_float(r[1][i + 2]), __uint_as_float(r[1][i + 3]));
+                }
+                mx = fmax3(fmaxf(a0, a1), a2, a3);
             }
             mx *= p.scale_log2;   // -inf stays -inf
             // Lazy rescale: P is taken relative to a reference max m that moves only
