@@ -74,6 +74,10 @@ typedef struct {
 } baton_config;
 
 /* ---------------------------------------------------------------- lifetime */
+/* Bytes of a shard's workspace: the device metadata copies, two split-K partial
+ * buffers (consecutive layers of baton_decode_step alternate them: a GQA layer's merge
+ * runs in the next layer's launch), the tickets / work counters.  Its last
+ * baton_decode_workspace_bytes(shape) bytes have the stateless call's layout. */
 size_t baton_workspace_bytes(const baton_shape *shape);
 /* Bytes of the workspace the stateless baton_decode_attention() needs. */
 size_t baton_decode_workspace_bytes(const baton_shape *shape);

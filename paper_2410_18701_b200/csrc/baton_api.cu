@@ -145,9 +145,13 @@ int baton_create(const baton_config *cfg, void *stream, baton_state **out) {
     st->d_S = reinterpret_cast<int32_t *>(ws);
     st->d_lens = st->d_S + 1;
     st->d_pad = st->d_lens + s.slots;
-    st->tickets = reinterpret_cast<int32_t *>(ws + meta_bytes(&s));
-    st->partial = reinterpret_cast<float *>(ws + meta_bytes(&s) + ticket_region(&s));
-    st->partial2 = reinterpret_cast<float *>(ws + meta_bytes(&s) + baton_decode_workspace_bytes(&s));
+    // [meta | second partial buffer | tickets + counters | partial buffer]: the last
+    // baton_decode_workspace_bytes are the stateless decode's layout (the binding hands
+    // that tail to baton_decode_attention)
+    const size_t p2 = align256(decode_partial_bytes(s.slots, s.q_heads, s.head_dim, s.max_ctx));
+    st->partial2 = reinterpret_cast<float *>(ws + meta_bytes(&s));
+    st->tickets = reinterpret_cast<int32_t *>(ws + meta_bytes(&s) + p2);
+    st->partial = reinterpret_cast<float *>(ws + meta_bytes(&s) + p2 + ticket_region(&s));
     st->max_chunks = ceil_div(s.max_ctx, CHUNK);
     st->layer_elems = (size_t)s.slots * s.kv_heads * s.max_ctx * s.head_dim;
     cudaStream_t cs = as_stream(stream);
