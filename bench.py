@@ -859,12 +859,11 @@ def summarize(args, r, world, red):
     splice_s = sum(w["splice_s"] for w in wins)
     achieved = attn_bytes / attn_s / 1e9 if attn_s else 0.0
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "r02_traffic.json")
-    if not os.path.exists(tp):
-        tp = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    tp = os.path.join(ROOT, "profiles", "r02_traffic.json" if args.config == "7b"
+                      else f"r02_traffic_{args.config}.json")
     kernel = {"7b": "decode_attention_kernel<128, 4, 2, 3>", "13b": "decode_attention_kernel<128, 4, 2, 3>",
               "stress": "decode_attention_kernel<128, 4, 2, 3>", "70b": "decode_gqa_tc_kernel"}[args.config]
-    if os.path.exists(tp) and args.config in ("7b",):
+    if os.path.exists(tp):
         traffic = json.load(open(tp))["traffic_bytes"]
     all_iter = sum((w["iter_ms"] for w in wins), [])
     line = {
