@@ -51,6 +51,7 @@ __global__ void __launch_bounds__(128) decode_combine_kernel(const int32_t *__re
                     gridDim.x * 4, threadIdx.x & 31);
 }
 
+#if BATON_EXPERIMENTS
 // The same merge, started before the attention grid completes: a CTA owns whole
 // (slot, kv group)s -- 4 warps x 2 pairs = the group's 8 q heads -- and polls the
 // group's ticket (chunks published by the attention kernel's P.V issuers, release
@@ -133,14 +134,18 @@ __global__ void __launch_bounds__(128) decode_combine_spin_kernel(const int32_t 
     }
 }
 
+#endif  // BATON_EXPERIMENTS
+
 }  // namespace
 
+#if BATON_EXPERIMENTS
 cudaError_t launch_gqa_combine_spin(const DecodeArgs &a, cudaStream_t s) {
     const int num_sms = device_sms();
     return launch_pdl(decode_combine_spin_kernel, dim3(num_sms), dim3(128), 0, s, a.lens,
                       (const float *)a.partial, a.tickets, static_cast<__nv_bfloat16 *>(a.out), a.slots,
                       a.q_heads, a.max_chunks);
 }
+#endif
 
 bool gqa_supported(int q_heads, int kv_heads, int head_dim) {
     return head_dim == D && kv_heads > 0 && q_heads == GS * kv_heads;

@@ -403,7 +403,7 @@ decode_gqa_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_cons
                 umma_commit(&sm.o_done[g]);
                 umma_commit(&sm.empty[e.stage]);
                 if (trace && g == 0 && n < 16) tr[7 + 4 * n] = tt_now();
-                if (p.publish) {
+                if (BATON_EXPERIMENTS && p.publish) {   // variant 23 (experiment builds)
                     publish();
                     if (e.multi) pending = e.bh0;
                 }
@@ -547,7 +547,7 @@ decode_gqa_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_cons
                             pp[D + 1] = lt[h];
                         }
                     }
-                    if (p.publish) mbar_arrive(&sm.pub[grp]);   // release.cta: the PV issuer publishes
+                    if (BATON_EXPERIMENTS && p.publish) mbar_arrive(&sm.pub[grp]);   // variant 23
                     if (p.fused) {
                         // in-kernel split-K merge: the group that draws the last ticket of
                         // (slot, kv group) merges the chunks in ascending order.  The
