@@ -404,10 +404,12 @@ def run_window(ctx, win, clocks):
 
     tokens = sum(s.decoded for s in st)
     live_rows = sum(s.live_rows for s in st)      # sum of lens over decoding slots
-    # our kernels per step: mask update + one fused append/attention per layer, the
-    # remove/release mask splice, per stored query an extract copy (+ its remove), the
-    # compaction (copy + mask move), the batched KV copy + mask splice of inserts
-    n_launch = sum(1 + L + (1 if (s.removed or s.released) else 0)
+    # our kernels per step: mask update + one fused append/attention per layer (+ the
+    # GQA split-K combine after the last layer), the remove/release mask splice, per
+    # stored query an extract copy (+ its remove), the compaction (copy + mask move),
+    # the batched KV copy + mask splice of inserts
+    gqa = Hq == 8 * Hkv and D == 128
+    n_launch = sum(1 + L + (1 if gqa else 0) + (1 if (s.removed or s.released) else 0)
                    + (2 * s.stored if s.stored else 0) + (2 if s.compact_rows else 0)
                    + (2 if s.inserted else 0) for s in st)
     tau = 2 * Hkv * D * 2                          # K+V bytes per token per layer
