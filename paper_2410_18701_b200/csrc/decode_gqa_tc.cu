@@ -417,10 +417,12 @@ decode_gqa_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_cons
             griddep_launch_dependents();
         }
         // decode step: the previous layer's split-K merge (its partials are complete and
-        // visible once griddepcontrol.wait returned) while this layer's first K/V stream in
-        if (p.prev_partial)
+        // visible once griddepcontrol.wait returned), by group 1 only: group 0 starts on
+        // this layer's first item at once (4 warps x 2 pairs x 148 CTAs still cover the
+        // 70B shard's 1024 (slot, q head) pairs in one pass)
+        if (p.prev_partial && grp == 1)
             gqa_merge_pairs(p.lens, p.prev_partial, p.prev_out, p.B, p.Hq, p.max_chunks,
-                            blockIdx.x * 8 + warp, gridDim.x * 8, lane);
+                            blockIdx.x * 4 + wq, gridDim.x * 4, lane);
         for (int b = blockIdx.x; b < p.B; b += gridDim.x) {   // empty slots -> zero rows (C6)
             if (p.lens[b] <= 0) {
                 uint4 *o = reinterpret_cast<uint4 *>(p.out + (size_t)b * p.Hq * D);
