@@ -241,6 +241,20 @@ int baton_decode_attention(const void *q, const void *k, const void *v, const ui
 }
 
 namespace {
+// experiment builds: BATON_DEFER_MERGE=0 restores the in-layer merges for A/B runs
+bool defer_merge_enabled() {
+#if BATON_EXPERIMENTS
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("BATON_DEFER_MERGE");
+        v = e ? atoi(e) : 1;
+    }
+    return v != 0;
+#else
+    return true;
+#endif
+}
+
 DecodeArgs layer_args(baton_state *st, int layer, const void *q, const void *k_new, const void *v_new,
                       void *out, bool early) {
     const baton_shape &s = st->sh;
@@ -311,10 +325,11 @@ int baton_decode_step(baton_state *st, const void *q, const void *k_new, const v
         if ((e = cudaStreamBeginCapture(st->cap_stream, cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
             return cuda_status(e);
         e = launch_mask_update(st->cfg.mask, st->d_S, st->d_lens, s.slots, s.max_ctx, st->cap_stream);
-        // GQA: layer l's split-K merge runs at the start of layer l+1's launch (buffers
-        // alternate by layer), so no combine kernel sits in the layer chain; one
-        // combine after the last layer
-        const bool defer = gqa_supported(s.q_heads, s.kv_heads, s.head_dim);
+        // head_dim 128 (GQA and MHA): layer l's split-K merge runs at the start of
+        // layer l+1's launch (buffers alternate by layer), so no merge sits in the
+        // layer chain -- no combine kernel (GQA), no gpu-scope tickets on the
+        // streaming warps (MHA); one combine after the last layer
+        const bool defer = s.head_dim == 128 && defer_merge_enabled();
         DecodeArgs last{};
         for (int l = 0; l < s.layers && e == cudaSuccess; ++l) {
             const __nv_bfloat16 *ql = static_cast<const __nv_bfloat16 *>(q) + l * qstride;

@@ -26,6 +26,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "gqa_merge.cuh"
 #include "sched.cuh"
 
 namespace baton {
@@ -81,6 +82,9 @@ struct Params {
     int B, Hq, Hkv, max_ctx, max_chunks;
     float scale_log2;
     bool early;                              // prefetch before griddepcontrol.wait
+    bool defer;                              // decode step: leave split-K merges to the next launch
+    const float *prev_partial;               // ... and merge the previous layer's (head_dim 128)
+    __nv_bfloat16 *prev_out;
     int trace_slot;                          // debug timeline slot
 };
 
@@ -264,6 +268,13 @@ __global__ void __launch_bounds__((CWARPS + 1) * 32, MINB) decode_attention_kern
         griddep_wait();
         griddep_launch_dependents();
     }
+    // decode step (head_dim 128): the previous layer's split-K merge, its partials
+    // complete and visible now; the producer keeps filling the ring meanwhile
+    if constexpr (D == 128) {
+        if (p.prev_partial)
+            gqa_merge_pairs(p.lens, p.prev_partial, p.prev_out, p.B, p.Hq, p.max_chunks,
+                            blockIdx.x * CWARPS + warp, gridDim.x * CWARPS, lane);
+    }
     // Empty slots produce a zero output row (C6).
     for (int b = blockIdx.x; b < p.B; b += gridDim.x) {
         if (p.lens[b] <= 0) {
@@ -430,7 +441,7 @@ __global__ void __launch_bounds__((CWARPS + 1) * 32, MINB) decode_attention_kern
                 }
             }
             rb ^= 1;
-            if (d.nchunks > 1) {
+            if (d.nchunks > 1 && !p.defer) {
                 // publish the partial: every thread arrives (release, non-blocking);
                 // warp 0 alone waits, then one gpu-scope acq_rel ticket.  The CTA that
                 // draws the last ticket merges the chunks in ascending chunk order.
@@ -531,6 +542,9 @@ cudaError_t launch_d(const DecodeArgs &a, cudaStream_t s) {
     p.max_chunks = a.max_chunks;
     p.scale_log2 = a.scale * 1.4426950408889634f;
     p.early = a.early;
+    p.defer = a.defer_merge && D == 128;
+    p.prev_partial = D == 128 ? a.prev_partial : nullptr;
+    p.prev_out = static_cast<__nv_bfloat16 *>(a.prev_out);
     p.trace_slot = g_mtrace_launch++ % MT_L;
     return launch_pdl(decode_attention_kernel<D, CW, ST, MINB>, dim3(MINB * num_sms),
                       dim3((CW + 1) * 32), smem, s, p);

@@ -148,17 +148,19 @@ def test_graph_step_equals_eager_layers_bitwise():
         assert np.array_equal(a.outputs[k], b.outputs[k])
 
 
-def test_gqa_graph_step_deferred_merge_equals_eager_and_oracle():
-    """The decode-step graph runs layer l's GQA split-K merge at the start of layer
-    l+1's launch (one combine after the last layer).  Multi-chunk queries (lengths
-    past 256 keys) on a GQA-8 shape: every output of the graph path equals the
-    per-layer path (attention + combine per call) bitwise, and the oracle within C13."""
+@pytest.mark.parametrize("hq,hkv", [(16, 2), (8, 8)])
+def test_gqa_graph_step_deferred_merge_equals_eager_and_oracle(hq, hkv):
+    """The decode-step graph runs layer l's split-K merge (head_dim 128: GQA and MHA)
+    at the start of layer l+1's launch (one combine after the last layer).  Multi-chunk
+    queries (lengths past 256 keys, at most 8 chunks): every output of the graph path
+    equals the per-layer path (GQA: attention + combine per call; MHA: the in-kernel
+    last-arriver merge) bitwise, and the oracle within C13."""
     require_cuda()
     from baton_inputs import Workload, Query
     from paper_2410_18701_b200.engine import Engine
     rng = np.random.default_rng(11)
     qs = [Query(i, int(i // 2), int(rng.integers(200, 1500)), int(rng.integers(2, 7))) for i in range(10)]
-    wl = Workload("gqa_defer", qs, layers=3, q_heads=16, kv_heads=2, head_dim=128, slots=4,
+    wl = Workload("gqa_defer", qs, layers=3, q_heads=hq, kv_heads=hkv, head_dim=128, slots=4,
                   max_ctx=2048, scales=SCALES_PEAKY)
     a = Engine(wl, keep_outputs=True, use_graph=True)
     b = Engine(wl, keep_outputs=True, use_graph=False)
