@@ -385,6 +385,7 @@ def run_window(ctx, win, clocks):
     barrier_sync()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     eng.gather_s, eng.gathers = 0.0, 0
+    gc.disable()                     # no collector pause inside the timed region
     h0 = time.time()
     e0.record()
     st, marks = [], []
@@ -395,6 +396,7 @@ def run_window(ctx, win, clocks):
         marks.append(ev)
     e1.record()
     barrier_sync()
+    gc.enable()
     clocks.span(h0, time.time())
     ms = e0.elapsed_time(e1)
     iter_ms = [a.elapsed_time(b) for a, b in zip([e0] + marks[:-1], marks)]
@@ -450,9 +452,11 @@ def run_window(ctx, win, clocks):
         eng.iteration()
     torch.cuda.synchronize()
     timing["on"] = True
+    gc.disable()
     for _ in range(K_steps):      # the same K iterations as pass 1 (deterministic window)
         eng.iteration()
     torch.cuda.synchronize()
+    gc.enable()
     graph_ms = [a.elapsed_time(b) for a, b in step_ev]
     splice_bytes = sum(n for _, _, n in splice_ev)
     splice_s = sum(a.elapsed_time(b) for a, b, _ in splice_ev) / 1e3
@@ -619,6 +623,7 @@ def run_e2e(ctx, win, B):
     torch.cuda.synchronize()
     counters["h2d"] = counters["d2h"] = 0
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    gc.disable()
     e0.record()
     h0 = time.perf_counter()
     st2 = [step(eng, W + i, False) for i in range(K_steps)]
@@ -628,6 +633,7 @@ def run_e2e(ctx, win, B):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    gc.enable()
     ms2 = e0.elapsed_time(e1)
     marks = [x for x in step_ev if x[0] >= W] + [(None, e1, 0)]
     step_ms = [marks[k][1].elapsed_time(marks[k + 1][1]) for k in range(len(marks) - 1)]
