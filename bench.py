@@ -637,9 +637,13 @@ def run_e2e(ctx, win, B):
     ms2 = e0.elapsed_time(e1)
     marks = [x for x in step_ev if x[0] >= W] + [(None, e1, 0)]
     step_ms = [marks[k][1].elapsed_time(marks[k + 1][1]) for k in range(len(marks) - 1)]
+    slow = sorted(range(len(step_ms)), key=lambda k: -step_ms[k])[:3]
     out = {"ms": ms2, "host_ms": host_ms, "step_ms": step_ms,
            "tokens": sum(s.decoded for s in st2), "h2d": counters["h2d"] / K_steps,
-           "d2h": counters["d2h"] / K_steps, "inserts_h2d": ins_h2d}
+           "d2h": counters["d2h"] / K_steps, "inserts_h2d": ins_h2d,
+           "slowest": [{"ms": step_ms[k], "t": st2[k].t, "inserted": st2[k].inserted,
+                        "stored": st2[k].stored, "compact_rows": st2[k].compact_rows,
+                        "removed": st2[k].removed} for k in slow]}
     eng = q_h = k_h = v_h = pref_h = sets = res_dev = res_h = None
     _release()
     return out
@@ -935,6 +939,7 @@ def summarize(args, r, world, red):
                                   " (prefilled K/V in HBM)")
                                + " + D2H of all layers' outputs every step, inside the timed region",
                        "host_enqueue_ms_per_step": e["host_ms"] / args.steps,
+                       "slowest_steps": e["slowest"],
                        "step_ms_p50_p90_max": [statistics.median(e["step_ms"]),
                                                sorted(e["step_ms"])[int(0.9 * (len(e["step_ms"]) - 1))],
                                                max(e["step_ms"])]}
