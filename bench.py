@@ -719,6 +719,26 @@ def run_prefill(ctx, plens):
     return out
 
 
+def read_stream_gbs(dev, gib=8):
+    """Context for the roofline: a read-only stream over `gib` GiB (torch's sum
+    reduction, best of 5, CUDA events).  The peak the line divides by is
+    MEASURED_PEAKS.json's copy (read + write) bandwidth; a read-only kernel such as
+    the decode attention can run a little above it."""
+    import torch
+    x = torch.ones((gib << 30) // 4, dtype=torch.int32, device=dev)
+    best = 0.0
+    for _ in range(5):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        x.sum()
+        b.record()
+        torch.cuda.synchronize()
+        best = max(best, x.numel() * 4 / (a.elapsed_time(b) / 1e3) / 1e9)
+    del x
+    torch.cuda.empty_cache()
+    return best
+
+
 def run_baton(args, rank, world, local_rank):
     import torch
     torch.cuda.set_device(local_rank)
@@ -739,8 +759,9 @@ def run_baton(args, rank, world, local_rank):
     full_run = run_full(ctx) if (world == 1 and not args.no_full_run) else None
     plens = sum((w["fresh"] for w in wins), [])[:64]
     prefill = run_prefill(ctx, plens) if (rank == 0 and plens) else None
+    read_gbs = read_stream_gbs(ctx.dev) if rank == 0 else None
     return dict(wins=wins, steady=steady, clocks=clk, full_run=full_run, prefill=prefill,
-                scaling=ctx.scaling, wl=ctx.wl)
+                scaling=ctx.scaling, wl=ctx.wl, read_gbs=read_gbs)
 
 
 # ------------------------------------------------------------------ the oracle arm
@@ -918,7 +939,12 @@ def summarize(args, r, world, red):
                      "timing": "rank 0: CUDA events around each decode-step graph (mask update + L "
                                "PDL-chained attention launches) over every window's K steps; "
                                "avg_launch_us = graph time / (steps * L)",
-                     "step_hbm_GBps": attn_bytes / (sum(w["ms"] for w in wins) / 1e3) / 1e9},
+                     "step_hbm_GBps": attn_bytes / (sum(w["ms"] for w in wins) / 1e3) / 1e9,
+                     "read_stream_GBps": r.get("read_gbs"),
+                     "read_stream_note": "context: a read-only stream (torch sum over 8 GiB, best "
+                                         "of 5) on this box; `peak` is the measured copy "
+                                         "(read+write) bandwidth, which a read-only kernel can "
+                                         "slightly exceed"},
         "splice": {"calls": sum(w["splice_calls"] for w in wins), "bytes": splice_bytes,
                    "GBps": (splice_bytes / splice_s / 1e9) if splice_s else None,
                    "frac": (splice_bytes / splice_s / 1e9 / peak) if splice_s else None,
