@@ -720,12 +720,13 @@ def run_prefill(ctx, plens):
 
 
 def read_stream_gbs(dev, gib=8):
-    """Context for the roofline: a read-only stream over `gib` GiB (torch's sum
-    reduction, best of 5, CUDA events).  The peak the line divides by is
+    """Context for the roofline: a read-only stream over `gib` GiB (torch's fp32 sum
+    reduction, best of 5, CUDA events; an int32 sum accumulates in int64 and ran at a
+    sixth of the bandwidth).  The peak the line divides by is
     MEASURED_PEAKS.json's copy (read + write) bandwidth; a read-only kernel such as
     the decode attention can run a little above it."""
     import torch
-    x = torch.ones((gib << 30) // 4, dtype=torch.int32, device=dev)
+    x = torch.ones((gib << 30) // 4, dtype=torch.float32, device=dev)
     best = 0.0
     for _ in range(5):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -941,7 +942,7 @@ def summarize(args, r, world, red):
                                "avg_launch_us = graph time / (steps * L)",
                      "step_hbm_GBps": attn_bytes / (sum(w["ms"] for w in wins) / 1e3) / 1e9,
                      "read_stream_GBps": r.get("read_gbs"),
-                     "read_stream_note": "context: a read-only stream (torch sum over 8 GiB, best "
+                     "read_stream_note": "context: a read-only stream (torch fp32 sum over 8 GiB, best "
                                          "of 5) on this box; `peak` is the measured copy "
                                          "(read+write) bandwidth, which a read-only kernel can "
                                          "slightly exceed"},

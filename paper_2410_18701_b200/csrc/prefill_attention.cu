@@ -5,12 +5,14 @@
 // SDPA of query token i over keys 0..i -- the decode attention of every
 // prefix at once, a dense contraction, so it runs on the 5th-gen tensor cores.
 //
-// One CTA per (q head, 128-query tile), TWO CTAs per SM (~98 KB smem, 256 TMEM
-// columns each) so one CTA's softmax overlaps the other's MMAs.  Warp roles
-// (DESIGN.md §6.3):
-//   warp 4   TMA producer: the Q tile once (128 x 128, SWIZZLE_128B), then per
-//            64-key tile K and V, each through a 2-stage ring -- cp.async.bulk.tensor
-//            with mbarrier tx-counts
+// Work item = (q head, 128-query tile); a persistent grid of TWO CTAs per SM (~98 KB
+// smem, 256 TMEM columns each) walks the items, so one CTA's softmax overlaps the
+// other's MMAs and an item's Q load, first K/V tiles and first S MMAs run under the
+// previous item's last P.V and epilogue.  Warp roles:
+//   warp 4   TMA producer: per item the Q tile (128 x 128, SWIZZLE_128B; once the
+//            previous item's last S MMA has read the buffer), then per 64-key tile K
+//            and V, each through a 2-stage ring that runs on across items --
+//            cp.async.bulk.tensor with mbarrier tx-counts
 //   warp 5   MMA issuer (one elected thread): S(j) = Q K(j)^T (M=128, N=64, K=16 x8)
 //            into TMEM buffer j&1, then O += P(j) V(j) (M=128, N=128, K=16 x4) with
 //            P(j) read from TMEM (the "TS" form: P overwrites the first 32 columns of
@@ -23,7 +25,7 @@
 //            O rescale in TMEM (tcgen05.ld/st) when the reference max moves, epilogue.
 //
 // The same kernel runs the EXTEND attention of a vector-shaping iteration
-// (NEXT-1, launch_extend_attention): a CTA per (slot, q head, query
+// (NEXT-1, launch_extend_attention): an item per (slot, q head, query
 // tile); query row t of slot b is input token t of width W (q/out token-major,
 // [slots][W][q_heads][D]: a 4-D Q map with a (64, 1, 128, 1) box), its keys are the
 // slot's cache rows 0 .. off_b + t (off_b = lens_b - W, the rows before this
@@ -59,7 +61,7 @@ struct __align__(1024) PfSmem {
     uint8_t k[2][KV_BYTES];
     uint8_t v[2][KV_BYTES];
     uint8_t mk[2][PF_N + 16];       // extend: mask bytes of the V stage's key tile
-    uint64_t bar_q, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], p_full[2], pv_done[2];
+    uint64_t bar_q, q_empty, o_free, k_full[2], k_empty[2], v_full[2], v_empty[2], s_full[2], p_full[2], pv_done[2];
     uint32_t tmem_base;
 };
 
@@ -98,6 +100,7 @@ BATON_DEV float2 fadd2(float2 a, float2 b) {
 
 struct PfParams {
     int Hq, Hkv, len, n_mtiles;     // extend: len = W query rows per (slot, head)
+    int n_items;                    // work items (prefill: entries x Hq; extend: n_mtiles x Hq x slots)
     float scale_log2;
     float rescale_t;                // lazy-rescale threshold (log2 units): P <= 2^rescale_t
     __nv_bfloat16 *out;
@@ -113,53 +116,102 @@ struct PfParams {
     uint32_t vl_tile[VL_MAXT];
 };
 
+// One work item = (prompt or slot, q head, 128-query tile).  Items are numbered
+// heaviest first (prefill: the host's order; extend: slot-major, heavy tiles first
+// within a (slot, head)).
+struct PfItem {
+    int b, h, mt, s0, len, off, kpad, n_kt;   // n_kt == 0: an empty extend slot (zero rows)
+};
+
+template <bool EXT>
+BATON_DEV PfItem pf_item(const PfParams &p, int k) {
+    PfItem it;
+    if (EXT) {
+        it.mt = p.n_mtiles - 1 - k % p.n_mtiles;
+        it.h = (k / p.n_mtiles) % p.Hq;
+        it.b = k / (p.n_mtiles * p.Hq);
+        it.s0 = 0;
+        it.len = p.len;
+        const int lb = p.lens[it.b];
+        if (lb <= 0) {
+            it.off = it.kpad = it.n_kt = 0;
+            return it;
+        }
+        it.off = lb - p.len;
+        it.kpad = p.pad[it.b];
+    } else {
+        const uint32_t e = p.vl_tile[k / p.Hq];
+        it.mt = (int)(e & 0xffff);
+        it.h = k % p.Hq;
+        it.b = 0;
+        it.s0 = p.vl_start[e >> 16];
+        it.len = p.vl_len[e >> 16];
+        it.off = it.kpad = 0;
+    }
+    // key tiles up to the diagonal.  Varlen prefill: a tile may run past this prompt
+    // into the next one's rows; those keys are past every query row of the tile
+    // (causally masked, P = 0 exactly) and their V rows are finite
+    it.n_kt = (it.off + min(it.mt * PF_M + PF_M, it.len) + PF_N - 1) / PF_N;
+    return it;
+}
+
+// A persistent CTA's walk over its items: round r takes item r*G + c on even rounds
+// and r*G + G-1-c on odd ones (a snake over the heaviest-first order, so the CTAs'
+// loads even out), and positions (item, key tile j) in that order.  `seq` counts the
+// non-empty items so far (the Q buffer's and the O accumulator's phases).
+template <bool EXT>
+struct PfWalk {
+    const PfParams *p;
+    int r, seq, j;
+    bool valid;
+    PfItem it;
+    BATON_DEV int item_at(int rr) const {
+        const int G = gridDim.x, c = blockIdx.x;
+        return rr * G + ((rr & 1) ? G - 1 - c : c);
+    }
+    // first item at or after round rr (empty extend slots included: the softmax
+    // warps write their zero rows)
+    BATON_DEV void load(int rr) {
+        r = rr;
+        const int k = item_at(rr);
+        valid = k < p->n_items;
+        if (valid) it = pf_item<EXT>(*p, k);
+        j = 0;
+    }
+    BATON_DEV void init(const PfParams *pp) {
+        p = pp;
+        seq = 0;
+        load(0);
+    }
+    BATON_DEV void next_item() {
+        if (it.n_kt > 0) ++seq;
+        load(r + 1);
+    }
+    // next (item, tile) position, skipping empty items
+    BATON_DEV void skip_empty() {
+        while (valid && it.n_kt == 0) load(r + 1);
+    }
+    BATON_DEV void advance() {
+        if (++j == it.n_kt) {
+            next_item();
+            skip_empty();
+        }
+    }
+};
+
 template <bool EXT>
 __global__ void __launch_bounds__(PF_THREADS, 2)
 prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                         const __grid_constant__ CUtensorMap tm_v, const PfParams p) {
+                         const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ PfParams p) {
     extern __shared__ uint8_t smem_raw[];
     PfSmem &sm = *reinterpret_cast<PfSmem *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr bool ext = EXT;
-    int mt, h, b, s0 = 0, len = p.len;
-    if (EXT) {   // heavy tiles (near the diagonal end) first within a (slot, head)
-        mt = p.n_mtiles - 1 - (int)(blockIdx.x % p.n_mtiles);
-        h = (blockIdx.x / p.n_mtiles) % p.Hq;
-        b = blockIdx.x / (p.n_mtiles * p.Hq);                 // slot
-    } else {     // prefill: the host lists (prompt, query tile) heaviest first
-        const uint32_t e = p.vl_tile[blockIdx.x / p.Hq];
-        const int pi = (int)(e >> 16);
-        mt = (int)(e & 0xffff);
-        h = blockIdx.x % p.Hq;
-        b = 0;
-        s0 = p.vl_start[pi];
-        len = p.vl_len[pi];
-    }
-    const int g = h * p.Hkv / p.Hq;
-    const int q0 = mt * PF_M;
-    int off = 0, kpad = 0;
-    if (ext) {
-        const int lb = p.lens[b];
-        if (lb <= 0) {   // empty slot: zero output rows, nothing else
-            for (int i = threadIdx.x; i < PF_M * PF_D / 8; i += PF_THREADS) {
-                const int r = q0 + i / (PF_D / 8);
-                if (r < p.len)
-                    reinterpret_cast<uint4 *>(p.out + (((size_t)b * p.len + r) * p.Hq + h) * PF_D)[i % (PF_D / 8)] =
-                        make_uint4(0, 0, 0, 0);
-            }
-            return;
-        }
-        off = lb - p.len;
-        kpad = p.pad[b];
-    }
-    const int qrow = b * p.Hq + h, krow = b * p.Hkv + g;        // outer coordinate of the maps
-    // key tiles up to the diagonal.  Varlen prefill: a tile may run past this prompt
-    // into the next one's rows; those keys are past every query row of the tile
-    // (causally masked, P = 0 exactly) and their V rows are finite
-    const int n_kt = (off + min(q0 + PF_M, len) + PF_N - 1) / PF_N;
 
     if (threadIdx.x == 0) {
         mbar_init(&sm.bar_q, 1);
+        mbar_init(&sm.q_empty, 1);
+        mbar_init(&sm.o_free, 128);
         for (int s = 0; s < 2; ++s) {
             mbar_init(&sm.k_full[s], 1);
             mbar_init(&sm.k_empty[s], 1);
@@ -184,54 +236,78 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
 
     if (warp == 4) {
         // ======================= TMA producer =======================
+        // per item: the Q tile (once the previous item's last S MMA has read the Q
+        // buffer), then its K and V tiles through the 2-stage rings; ring stages and
+        // phases run on across items (t = this CTA's tile count)
         if (lane == 0) {
             prefetch_tmap(&tm_q);
             prefetch_tmap(&tm_k);
             prefetch_tmap(&tm_v);
-            mbar_arrive_expect_tx(&sm.bar_q, Q_BYTES);
-            if constexpr (EXT) {
-                tma_load_4d(sm.q, &tm_q, 0, h, q0, b, &sm.bar_q);
-                tma_load_4d(sm.q + Q_REGION, &tm_q, 64, h, q0, b, &sm.bar_q);
-            } else {
-                tma_load_3d(sm.q, &tm_q, 0, s0 + q0, qrow, &sm.bar_q);
-                tma_load_3d(sm.q + Q_REGION, &tm_q, 64, s0 + q0, qrow, &sm.bar_q);
-            }
-            for (int j = 0; j < n_kt; ++j) {
-                const int s = j & 1;
-                if (j >= 2) mbar_wait(&sm.k_empty[s], ((j >> 1) + 1) & 1);   // S(j-2) done with K
-                mbar_arrive_expect_tx(&sm.k_full[s], KV_BYTES);
-                tma_load_3d(sm.k[s], &tm_k, 0, s0 + j * PF_N, krow, &sm.k_full[s]);
-                tma_load_3d(sm.k[s] + KV_REGION, &tm_k, 64, s0 + j * PF_N, krow, &sm.k_full[s]);
-                if (j >= 2) mbar_wait(&sm.v_empty[s], ((j >> 1) + 1) & 1);   // PV(j-2) done
-                uint32_t mbytes = 0;
-                size_t a0 = 0;
-                if (ext) {   // aligned superset of the tile's mask bytes (rows start 16-B aligned)
-                    const size_t row0 = (size_t)b * p.max_ctx;
-                    const size_t j0 = row0 + kpad + j * PF_N;
-                    a0 = j0 & ~(size_t)15;
-                    size_t need = (j0 + PF_N - a0 + 15) & ~(size_t)15;
-                    if (a0 + need > row0 + p.max_ctx) need = row0 + p.max_ctx - a0;
-                    mbytes = (uint32_t)need;
+            PfWalk<EXT> w;
+            w.init(&p);
+            w.skip_empty();
+            int t = 0;
+            for (; w.valid; w.next_item(), w.skip_empty()) {
+                const PfItem &it = w.it;
+                const int q0 = it.mt * PF_M;
+                const int krow = it.b * p.Hkv + it.h * p.Hkv / p.Hq;
+                if (w.seq > 0) mbar_wait(&sm.q_empty, (w.seq - 1) & 1);
+                mbar_arrive_expect_tx(&sm.bar_q, Q_BYTES);
+                if constexpr (EXT) {
+                    tma_load_4d(sm.q, &tm_q, 0, it.h, q0, it.b, &sm.bar_q);
+                    tma_load_4d(sm.q + Q_REGION, &tm_q, 64, it.h, q0, it.b, &sm.bar_q);
+                } else {
+                    tma_load_3d(sm.q, &tm_q, 0, it.s0 + q0, it.h, &sm.bar_q);
+                    tma_load_3d(sm.q + Q_REGION, &tm_q, 64, it.s0 + q0, it.h, &sm.bar_q);
                 }
-                mbar_arrive_expect_tx(&sm.v_full[s], KV_BYTES + mbytes);
-                tma_load_3d(sm.v[s], &tm_v, 0, s0 + j * PF_N, krow, &sm.v_full[s]);
-                tma_load_3d(sm.v[s] + KV_REGION, &tm_v, 64, s0 + j * PF_N, krow, &sm.v_full[s]);
-                if (mbytes) bulk_g2s(sm.mk[s], p.mask + a0, mbytes, &sm.v_full[s]);
+                for (int j = 0; j < it.n_kt; ++j, ++t) {
+                    const int s = t & 1;
+                    if (t >= 2) mbar_wait(&sm.k_empty[s], ((t >> 1) + 1) & 1);   // S(t-2) done with K
+                    mbar_arrive_expect_tx(&sm.k_full[s], KV_BYTES);
+                    tma_load_3d(sm.k[s], &tm_k, 0, it.s0 + j * PF_N, krow, &sm.k_full[s]);
+                    tma_load_3d(sm.k[s] + KV_REGION, &tm_k, 64, it.s0 + j * PF_N, krow, &sm.k_full[s]);
+                    if (t >= 2) mbar_wait(&sm.v_empty[s], ((t >> 1) + 1) & 1);   // PV(t-2) done
+                    uint32_t mbytes = 0;
+                    size_t a0 = 0;
+                    if (ext) {   // aligned superset of the tile's mask bytes (rows start 16-B aligned)
+                        const size_t row0 = (size_t)it.b * p.max_ctx;
+                        const size_t j0 = row0 + it.kpad + j * PF_N;
+                        a0 = j0 & ~(size_t)15;
+                        size_t need = (j0 + PF_N - a0 + 15) & ~(size_t)15;
+                        if (a0 + need > row0 + p.max_ctx) need = row0 + p.max_ctx - a0;
+                        mbytes = (uint32_t)need;
+                    }
+                    mbar_arrive_expect_tx(&sm.v_full[s], KV_BYTES + mbytes);
+                    tma_load_3d(sm.v[s], &tm_v, 0, it.s0 + j * PF_N, krow, &sm.v_full[s]);
+                    tma_load_3d(sm.v[s] + KV_REGION, &tm_v, 64, it.s0 + j * PF_N, krow, &sm.v_full[s]);
+                    if (mbytes) bulk_g2s(sm.mk[s], p.mask + a0, mbytes, &sm.v_full[s]);
+                }
             }
         }
     } else if (warp == 5) {
         // ======================= MMA issuer =======================
+        // order over this CTA's whole tile stream: S(0), S(1), PV(0), S(2), PV(1), ...
+        // S(t+2) goes into the TMEM buffer that P(t) occupies; it is issued after PV(t),
+        // and the tensor pipe executes in issue order.  S(t+2) may be the next item's
+        // first tile (its Q tile must have landed); an item's first PV overwrites O,
+        // so it waits until the softmax warps have read the previous item's O out.
         if (lane == 0) {
             constexpr uint32_t idS = idesc_bf16(PF_M, PF_N, 0);   // B = K tile, K-major
             constexpr uint32_t idO = idesc_bf16(PF_M, PF_D, 1);   // A = P (TMEM, K-major), B = V tile, MN-major
             const uint32_t qa = smem_u32(sm.q);
-            mbar_wait(&sm.bar_q, 0);
-            // order: S(0), S(1), PV(0), S(2), PV(1), S(3), ...  S(j+2) goes into the TMEM
-            // buffer that P(j) occupies; it is issued after PV(j), and the tensor pipe
-            // executes in issue order.
-            auto issue_s = [&](int j) {
-                const int b2 = j & 1;
-                mbar_wait(&sm.k_full[b2], (j >> 1) & 1);
+            PfWalk<EXT> ws, wp;   // next S to issue, next PV to issue
+            ws.init(&p);
+            ws.skip_empty();
+            wp.init(&p);
+            wp.skip_empty();
+            int ts = 0;
+            auto issue_s = [&]() {
+                const int b2 = ts & 1;
+                if (ws.j == 0) {
+                    mbar_wait(&sm.bar_q, ws.seq & 1);
+                    tc_fence_after();
+                }
+                mbar_wait(&sm.k_full[b2], (ts >> 1) & 1);
                 tc_fence_after();
                 const uint32_t ka = smem_u32(sm.k[b2]);
 #pragma unroll
@@ -241,166 +317,190 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
                 }
                 umma_commit(&sm.s_full[b2]);
                 umma_commit(&sm.k_empty[b2]);
+                if (ws.j == ws.it.n_kt - 1) umma_commit(&sm.q_empty);   // the item's last S: Q may go
+                ++ts;
+                ws.advance();
             };
-            issue_s(0);
-            if (n_kt > 1) issue_s(1);
-            for (int j = 0; j < n_kt; ++j) {
-                const int s = j & 1;
-                mbar_wait(&sm.p_full[s], (j >> 1) & 1);           // P(j) in TMEM, O rescaled
-                mbar_wait(&sm.v_full[s], (j >> 1) & 1);
+            if (ws.valid) issue_s();
+            if (ws.valid) issue_s();
+            for (int t = 0; wp.valid; ++t) {
+                const int s = t & 1;
+                mbar_wait(&sm.p_full[s], (t >> 1) & 1);           // P(t) in TMEM, O rescaled
+                mbar_wait(&sm.v_full[s], (t >> 1) & 1);
+                if (wp.j == 0 && wp.seq > 0) mbar_wait(&sm.o_free, (wp.seq - 1) & 1);   // previous O read out
                 tc_fence_after();
                 const uint32_t va = smem_u32(sm.v[s]);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {   // K = 64 keys in steps of 16 (8 TMEM columns of bf16 pairs)
                     umma_f16_ts(tO, tS + 64 * s + 8 * k, smem_desc(va + k * 2048, KV_REGION, 1024), idO,
-                                (j > 0 || k > 0));
+                                (wp.j > 0 || k > 0));
                 }
                 umma_commit(&sm.pv_done[s]);
                 umma_commit(&sm.v_empty[s]);
-                if (j + 2 < n_kt) issue_s(j + 2);
+                wp.advance();
+                if (ws.valid) issue_s();
             }
         }
     } else {
         // ======================= softmax warps 0-3 =======================
         const int row = warp * 32 + lane;            // query row within the tile = TMEM lane
-        const int qi = q0 + row;
         const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-        float m = -INFINITY, l = 0.f;
         uint32_t pk[32];                              // P row (64 keys) packed bf16x2
-        const int mrow = ext ? (int)(((size_t)b * p.max_ctx + kpad) & 15) : 0;   // mask byte offset
-        for (int j = 0; j < n_kt; ++j) {
-            const int sb = j & 1;
-            const uint32_t tSj = tS + 64 * sb + lane_off;
-            mbar_wait(&sm.s_full[sb], (j >> 1) & 1);
-            // one thread observes PV(j-2)'s completion on its barrier: already done (S(j)
-            // was issued after it and its commit covers every earlier MMA), so this never
-            // blocks; it keeps every phase of pv_done waited on (compute-sanitizer
-            // synccheck flags a phase completed with no wait; with all 128 threads
-            // polling it cost ~1%)
-            if (j >= 2 && threadIdx.x == 0) mbar_wait(&sm.pv_done[sb], ((j - 2) >> 1) & 1);
-            tc_fence_after();
-            const int kbase = j * PF_N;
-            const bool diag = kbase + PF_N > off + q0;   // tile touches the causal diagonal
-            const uint8_t *mk = sm.mk[j & 1] + mrow;
-            if (ext) mbar_wait(&sm.v_full[j & 1], (j >> 1) & 1);   // this tile's mask bytes
-            uint32_t r[2][32];
-            tmem_ld32(tSj, r[0]);
-            tmem_ld32(tSj + 32, r[1]);
-            tmem_wait_ld();
-            // Masked keys become -inf in the RAW scores; the scale (> 0) is folded into
-            // the exponent (one FFMA + ex2 per key) and the row max is taken raw.  Tiles
-            // off the diagonal (and prefill has no mask) skip the per-key tests.
-            if (diag || ext) {
+        PfWalk<EXT> w;
+        w.init(&p);
+        int t = 0;                                    // this CTA's tile count (buffers, phases)
+        for (; w.valid; w.next_item()) {
+            const PfItem &it = w.it;
+            const int q0 = it.mt * PF_M, qi = q0 + row, off = it.off;
+            if (it.n_kt == 0) {   // extend, empty slot: zero output rows, nothing else
+                for (int i = row; i < PF_M * PF_D / 8; i += 128) {
+                    const int r = q0 + i / (PF_D / 8);
+                    if (r < p.len)
+                        reinterpret_cast<uint4 *>(p.out + (((size_t)it.b * p.len + r) * p.Hq + it.h) * PF_D)[i % (PF_D / 8)] =
+                            make_uint4(0, 0, 0, 0);
+                }
+                continue;
+            }
+            float m = -INFINITY, l = 0.f;
+            const int mrow = ext ? (int)(((size_t)it.b * p.max_ctx + it.kpad) & 15) : 0;   // mask byte offset
+            for (int j = 0; j < it.n_kt; ++j, ++t) {
+                const int sb = t & 1;
+                const uint32_t tSj = tS + 64 * sb + lane_off;
+                mbar_wait(&sm.s_full[sb], (t >> 1) & 1);
+                // one thread observes PV(t-2)'s completion on its barrier: already done (S(t)
+                // was issued after it and its commit covers every earlier MMA), so this never
+                // blocks; it keeps every phase of pv_done waited on (compute-sanitizer
+                // synccheck flags a phase completed with no wait; with all 128 threads
+                // polling it cost ~1%)
+                if (t >= 2 && threadIdx.x == 0) mbar_wait(&sm.pv_done[sb], ((t - 2) >> 1) & 1);
+                tc_fence_after();
+                const int kbase = j * PF_N;
+                const bool diag = kbase + PF_N > off + q0;   // tile touches the causal diagonal
+                const uint8_t *mk = sm.mk[sb] + mrow;
+                if (ext) mbar_wait(&sm.v_full[sb], (t >> 1) & 1);   // this tile's mask bytes
+                uint32_t r[2][32];
+                tmem_ld32(tSj, r[0]);
+                tmem_ld32(tSj + 32, r[1]);
+                tmem_wait_ld();
+                // Masked keys become -inf in the RAW scores; the scale (> 0) is folded into
+                // the exponent (one FFMA + ex2 per key) and the row max is taken raw.  Tiles
+                // off the diagonal (and prefill has no mask) skip the per-key tests.
+                if (diag || ext) {
+#pragma unroll
+                    for (int c = 0; c < 2; ++c)
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) {
+                            const bool dead = (diag && kbase + c * 32 + i > off + qi) || (ext && mk[c * 32 + i] == 0);
+                            if (dead) r[c][i] = __float_as_uint(-INFINITY);
+                        }
+                }
+                float mx;
+                {   // row max: 3-input FMNMX3 in four independent chains
+                    float a0 = -INFINITY, a1 = -INFINITY, a2 = -INFINITY, a3 = -INFINITY;
+#pragma unroll
+                    for (int i = 0; i < 32; i += 4) {
+                        a0 = fmax3(a0, __uint_as_float(r[0][i]), __uint_as_float(r[0][i + 1]));
+                        a1 = fmax3(a1, __uint_as_float(r[0][i + 2]), __uint_as_float(r[0][i + 3]));
+                        a2 = fmax3(a2, __uint_as_float(r[1][i]), __uint_as_float(r[1][i + 1]));
+                        a3 = fmax3(a3, __uint_as_float(r[1][i + 2]), __uint_as_float(r[1][i + 3]));
+                    }
+                    mx = fmax3(fmaxf(a0, a1), a2, a3);
+                }
+                mx *= p.scale_log2;   // -inf stays -inf
+                // Lazy rescale: P is taken relative to a reference max m that moves only
+                // when the row max exceeds it by more than rescale_t (log2 units), so P <=
+                // 2^rescale_t (exact in fp32 accumulation, same bf16 rounding of P) and the
+                // O rows in TMEM are rescaled only on those tiles, not whenever the max moves.
+                // A row may see only masked keys so far (extend: holes, padding): keep exp2
+                // finite -- ex2(-inf - 0) = 0.
+                const float m_new = (mx > m + p.rescale_t || m == -INFINITY) ? fmaxf(m, mx) : m;
+                const float mref = (m_new == -INFINITY) ? 0.f : m_new;
+                const float alpha = ex2(m - mref);
+                const float nref = -mref;
+                // the row sum adds the fp32 exponentials; the P.V MMA multiplies their bf16
+                // roundings (relative difference <= 2^-9 per key, far inside C13's 1e-2)
+                float2 rs2 = make_float2(0.f, 0.f);
+                const float2 sc2 = make_float2(p.scale_log2, p.scale_log2), nr2 = make_float2(nref, nref);
 #pragma unroll
                 for (int c = 0; c < 2; ++c)
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        const bool dead = (diag && kbase + c * 32 + i > off + qi) || (ext && mk[c * 32 + i] == 0);
-                        if (dead) r[c][i] = __float_as_uint(-INFINITY);
+                    for (int i = 0; i < 32; i += 2) {
+                        float2 a = ffma2(make_float2(__uint_as_float(r[c][i]), __uint_as_float(r[c][i + 1])), sc2, nr2);
+                        a.x = ex2(a.x);
+                        a.y = ex2(a.y);
+                        const __nv_bfloat162 b = __floats2bfloat162_rn(a.x, a.y);
+                        rs2 = fadd2(rs2, a);
+                        pk[c * 16 + i / 2] = *reinterpret_cast<const uint32_t *>(&b);
                     }
-            }
-            float mx;
-            {   // row max: 3-input FMNMX3 in four independent chains
-                float a0 = -INFINITY, a1 = -INFINITY, a2 = -INFINITY, a3 = -INFINITY;
+                const float rs = rs2.x + rs2.y;
+                l = l * alpha + rs;
+                m = m_new;
+                // warp-uniform: tcgen05.ld/st are .sync.aligned (all 32 lanes converged)
+                if (j > 0 && __any_sync(FULL_MASK, alpha != 1.f)) {
+                    // O is stable once PV(t-1) is done (PV(t-3) on that barrier completed
+                    // before S(t-1), which this warp group already read: at most one phase behind)
+                    mbar_wait(&sm.pv_done[(t - 1) & 1], ((t - 1) >> 1) & 1);
+                    tc_fence_after();
+                    if (lane == 0) atomicAdd(&g_pf_rescales, 1ull);
+                    {
 #pragma unroll
-                for (int i = 0; i < 32; i += 4) {
-                    a0 = fmax3(a0, __uint_as_float(r[0][i]), __uint_as_float(r[0][i + 1]));
-                    a1 = fmax3(a1, __uint_as_float(r[0][i + 2]), __uint_as_float(r[0][i + 3]));
-                    a2 = fmax3(a2, __uint_as_float(r[1][i]), __uint_as_float(r[1][i + 1]));
-                    a3 = fmax3(a3, __uint_as_float(r[1][i + 2]), __uint_as_float(r[1][i + 3]));
-                }
-                mx = fmax3(fmaxf(a0, a1), a2, a3);
-            }
-            mx *= p.scale_log2;   // -inf stays -inf
-            // Lazy rescale: P is taken relative to a reference max m that moves only
-            // when the row max exceeds it by more than rescale_t (log2 units), so P <=
-            // 2^rescale_t (exact in fp32 accumulation, same bf16 rounding of P) and the
-            // O rows in TMEM are rescaled only on those tiles, not whenever the max moves.
-            // A row may see only masked keys so far (extend: holes, padding): keep exp2
-            // finite -- ex2(-inf - 0) = 0.
-            const float m_new = (mx > m + p.rescale_t || m == -INFINITY) ? fmaxf(m, mx) : m;
-            const float mref = (m_new == -INFINITY) ? 0.f : m_new;
-            const float alpha = ex2(m - mref);
-            const float nref = -mref;
-            // the row sum adds the fp32 exponentials; the P.V MMA multiplies their bf16
-            // roundings (relative difference <= 2^-9 per key, far inside C13's 1e-2)
-            float2 rs2 = make_float2(0.f, 0.f);
-            const float2 sc2 = make_float2(p.scale_log2, p.scale_log2), nr2 = make_float2(nref, nref);
+                        for (int c = 0; c < 4; ++c) {
+                            uint32_t o[32];
+                            tmem_ld32(tO + lane_off + c * 32, o);
+                            tmem_wait_ld();
 #pragma unroll
-            for (int c = 0; c < 2; ++c)
-#pragma unroll
-                for (int i = 0; i < 32; i += 2) {
-                    float2 a = ffma2(make_float2(__uint_as_float(r[c][i]), __uint_as_float(r[c][i + 1])), sc2, nr2);
-                    a.x = ex2(a.x);
-                    a.y = ex2(a.y);
-                    const __nv_bfloat162 b = __floats2bfloat162_rn(a.x, a.y);
-                    rs2 = fadd2(rs2, a);
-                    pk[c * 16 + i / 2] = *reinterpret_cast<const uint32_t *>(&b);
-                }
-            const float rs = rs2.x + rs2.y;
-            l = l * alpha + rs;
-            m = m_new;
-            // warp-uniform: tcgen05.ld/st are .sync.aligned (all 32 lanes converged)
-            if (j > 0 && __any_sync(FULL_MASK, alpha != 1.f)) {
-                // O is stable once PV(j-1) is done (PV(j-3) on that barrier completed
-                // before S(j-1), which this warp group already read: at most one phase behind)
-                mbar_wait(&sm.pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
-                tc_fence_after();
-                if (lane == 0) atomicAdd(&g_pf_rescales, 1ull);
-                {
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        uint32_t o[32];
-                        tmem_ld32(tO + lane_off + c * 32, o);
-                        tmem_wait_ld();
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-                        tmem_st32(tO + lane_off + c * 32, o);
+                            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+                            tmem_st32(tO + lane_off + c * 32, o);
+                        }
+                        tmem_wait_st();
                     }
-                    tmem_wait_st();
                 }
-            }
-            // extend: cache rows past lens in this tile are stale memory (maybe NaN
-            // bits); P is 0 there but 0 * NaN is not, so zero those V rows (whole 128-B
-            // rows of both halves, swizzle-independent) before the P.V MMA reads them
-            if (ext && kbase + PF_N > off + p.len) {
-                const int first = off + p.len - kbase;
-                for (int i = row; i < (PF_N - first) * 16; i += 128) {
-                    const int rr = first + i / 16, ch = i % 16;
-                    *reinterpret_cast<uint4 *>(sm.v[j & 1] + (ch >> 3) * KV_REGION + rr * 128 + (ch & 7) * 16) =
-                        make_uint4(0, 0, 0, 0);
+                // extend: cache rows past lens in this tile are stale memory (maybe NaN
+                // bits); P is 0 there but 0 * NaN is not, so zero those V rows (whole 128-B
+                // rows of both halves, swizzle-independent) before the P.V MMA reads them
+                if (ext && kbase + PF_N > off + p.len) {
+                    const int first = off + p.len - kbase;
+                    for (int i = row; i < (PF_N - first) * 16; i += 128) {
+                        const int rr = first + i / 16, ch = i % 16;
+                        *reinterpret_cast<uint4 *>(sm.v[sb] + (ch >> 3) * KV_REGION + rr * 128 + (ch & 7) * 16) =
+                            make_uint4(0, 0, 0, 0);
+                    }
+                    fence_async_smem();   // generic-proxy writes -> the tensor core's reads
                 }
-                fence_async_smem();   // generic-proxy writes -> the tensor core's reads
+                // P row -> TMEM over the first 32 columns of this S buffer (bf16 pairs,
+                // key 2c in the low half of column c): the A operand of PV(t)
+                tmem_st32(tSj, pk);
+                tmem_wait_st();
+                tc_fence_before();
+                mbar_arrive(&sm.p_full[sb]);
             }
-            // P row -> TMEM over the first 32 columns of this S buffer (bf16 pairs,
-            // key 2c in the low half of column c): the A operand of PV(j)
-            tmem_st32(tSj, pk);
-            tmem_wait_st();
-            tc_fence_before();
-            mbar_arrive(&sm.p_full[sb]);
-        }
-        // epilogue: O / l -> bf16 once the last PV is done (the tensor pipe completes in order)
-        mbar_wait(&sm.pv_done[(n_kt - 1) & 1], ((n_kt - 1) >> 1) & 1);
-        tc_fence_after();
-        const float inv = l > 0.f ? 1.f / l : 0.f;
-        __nv_bfloat16 *orow = EXT ? p.out + (((size_t)b * p.len + qi) * p.Hq + h) * PF_D
-                                  : p.out + ((size_t)qrow * p.total + s0 + qi) * PF_D;
+            // epilogue: O / l -> bf16 once the item's last PV is done (the tensor pipe
+            // completes in order); then O is released to the next item's first PV
+            mbar_wait(&sm.pv_done[(t - 1) & 1], ((t - 1) >> 1) & 1);
+            tc_fence_after();
+            const float inv = l > 0.f ? 1.f / l : 0.f;
+            uint32_t o[4][32];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            uint32_t o[32];
-            tmem_ld32(tO + lane_off + c * 32, o);
+            for (int c = 0; c < 4; ++c) tmem_ld32(tO + lane_off + c * 32, o[c]);
             tmem_wait_ld();
-            if (qi < len) {
-                uint32_t w[16];
+            tc_fence_before();
+            mbar_arrive(&sm.o_free);
+            if (qi < it.len) {
+                __nv_bfloat16 *orow = EXT ? p.out + (((size_t)it.b * p.len + qi) * p.Hq + it.h) * PF_D
+                                          : p.out + ((size_t)it.h * p.total + it.s0 + qi) * PF_D;
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const __nv_bfloat162 b = __floats2bfloat162_rn(__uint_as_float(o[2 * i]) * inv,
-                                                                   __uint_as_float(o[2 * i + 1]) * inv);
-                    w[i] = *reinterpret_cast<const uint32_t *>(&b);
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t wv[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const __nv_bfloat162 b = __floats2bfloat162_rn(__uint_as_float(o[c][2 * i]) * inv,
+                                                                       __uint_as_float(o[c][2 * i + 1]) * inv);
+                        wv[i] = *reinterpret_cast<const uint32_t *>(&b);
+                    }
+                    uint4 *o4 = reinterpret_cast<uint4 *>(orow + c * 32);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) o4[i] = make_uint4(wv[4 * i], wv[4 * i + 1], wv[4 * i + 2], wv[4 * i + 3]);
                 }
-                uint4 *o4 = reinterpret_cast<uint4 *>(orow + c * 32);
-#pragma unroll
-                for (int i = 0; i < 4; ++i) o4[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
             }
         }
     }
@@ -425,6 +525,7 @@ bool prefill_supported(int head_dim) { return head_dim == PF_D; }
 
 namespace {
 float g_rescale_override = -1.f;   // baton_debug_prefill_rescale_t
+int g_grid_cap = 0;                // baton_debug_prefill_grid
 // lazy-rescale threshold in log2 units: BATON_PF_RESCALE_T, default 8 (0 = rescale
 // whenever the row max moves)
 float pf_rescale_t() {
@@ -438,6 +539,15 @@ float pf_rescale_t() {
     return t;
 }
 
+bool pf_persist() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("BATON_PF_PERSIST");
+        v = e ? atoi(e) != 0 : 1;
+    }
+    return v != 0;
+}
+
 cudaError_t launch_pf(const CUtensorMap &mq, const CUtensorMap &mk, const CUtensorMap &mv, const PfParams &p,
                       int slots, cudaStream_t s) {
     const size_t smem = sizeof(PfSmem) + 1024;
@@ -449,10 +559,16 @@ cudaError_t launch_pf(const CUtensorMap &mq, const CUtensorMap &mk, const CUtens
                             : ensure_smem_attr(prefill_attention_kernel<false>, smem);
         if (e != cudaSuccess) return e;
     }
+    // prefill: n_mtiles = number of (prompt, query tile) entries
+    pp.n_items = p.n_mtiles * p.Hq * (ext ? slots : 1);
+    // persistent grid: two CTAs per SM walk the items (BATON_PF_PERSIST=0: one CTA per
+    // item, the round-1 launch shape, for A/B runs)
+    int grid = pf_persist() ? std::min(pp.n_items, 2 * device_sms()) : pp.n_items;
+    if (g_grid_cap > 0) grid = std::min(grid, g_grid_cap);   // tests: many items per CTA
     if (ext)
-        prefill_attention_kernel<true><<<p.n_mtiles * p.Hq * slots, PF_THREADS, smem, s>>>(mq, mk, mv, pp);
-    else   // prefill: n_mtiles = number of (prompt, query tile) entries
-        prefill_attention_kernel<false><<<p.n_mtiles * p.Hq, PF_THREADS, smem, s>>>(mq, mk, mv, pp);
+        prefill_attention_kernel<true><<<grid, PF_THREADS, smem, s>>>(mq, mk, mv, pp);
+    else
+        prefill_attention_kernel<false><<<grid, PF_THREADS, smem, s>>>(mq, mk, mv, pp);
     return cudaGetLastError();
 }
 }  // namespace
@@ -576,5 +692,12 @@ extern "C" long long baton_debug_prefill_rescales(int reset) {
 }
 extern "C" int baton_debug_prefill_rescale_t(float t) {
     baton::g_rescale_override = t;
+    return 0;
+}
+// baton_debug_prefill_grid: cap the persistent grid at g CTAs (g <= 0 restores the
+// default), so tests can make every CTA walk many items (results are independent of
+// which CTA runs an item).
+extern "C" int baton_debug_prefill_grid(int g) {
+    baton::g_grid_cap = g > 0 ? g : 0;
     return 0;
 }

@@ -56,6 +56,13 @@ def main():
     # launch per prompt (same arithmetic, bit-identical rows)
     batches = [("13b", 40, 40, [600, 550]), ("7b", 32, 32, [1500, 350, 120, 900]),
                ("70b", 64, 8, [3400, 300, 200])]
+    # the bench line's prefill leg: 64 prompts of a config's length mix in one launch
+    from baton_inputs import config_workload
+    for cname, Hq, Hkv in (("7b", 32, 32), ("13b", 40, 40)):
+        wl = config_workload(cname)
+        batches.append((cname + "-mix64", Hq, Hkv, [q.l_q for q in wl.queries[:64]]))
+    wl = config_workload("70b")
+    batches.append(("70b-mix18", 64, 8, [q.l_q for q in wl.queries[:18]]))
     for name, Hq, Hkv, lens in ([] if args.only else batches):
         D, T = 128, sum(lens)
         q = torch.randn((Hq, T, D), device="cuda").to(torch.bfloat16)
@@ -72,7 +79,7 @@ def main():
             s0 += n
         us_s = graph_us(lambda: [baton_prefill_attention(a, b, c, d, n, Hq, Hkv, D) for a, b, c, d, n in parts])
         flops = sum(4.0 * Hq * D * (n * (n + 1) / 2) for n in lens)
-        print(json.dumps({"shape": name, "varlen": lens, "q_heads": Hq, "kv_heads": Hkv, "us": us_v,
+        print(json.dumps({"shape": name, "varlen": lens if len(lens) <= 8 else f"{len(lens)} prompts, {sum(lens)} tokens", "q_heads": Hq, "kv_heads": Hkv, "us": us_v,
                           "us_separate": us_s, "tflops": flops / us_v / 1e6,
                           "tflops_separate": flops / us_s / 1e6, "frac": flops / us_v / 1e6 / peak}))
 

@@ -162,3 +162,44 @@ def test_prefill_varlen_max_prompts_bitwise():
         torch.cuda.synchronize()
         assert np.array_equal(bf16_bits(O[:, sl]), bf16_bits(o1)), n
         s0 += n
+
+
+@pytest.fixture
+def grid_cap():
+    """Cap the persistent prefill grid (baton_debug_prefill_grid) so every CTA walks
+    many work items: the Q reload, the K/V ring, the S buffers and the O hand-over run
+    on across items (prefill_attention.cu, PfWalk)."""
+    import ctypes
+    from paper_2410_18701_b200 import _lib
+    lib = _lib.lib
+    lib.baton_debug_prefill_grid.restype = ctypes.c_int
+    lib.baton_debug_prefill_grid.argtypes = [ctypes.c_int]
+    yield lib.baton_debug_prefill_grid
+    lib.baton_debug_prefill_grid(0)
+
+
+@pytest.mark.parametrize("cap", [1, 3, 7])
+def test_prefill_persistent_walk_bitwise(grid_cap, cap):
+    """Which CTA runs an item, and after which items, never changes a bit: a varlen
+    launch (ragged prompts, 1-token and tile-boundary lengths, GQA) on a grid of `cap`
+    CTAs equals the default grid bitwise, and the oracle on sampled rows."""
+    require_cuda()
+    from paper_2410_18701_b200.baton import baton_prefill_attention_varlen
+    Hq, Hkv, lens = 8, 2, [700, 1, 33, 256, 129, 128, 511, 64]
+    Q, K, V = _packed(91, Hq, Hkv, lens)
+    ref = torch.empty_like(Q)
+    baton_prefill_attention_varlen(Q, K, V, ref, lens, Hq, Hkv, 128)
+    grid_cap(cap)
+    O = torch.full_like(Q, float("nan"))
+    baton_prefill_attention_varlen(Q, K, V, O, lens, Hq, Hkv, 128)
+    torch.cuda.synchronize()
+    assert np.array_equal(bf16_bits(O), bf16_bits(ref))
+    got = bits_to_f64(bf16_bits(O))
+    s0, worst = 0, 0.0
+    for n in lens:
+        sl = slice(s0, s0 + n)
+        rows = sorted({0, n - 1, n // 2})
+        r = _reference(Q[:, sl], K[:, sl], V[:, sl], rows)
+        worst = max(worst, max(row_rel_err(got[:, s0 + i], r[i]) for i in rows))
+        s0 += n
+    assert worst <= ATTN_RTOL, worst

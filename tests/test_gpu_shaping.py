@@ -189,3 +189,27 @@ def test_engine_shape_policy_replay(wl_fn):
     assert set(eng.outputs) == set(sim.outputs)
     worst = max(row_rel_err(eng.outputs[k], o) for k, o in sim.outputs.items())
     assert worst <= ATTN_RTOL, worst
+
+
+@pytest.mark.parametrize("cap", [1, 5])
+def test_shaping_replay_persistent_walk(cap):
+    """The extend attention on a capped persistent grid (baton_debug_prefill_grid): one
+    CTA (or five) walks every (slot, head, query tile) item of a shaped iteration,
+    empty slots (zero rows) included, and the whole replay still matches the oracle
+    bit for bit in state and within C13 in outputs."""
+    require_cuda()
+    import ctypes
+    from paper_2410_18701_b200 import _lib
+    lib = _lib.lib
+    lib.baton_debug_prefill_grid.restype = ctypes.c_int
+    lib.baton_debug_prefill_grid.argtypes = [ctypes.c_int]
+    qs = [Query(0, 0, 300, 40), Query(1, 0, 170, 30), Query(2, 0, 90, 50),
+          Query(3, 5, 260, 20), Query(4, 5, 140, 25), Query(5, 12, 333, 10)]
+    wl = Workload("shape-walk", qs, layers=1, q_heads=4, kv_heads=2, head_dim=128, slots=4,
+                  max_ctx=2048)
+    lib.baton_debug_prefill_grid(cap)
+    try:
+        n, _ = _replay(wl)
+    finally:
+        lib.baton_debug_prefill_grid(0)
+    assert n >= 3
