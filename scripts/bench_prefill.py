@@ -20,7 +20,7 @@ from paper_2410_18701_b200.baton import baton_prefill_attention, baton_prefill_a
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=20)
-    ap.add_argument("--only", default=None, help="e.g. 70b:3400 (one shape)")
+    ap.add_argument("--only", default=None, help="one shape: e.g. 70b:3400 or 7b-mix64")
     args = ap.parse_args()
     peak = 1657.7
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -28,8 +28,6 @@ def main():
         peak = json.load(open(p))["bf16_tflops"]
     shapes = [("7b", 32, 32, 512), ("7b", 32, 32, 1024), ("7b", 32, 32, 1800),
               ("13b", 40, 40, 1024), ("70b", 64, 8, 3400)]
-    if args.only:
-        shapes = [s for s in shapes if f"{s[0]}:{s[3]}" == args.only]
     def graph_us(fn):
         for _ in range(3):
             fn()
@@ -63,7 +61,10 @@ def main():
         batches.append((cname + "-mix64", Hq, Hkv, [q.l_q for q in wl.queries[:64]]))
     wl = config_workload("70b")
     batches.append(("70b-mix18", 64, 8, [q.l_q for q in wl.queries[:18]]))
-    for name, Hq, Hkv, lens in ([] if args.only else batches):
+    if args.only:   # a batch by name (e.g. 7b-mix64) or one single-prompt shape
+        batches = [b for b in batches if b[0] == args.only]
+        shapes = [s for s in shapes if f"{s[0]}:{s[3]}" == args.only]
+    for name, Hq, Hkv, lens in batches:
         D, T = 128, sum(lens)
         q = torch.randn((Hq, T, D), device="cuda").to(torch.bfloat16)
         k = torch.randn((Hkv, T, D), device="cuda").to(torch.bfloat16)
