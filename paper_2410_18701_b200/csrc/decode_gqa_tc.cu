@@ -44,7 +44,7 @@ namespace baton {
 // [6+4j] softmax published P(j), [7+4j] MMA issued P.V(j).
 constexpr int TT_CTAS = BATON_EXPERIMENTS ? 160 : 1, TT_W = 68;
 __device__ int g_tt_on;
-__device__ long long g_tt[TT_CTAS][TT_W];
+__device__ long long g_tt[2][TT_CTAS][TT_W];
 
 namespace {
 using namespace tc;
@@ -146,7 +146,7 @@ decode_gqa_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_cons
     TSmem &sm = *reinterpret_cast<TSmem *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool trace = BATON_EXPERIMENTS && g_tt_on && blockIdx.x < TT_CTAS;
-    long long *tr = g_tt[trace ? blockIdx.x : 0];
+    long long *tr = g_tt[(p.prev_partial && p.partial > p.prev_partial) ? 1 : 0][trace ? blockIdx.x : 0];
     if (trace && threadIdx.x == 0) tr[0] = tt_now();
 
     if (threadIdx.x == 0) {
@@ -416,6 +416,7 @@ decode_gqa_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_cons
             griddep_wait();
             griddep_launch_dependents();
         }
+        if (trace && threadIdx.x == 0) tr[2] = tt_now();
         // decode step: the previous layer's split-K merge (its partials are complete and
         // visible once griddepcontrol.wait returned), by group 1 only: group 0 starts on
         // this layer's first item at once (4 warps x 2 pairs x 148 CTAs still cover the
@@ -423,6 +424,7 @@ decode_gqa_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_cons
         if (p.prev_partial && grp == 1)
             gqa_merge_pairs(p.lens, p.prev_partial, p.prev_out, p.B, p.Hq, p.max_chunks,
                             blockIdx.x * 4 + wq, gridDim.x * 4, lane);
+        if (trace && p.prev_partial && threadIdx.x == 128) tr[3] = tt_now();
         for (int b = blockIdx.x; b < p.B; b += gridDim.x) {   // empty slots -> zero rows (C6)
             if (p.lens[b] <= 0) {
                 uint4 *o = reinterpret_cast<uint4 *>(p.out + (size_t)b * p.Hq * D);
@@ -693,7 +695,7 @@ extern "C" int baton_debug_gqa_tc_trace(int on, void *host, size_t bytes) {
     }
     if (on >= 0) {
         if (on) {
-            static long long zero[baton::TT_CTAS][baton::TT_W];
+            static long long zero[2][baton::TT_CTAS][baton::TT_W];
             cudaMemcpyToSymbol(baton::g_tt, zero, sizeof(zero));
         }
         if (cudaMemcpyToSymbol(baton::g_tt_on, &on, sizeof(int)) != cudaSuccess) return -1;

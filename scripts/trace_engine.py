@@ -32,7 +32,7 @@ def main():
     mha = args.config != "70b"
     tc = not mha and os.environ.get("BATON_GQA_VARIANT") in ("20", "21")
     fn = lib.baton_debug_mha_trace if mha else (lib.baton_debug_gqa_tc_trace if tc else lib.baton_debug_gqa_trace)
-    shape = (8, 1024, 32) if mha else ((1, 160, 68) if tc else (8, 256, 64))
+    shape = (8, 1024, 32) if mha else ((2, 160, 68) if tc else (8, 256, 64))
     fn.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t]
     hook = {}
     orig_run = bench_configs.Engine.iteration
@@ -64,14 +64,34 @@ def main():
     bench_configs.Engine.iteration = counted
     res = bench_configs.run(args.config, steps, warm, torch.device("cuda"))
     buf = hook["buf"]
-    if tc:   # one launch (the step's last layer): entry spread, first S issue, exits
-        rows = buf[0][buf[0][:, 0] > 0]
-        t0 = rows[:, 0].min()
-        first_s = [r[4] - t0 for r in rows if r[4]]
-        print(json.dumps({"tc_ctas": len(rows), "enter_spread_ns": int(rows[:, 0].max() - t0),
-                          "first_S_med_ns": float(np.median(first_s)), "first_S_min_ns": int(min(first_s)),
-                          "exit_med_ns": float(np.median(rows[:, 1] - t0)), "exit_max_ns": int(rows[:, 1].max() - t0)}))
+    if tc:   # two consecutive launches (the layer-parity slots): the chain between them
+        launches = []
+        for sl in range(2):
+            rows = buf[sl][buf[sl][:, 0] > 0]
+            if len(rows):
+                launches.append(rows)
+        launches.sort(key=lambda r: r[:, 0].min())
+        t0 = launches[0][:, 0].min()
+        out = []
+        for rows in launches:
+            first_s = [r[4] - t0 for r in rows if r[4]]
+            waits = [r[2] - t0 for r in rows if r[2]]
+            merges = [r[3] - t0 for r in rows if r[3]]
+            out.append({"ctas": int(len(rows)), "enter_min": int(rows[:, 0].min() - t0),
+                        "enter_max": int(rows[:, 0].max() - t0),
+                        "wait_ret_min": int(min(waits)) if waits else None,
+                        "wait_ret_med": float(np.median(waits)) if waits else None,
+                        "wait_ret_max": int(max(waits)) if waits else None,
+                        "merge_done_med": float(np.median(merges)) if merges else None,
+                        "merge_done_max": int(max(merges)) if merges else None,
+                        "first_S_min": int(min(first_s)) if first_s else None,
+                        "first_S_med": float(np.median(first_s)) if first_s else None,
+                        "exit_min": int(rows[:, 1].min() - t0),
+                        "exit_med": float(np.median(rows[:, 1] - t0)), "exit_max": int(rows[:, 1].max() - t0)})
+        for x in out:
+            print(json.dumps(x))
         print(json.dumps({"config_run": res}))
+        json.dump({"launches": out, "raw": buf.tolist()}, open(args.out, "w"))
         return
     t0 = buf[:, :, 0][buf[:, :, 0] > 0].min()
     layers = []
