@@ -539,6 +539,27 @@ float pf_rescale_t() {
     return t;
 }
 
+// varlen item order (BATON_PF_ORDER): 0 = L2 panels (default), 1 = global heaviest
+// first, 2 = prompt-major
+int pf_order() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("BATON_PF_ORDER");
+        v = e ? atoi(e) : 0;
+        if (v < 0 || v > 2) v = 0;
+    }
+    return v;
+}
+int pf_panel_mb() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("BATON_PF_PANEL_MB");
+        v = e ? atoi(e) : 64;
+        if (v < 0) v = 0;
+    }
+    return v;
+}
+
 bool pf_persist() {
     static int v = -1;
     if (v < 0) {
@@ -617,7 +638,44 @@ cudaError_t launch_prefill_attention_varlen(const void *q, const void *k, const 
         const int len = p.vl_len[e >> 16], q0 = (int)(e & 0xffff) * PF_M;
         return (std::min(q0 + PF_M, len) + PF_N - 1) / PF_N;
     };
-    std::stable_sort(p.vl_tile, p.vl_tile + ne, [&](uint32_t a, uint32_t b) { return cost(a) > cost(b); });
+    if (pf_order() == 2) {
+        // prompt-major: longest prompt first, its query tiles heaviest first
+        std::stable_sort(p.vl_tile, p.vl_tile + ne, [&](uint32_t a, uint32_t b) {
+            const int la = p.vl_len[a >> 16], lb = p.vl_len[b >> 16];
+            if (la != lb) return la > lb;
+            if ((a >> 16) != (b >> 16)) return (a >> 16) < (b >> 16);
+            return (a & 0xffff) > (b & 0xffff);
+        });
+    } else {
+        // L2 panels: prompts longest first are cut into panels of <= panel_bytes of K/V
+        // (BATON_PF_PANEL_MB, default 64 of the 126 MB L2; 0 = one panel); items run
+        // panel by panel, heaviest first within a panel.  The items in flight then share
+        // a panel's prompts, so each (prompt, kv head)'s K/V is read from HBM about once
+        // and reused from L2 by its other query tiles, while within a panel the
+        // heaviest-first order keeps the CTAs' loads even.
+        int order[VL_MAXP], panel[VL_MAXP];
+        for (int i = 0; i < n; ++i) order[i] = i;
+        std::stable_sort(order, order + n, [&](int a, int b) { return p.vl_len[a] > p.vl_len[b]; });
+        const double cap = (double)pf_panel_mb() * (1 << 20);
+        double acc = 0.0;
+        int pid = 0;
+        for (int i = 0; i < n; ++i) {
+            const double kv = 4.0 * p.vl_len[order[i]] * kv_heads * head_dim;   // K + V bytes
+            if (cap > 0 && acc > 0 && acc + kv > cap) {
+                ++pid;
+                acc = 0.0;
+            }
+            acc += kv;
+            panel[order[i]] = pid;
+        }
+        std::stable_sort(p.vl_tile, p.vl_tile + ne, [&](uint32_t a, uint32_t b) {
+            const int pa = panel[a >> 16], pb = panel[b >> 16];
+            if (pa != pb) return pa < pb;
+            return pf_order() == 1 ? false : cost(a) > cost(b);
+        });
+        if (pf_order() == 1)   // global heaviest first (round 1)
+            std::stable_sort(p.vl_tile, p.vl_tile + ne, [&](uint32_t a, uint32_t b) { return cost(a) > cost(b); });
+    }
     const int total = cu_lens[n];
     CUtensorMap mq, mk, mv;
     if (!make_map(&mq, q, q_heads, total, PF_M) || !make_map(&mk, k, kv_heads, total, PF_N) ||

@@ -21,6 +21,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--only", default=None, help="one shape: e.g. 70b:3400 or 7b-mix64")
+    ap.add_argument("--batches-only", action="store_true", help="only the varlen batches and mixes")
     args = ap.parse_args()
     peak = 1657.7
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -84,7 +85,7 @@ def main():
                           "us_separate": us_s, "tflops": flops / us_v / 1e6,
                           "tflops_separate": flops / us_s / 1e6, "frac": flops / us_v / 1e6 / peak}))
 
-    for name, Hq, Hkv, n in shapes:
+    for name, Hq, Hkv, n in ([] if args.batches_only else shapes):
         D = 128
         q = torch.randn((Hq, n, D), device="cuda").to(torch.bfloat16)
         k = torch.randn((Hkv, n, D), device="cuda").to(torch.bfloat16)
