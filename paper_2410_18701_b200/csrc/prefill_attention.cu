@@ -614,32 +614,30 @@ bool use_fa4() {
 }
 }  // namespace
 
-cudaError_t launch_prefill_attention_varlen(const void *q, const void *k, const void *v, void *out,
-                                            const int32_t *cu_lens, int n, int q_heads, int kv_heads,
-                                            int head_dim, float scale, cudaStream_t s) {
-    if (head_dim != PF_D || n < 1 || n > VL_MAXP || cu_lens[0] != 0) return cudaErrorInvalidValue;
-#if BATON_EXPERIMENTS
-    if (use_fa4()) return launch_prefill_fa4_varlen(q, k, v, out, cu_lens, n, q_heads, kv_heads, scale, pf_rescale_t(), s);
-#endif
-    PfParams p{};
-    // (prompt, query tile) entries, heaviest first (key tiles up to the diagonal),
-    // ties by prompt then tile: a longest-processing-time order over all prompts
+// The varlen launch's work list: the (prompt, query tile) entries of n packed prompts,
+// in the order the persistent grid walks them (x q heads, heads fastest).  Returns the
+// number of entries, or -1 for an invalid cu_lens / too many entries.  Host only.
+static int pf_plan(const int32_t *cu_lens, int n, int kv_heads, int head_dim, PfParams &p) {
+    if (n < 1 || n > VL_MAXP || cu_lens[0] != 0) return -1;
     int ne = 0;
     for (int i = 0; i < n; ++i) {
         const int len = cu_lens[i + 1] - cu_lens[i];
-        if (len < 1) return cudaErrorInvalidValue;
+        if (len < 1) return -1;
         p.vl_start[i] = cu_lens[i];
         p.vl_len[i] = len;
         const int nm = (len + PF_M - 1) / PF_M;
-        if (ne + nm > VL_MAXT || nm > 0xffff) return cudaErrorInvalidValue;
+        if (ne + nm > VL_MAXT || nm > 0xffff) return -1;
         for (int mt = 0; mt < nm; ++mt) p.vl_tile[ne++] = ((uint32_t)i << 16) | (uint32_t)mt;
     }
+    // cost of an entry: its key tiles up to the diagonal
     auto cost = [&](uint32_t e) {
         const int len = p.vl_len[e >> 16], q0 = (int)(e & 0xffff) * PF_M;
         return (std::min(q0 + PF_M, len) + PF_N - 1) / PF_N;
     };
-    if (pf_order() == 2) {
-        // prompt-major: longest prompt first, its query tiles heaviest first
+    const int order_mode = pf_order();
+    if (order_mode == 1) {   // global heaviest first (round 1)
+        std::stable_sort(p.vl_tile, p.vl_tile + ne, [&](uint32_t a, uint32_t b) { return cost(a) > cost(b); });
+    } else if (order_mode == 2) {   // prompt-major: longest prompt first, its tiles heaviest first
         std::stable_sort(p.vl_tile, p.vl_tile + ne, [&](uint32_t a, uint32_t b) {
             const int la = p.vl_len[a >> 16], lb = p.vl_len[b >> 16];
             if (la != lb) return la > lb;
@@ -647,12 +645,13 @@ cudaError_t launch_prefill_attention_varlen(const void *q, const void *k, const 
             return (a & 0xffff) > (b & 0xffff);
         });
     } else {
-        // L2 panels: prompts longest first are cut into panels of <= panel_bytes of K/V
-        // (BATON_PF_PANEL_MB, default 64 of the 126 MB L2; 0 = one panel); items run
-        // panel by panel, heaviest first within a panel.  The items in flight then share
-        // a panel's prompts, so each (prompt, kv head)'s K/V is read from HBM about once
+        // L2 panels (default): prompts longest first are cut into panels of <= 64 MB of
+        // K/V (BATON_PF_PANEL_MB; 0 = one panel) of the 126 MB L2; entries run panel by
+        // panel, heaviest first within a panel.  The items in flight then share a
+        // panel's prompts, so each (prompt, kv head)'s K/V is read from HBM about once
         // and reused from L2 by its other query tiles, while within a panel the
-        // heaviest-first order keeps the CTAs' loads even.
+        // heaviest-first order keeps the CTAs' loads even.  A batch that fits one panel
+        // keeps the round-1 order.
         int order[VL_MAXP], panel[VL_MAXP];
         for (int i = 0; i < n; ++i) order[i] = i;
         std::stable_sort(order, order + n, [&](int a, int b) { return p.vl_len[a] > p.vl_len[b]; });
@@ -671,11 +670,22 @@ cudaError_t launch_prefill_attention_varlen(const void *q, const void *k, const 
         std::stable_sort(p.vl_tile, p.vl_tile + ne, [&](uint32_t a, uint32_t b) {
             const int pa = panel[a >> 16], pb = panel[b >> 16];
             if (pa != pb) return pa < pb;
-            return pf_order() == 1 ? false : cost(a) > cost(b);
+            return cost(a) > cost(b);
         });
-        if (pf_order() == 1)   // global heaviest first (round 1)
-            std::stable_sort(p.vl_tile, p.vl_tile + ne, [&](uint32_t a, uint32_t b) { return cost(a) > cost(b); });
     }
+    return ne;
+}
+
+cudaError_t launch_prefill_attention_varlen(const void *q, const void *k, const void *v, void *out,
+                                            const int32_t *cu_lens, int n, int q_heads, int kv_heads,
+                                            int head_dim, float scale, cudaStream_t s) {
+    if (head_dim != PF_D || n < 1 || n > VL_MAXP || cu_lens[0] != 0) return cudaErrorInvalidValue;
+#if BATON_EXPERIMENTS
+    if (use_fa4()) return launch_prefill_fa4_varlen(q, k, v, out, cu_lens, n, q_heads, kv_heads, scale, pf_rescale_t(), s);
+#endif
+    PfParams p{};
+    const int ne = pf_plan(cu_lens, n, kv_heads, head_dim, p);
+    if (ne < 0) return cudaErrorInvalidValue;
     const int total = cu_lens[n];
     CUtensorMap mq, mk, mv;
     if (!make_map(&mq, q, q_heads, total, PF_M) || !make_map(&mk, k, kv_heads, total, PF_N) ||
@@ -758,4 +768,15 @@ extern "C" int baton_debug_prefill_rescale_t(float t) {
 extern "C" int baton_debug_prefill_grid(int g) {
     baton::g_grid_cap = g > 0 ? g : 0;
     return 0;
+}
+// baton_debug_prefill_plan: the varlen launch's (prompt, query tile) work list in walk
+// order, each entry prompt << 16 | tile, for n packed prompts (cu_lens[n + 1], host);
+// writes at most cap entries to `out` and returns their total count, or -1 if the
+// launch would refuse cu_lens.  Host only (no device work): CPU tests check the order.
+extern "C" int baton_debug_prefill_plan(const int32_t *cu_lens, int n, int kv_heads, int head_dim, uint32_t *out,
+                                        int cap) {
+    static baton::PfParams p;   // ~9 KB: not on the caller's stack
+    const int ne = baton::pf_plan(cu_lens, n, kv_heads, head_dim, p);
+    for (int i = 0; i < ne && i < cap; ++i) out[i] = p.vl_tile[i];
+    return ne;
 }
