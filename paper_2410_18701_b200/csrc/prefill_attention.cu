@@ -103,6 +103,7 @@ struct PfParams {
     int n_items;                    // work items (prefill: entries x Hq; extend: n_mtiles x Hq x slots)
     float scale_log2;
     float rescale_t;                // lazy-rescale threshold (log2 units): P <= 2^rescale_t
+    int skip;                       // prefill: skip causally dead 32-key chunks and dead warps (BATON_PF_SKIP)
     __nv_bfloat16 *out;
     // extend only (lens == nullptr for prefill)
     const int32_t *lens, *pad;      // device metadata AFTER the shaped mask update
@@ -363,6 +364,8 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
             }
             float m = -INFINITY, l = 0.f;
             const int mrow = ext ? (int)(((size_t)it.b * p.max_ctx + it.kpad) & 15) : 0;   // mask byte offset
+            // this warp's 32 rows are all past the prompt (prefill only: see the skips below)
+            const bool rows_dead = !EXT && p.skip && q0 + warp * 32 >= it.len;
             for (int j = 0; j < it.n_kt; ++j, ++t) {
                 const int sb = t & 1;
                 const uint32_t tSj = tS + 64 * sb + lane_off;
@@ -378,82 +381,102 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
                 const bool diag = kbase + PF_N > off + q0;   // tile touches the causal diagonal
                 const uint8_t *mk = sm.mk[sb] + mrow;
                 if (ext) mbar_wait(&sm.v_full[sb], (t >> 1) & 1);   // this tile's mask bytes
-                uint32_t r[2][32];
-                tmem_ld32(tSj, r[0]);
-                tmem_ld32(tSj + 32, r[1]);
-                tmem_wait_ld();
-                // Masked keys become -inf in the RAW scores; the scale (> 0) is folded into
-                // the exponent (one FFMA + ex2 per key) and the row max is taken raw.  Tiles
-                // off the diagonal (and prefill has no mask) skip the per-key tests.
-                if (diag || ext) {
+                // Warp-uniform skips: a 32-key chunk whose first key is past this warp's
+                // last row is causally dead for all 32 rows (the upper triangle of the
+                // diagonal block); a warp whose rows are all past the prompt writes no
+                // output.  Prefill only: in the extend kernel the extra branches made
+                // ptxas spill.  Neither loads S, takes exponentials or touches m, l; a dead
+                // chunk of a live warp gets P = 0 (its TMEM columns still hold S bits).
+                const int wlast = off + q0 + warp * 32 + 31;
+                const int live_c = rows_dead ? 0 : ((EXT || !p.skip) ? 2 : (kbase > wlast ? 0 : (kbase + 32 > wlast ? 1 : 2)));
+                if (live_c > 0) {
+                    uint32_t r[2][32];
+                    tmem_ld32(tSj, r[0]);
+                    tmem_ld32(tSj + 32, r[1]);
+                    tmem_wait_ld();
+                    // Masked keys become -inf in the RAW scores; the scale (> 0) is folded into
+                    // the exponent (one FFMA + ex2 per key) and the row max is taken raw.  Tiles
+                    // off the diagonal (and prefill has no mask) skip the per-key tests.
+                    if (diag || ext) {
 #pragma unroll
-                    for (int c = 0; c < 2; ++c)
+                        for (int c = 0; c < 2; ++c)
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) {
-                            const bool dead = (diag && kbase + c * 32 + i > off + qi) || (ext && mk[c * 32 + i] == 0);
-                            if (dead) r[c][i] = __float_as_uint(-INFINITY);
+                            for (int i = 0; i < 32; ++i) {
+                                const bool dead = c >= live_c || (diag && kbase + c * 32 + i > off + qi) ||
+                                                  (ext && mk[c * 32 + i] == 0);
+                                if (dead) r[c][i] = __float_as_uint(-INFINITY);
+                            }
+                    }
+                    float mx;
+                    {   // row max: 3-input FMNMX3 in four independent chains
+                        float a0 = -INFINITY, a1 = -INFINITY, a2 = -INFINITY, a3 = -INFINITY;
+#pragma unroll
+                        for (int i = 0; i < 32; i += 4) {
+                            a0 = fmax3(a0, __uint_as_float(r[0][i]), __uint_as_float(r[0][i + 1]));
+                            a1 = fmax3(a1, __uint_as_float(r[0][i + 2]), __uint_as_float(r[0][i + 3]));
+                            a2 = fmax3(a2, __uint_as_float(r[1][i]), __uint_as_float(r[1][i + 1]));
+                            a3 = fmax3(a3, __uint_as_float(r[1][i + 2]), __uint_as_float(r[1][i + 3]));
                         }
-                }
-                float mx;
-                {   // row max: 3-input FMNMX3 in four independent chains
-                    float a0 = -INFINITY, a1 = -INFINITY, a2 = -INFINITY, a3 = -INFINITY;
-#pragma unroll
-                    for (int i = 0; i < 32; i += 4) {
-                        a0 = fmax3(a0, __uint_as_float(r[0][i]), __uint_as_float(r[0][i + 1]));
-                        a1 = fmax3(a1, __uint_as_float(r[0][i + 2]), __uint_as_float(r[0][i + 3]));
-                        a2 = fmax3(a2, __uint_as_float(r[1][i]), __uint_as_float(r[1][i + 1]));
-                        a3 = fmax3(a3, __uint_as_float(r[1][i + 2]), __uint_as_float(r[1][i + 3]));
+                        mx = fmax3(fmaxf(a0, a1), a2, a3);
                     }
-                    mx = fmax3(fmaxf(a0, a1), a2, a3);
-                }
-                mx *= p.scale_log2;   // -inf stays -inf
-                // Lazy rescale: P is taken relative to a reference max m that moves only
-                // when the row max exceeds it by more than rescale_t (log2 units), so P <=
-                // 2^rescale_t (exact in fp32 accumulation, same bf16 rounding of P) and the
-                // O rows in TMEM are rescaled only on those tiles, not whenever the max moves.
-                // A row may see only masked keys so far (extend: holes, padding): keep exp2
-                // finite -- ex2(-inf - 0) = 0.
-                const float m_new = (mx > m + p.rescale_t || m == -INFINITY) ? fmaxf(m, mx) : m;
-                const float mref = (m_new == -INFINITY) ? 0.f : m_new;
-                const float alpha = ex2(m - mref);
-                const float nref = -mref;
-                // the row sum adds the fp32 exponentials; the P.V MMA multiplies their bf16
-                // roundings (relative difference <= 2^-9 per key, far inside C13's 1e-2)
-                float2 rs2 = make_float2(0.f, 0.f);
-                const float2 sc2 = make_float2(p.scale_log2, p.scale_log2), nr2 = make_float2(nref, nref);
+                    mx *= p.scale_log2;   // -inf stays -inf
+                    // Lazy rescale: P is taken relative to a reference max m that moves only
+                    // when the row max exceeds it by more than rescale_t (log2 units), so P <=
+                    // 2^rescale_t (exact in fp32 accumulation, same bf16 rounding of P) and the
+                    // O rows in TMEM are rescaled only on those tiles, not whenever the max moves.
+                    // A row may see only masked keys so far (extend: holes, padding): keep exp2
+                    // finite -- ex2(-inf - 0) = 0.
+                    const float m_new = (mx > m + p.rescale_t || m == -INFINITY) ? fmaxf(m, mx) : m;
+                    const float mref = (m_new == -INFINITY) ? 0.f : m_new;
+                    const float alpha = ex2(m - mref);
+                    const float nref = -mref;
+                    // the row sum adds the fp32 exponentials; the P.V MMA multiplies their bf16
+                    // roundings (relative difference <= 2^-9 per key, far inside C13's 1e-2)
+                    float2 rs2 = make_float2(0.f, 0.f);
+                    const float2 sc2 = make_float2(p.scale_log2, p.scale_log2), nr2 = make_float2(nref, nref);
 #pragma unroll
-                for (int c = 0; c < 2; ++c)
+                    for (int c = 0; c < 2; ++c) {
+                        if (c >= live_c) {
 #pragma unroll
-                    for (int i = 0; i < 32; i += 2) {
-                        float2 a = ffma2(make_float2(__uint_as_float(r[c][i]), __uint_as_float(r[c][i + 1])), sc2, nr2);
-                        a.x = ex2(a.x);
-                        a.y = ex2(a.y);
-                        const __nv_bfloat162 b = __floats2bfloat162_rn(a.x, a.y);
-                        rs2 = fadd2(rs2, a);
-                        pk[c * 16 + i / 2] = *reinterpret_cast<const uint32_t *>(&b);
-                    }
-                const float rs = rs2.x + rs2.y;
-                l = l * alpha + rs;
-                m = m_new;
-                // warp-uniform: tcgen05.ld/st are .sync.aligned (all 32 lanes converged)
-                if (j > 0 && __any_sync(FULL_MASK, alpha != 1.f)) {
-                    // O is stable once PV(t-1) is done (PV(t-3) on that barrier completed
-                    // before S(t-1), which this warp group already read: at most one phase behind)
-                    mbar_wait(&sm.pv_done[(t - 1) & 1], ((t - 1) >> 1) & 1);
-                    tc_fence_after();
-                    if (lane == 0) atomicAdd(&g_pf_rescales, 1ull);
-                    {
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) {
-                            uint32_t o[32];
-                            tmem_ld32(tO + lane_off + c * 32, o);
-                            tmem_wait_ld();
-#pragma unroll
-                            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-                            tmem_st32(tO + lane_off + c * 32, o);
+                            for (int i = 0; i < 16; ++i) pk[c * 16 + i] = 0u;
+                            continue;
                         }
-                        tmem_wait_st();
+#pragma unroll
+                        for (int i = 0; i < 32; i += 2) {
+                            float2 a = ffma2(make_float2(__uint_as_float(r[c][i]), __uint_as_float(r[c][i + 1])), sc2, nr2);
+                            a.x = ex2(a.x);
+                            a.y = ex2(a.y);
+                            const __nv_bfloat162 b = __floats2bfloat162_rn(a.x, a.y);
+                            rs2 = fadd2(rs2, a);
+                            pk[c * 16 + i / 2] = *reinterpret_cast<const uint32_t *>(&b);
+                        }
                     }
+                    const float rs = rs2.x + rs2.y;
+                    l = l * alpha + rs;
+                    m = m_new;
+                    // warp-uniform: tcgen05.ld/st are .sync.aligned (all 32 lanes converged)
+                    if (j > 0 && __any_sync(FULL_MASK, alpha != 1.f)) {
+                        // O is stable once PV(t-1) is done (PV(t-3) on that barrier completed
+                        // before S(t-1), which this warp group already read: at most one phase behind)
+                        mbar_wait(&sm.pv_done[(t - 1) & 1], ((t - 1) >> 1) & 1);
+                        tc_fence_after();
+                        if (lane == 0) atomicAdd(&g_pf_rescales, 1ull);
+                        {
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) {
+                                uint32_t o[32];
+                                tmem_ld32(tO + lane_off + c * 32, o);
+                                tmem_wait_ld();
+#pragma unroll
+                                for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+                                tmem_st32(tO + lane_off + c * 32, o);
+                            }
+                            tmem_wait_st();
+                        }
+                    }
+                } else if (!rows_dead) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) pk[i] = 0u;
                 }
                 // extend: cache rows past lens in this tile are stale memory (maybe NaN
                 // bits); P is 0 there but 0 * NaN is not, so zero those V rows (whole 128-B
@@ -468,9 +491,12 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
                     fence_async_smem();   // generic-proxy writes -> the tensor core's reads
                 }
                 // P row -> TMEM over the first 32 columns of this S buffer (bf16 pairs,
-                // key 2c in the low half of column c): the A operand of PV(t)
-                tmem_st32(tSj, pk);
-                tmem_wait_st();
+                // key 2c in the low half of column c): the A operand of PV(t).  Rows past
+                // the prompt keep whatever the columns hold: their O rows are never written.
+                if (!rows_dead) {
+                    tmem_st32(tSj, pk);
+                    tmem_wait_st();
+                }
                 tc_fence_before();
                 mbar_arrive(&sm.p_full[sb]);
             }
@@ -560,6 +586,16 @@ int pf_panel_mb() {
     return v;
 }
 
+// warp-uniform skips of dead key chunks / rows in the prefill softmax (BATON_PF_SKIP=0: off)
+int pf_skip() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("BATON_PF_SKIP");
+        v = e ? (atoi(e) != 0) : 1;
+    }
+    return v;
+}
+
 bool pf_persist() {
     static int v = -1;
     if (v < 0) {
@@ -574,6 +610,7 @@ cudaError_t launch_pf(const CUtensorMap &mq, const CUtensorMap &mk, const CUtens
     const size_t smem = sizeof(PfSmem) + 1024;
     PfParams pp = p;
     pp.rescale_t = pf_rescale_t();
+    pp.skip = pf_skip();
     const bool ext = p.lens != nullptr;
     {
         cudaError_t e = ext ? ensure_smem_attr(prefill_attention_kernel<true>, smem)
