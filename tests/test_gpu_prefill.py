@@ -203,3 +203,42 @@ def test_prefill_persistent_walk_bitwise(grid_cap, cap):
         worst = max(worst, max(row_rel_err(got[:, s0 + i], r[i]) for i in rows))
         s0 += n
     assert worst <= ATTN_RTOL, worst
+
+
+def test_prefill_varlen_config_mix_panels():
+    """The bench's prefill leg: the 7B config's first 64 prompts in ONE varlen launch
+    (31k tokens, 508 MB of K/V: the work list runs in several 64 MB L2 panels, DESIGN
+    §6.3).  Every prompt's rows equal its own single-prompt launch bitwise (one panel,
+    round-1 order) for a sample of prompts, and the oracle (O-1 per prefix) on sampled
+    rows and heads."""
+    require_cuda()
+    from baton_inputs import config_workload
+    from paper_2410_18701_b200.baton import baton_prefill_attention, baton_prefill_attention_varlen
+    lens = [q.l_q for q in config_workload("7b").queries[:64]]
+    Hq = Hkv = 32
+    T = sum(lens)
+    assert 4 * T * Hkv * 128 > 4 * (64 << 20)          # spans several panels
+    g = torch.Generator(device="cuda").manual_seed(64)
+    mk = lambda H: (torch.rand((H, T, 128), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    Q, K, V = mk(Hq), mk(Hkv), mk(Hkv)
+    O = torch.full_like(Q, float("nan"))
+    baton_prefill_attention_varlen(Q, K, V, O, lens, Hq, Hkv, 128)
+    torch.cuda.synchronize()
+    starts = np.concatenate([[0], np.cumsum(lens)])
+    order = sorted(range(64), key=lambda i: -lens[i])
+    sample = sorted({order[0], order[1], order[31], order[32], order[62], order[63], 0, 17})
+    worst = 0.0
+    for i in sample:
+        n, s0 = lens[i], int(starts[i])
+        sl = slice(s0, s0 + n)
+        q1, k1, v1 = Q[:, sl].contiguous(), K[:, sl].contiguous(), V[:, sl].contiguous()
+        o1 = torch.empty_like(q1)
+        baton_prefill_attention(q1, k1, v1, o1, n, Hq, Hkv, 128)
+        torch.cuda.synchronize()
+        assert np.array_equal(bf16_bits(O[:, sl]), bf16_bits(o1)), i
+        heads = [0, 13, 31]
+        rows = sorted({0, n // 3, n - 1})
+        ref = _reference(q1[heads], k1[heads], v1[heads], rows)
+        got = bits_to_f64(bf16_bits(O[heads][:, sl]))
+        worst = max(worst, max(row_rel_err(got[:, r], ref[r]) for r in rows))
+    assert worst <= ATTN_RTOL, worst
