@@ -2,7 +2,7 @@
 # round-2 closing evidence on HEAD: GPU suite, smoke, the default bench line (+ reference
 # arm), the 70b line, and the launch list of the bench command
 cd "$(dirname "$0")/.."
-O=gpurun_out/r02f
+O=${OUT:-gpurun_out/r02f}
 mkdir -p $O
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > $O/smoke.log 2>&1
 timeout 900 python bench.py > $O/bench.log 2>&1
