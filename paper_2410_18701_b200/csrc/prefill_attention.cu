@@ -72,6 +72,17 @@ using namespace tc;
 // branch is rare by design (the reference max moves by > rescale_t log2 units).
 __device__ unsigned long long g_pf_rescales = 0;
 
+// Debug timeline (experiment builds; baton_debug_prefill_trace, scripts/trace_prefill.py):
+// per CTA < PFT_CTAS, clock64 at [0] start, [1] end, and for the CTA's tiles t < 12:
+// [2+5t] MMA issued S(t) (after its commits), [3+5t] softmax warp 0 holds S(t),
+// [4+5t] softmax thread 0 published P(t), [5+5t] MMA thread's wait for P(t) returned,
+// [6+5t] MMA issued P.V(t) (after its commits).
+constexpr int PFT_CTAS = BATON_EXPERIMENTS ? 296 : 1, PFT_W = 62, PFT_T = 12;
+__device__ int g_pft_on;
+__device__ long long g_pft[PFT_CTAS][PFT_W];
+#define PFT(t, f) \
+    if (BATON_EXPERIMENTS && g_pft_on && blockIdx.x < PFT_CTAS && (t) < PFT_T) g_pft[blockIdx.x][2 + 5 * (t) + (f)] = clock64()
+
 // packed fp32x2 FMA / add (SASS FFMA2 / FADD2): half the issue slots of the scalar ops
 BATON_DEV float2 ffma2(float2 a, float2 b, float2 c) {
     uint64_t A, B, C, D;
@@ -209,6 +220,7 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr bool ext = EXT;
 
+    if (BATON_EXPERIMENTS && g_pft_on && threadIdx.x == 0 && blockIdx.x < PFT_CTAS) g_pft[blockIdx.x][0] = clock64();
     if (threadIdx.x == 0) {
         mbar_init(&sm.bar_q, 1);
         mbar_init(&sm.q_empty, 1);
@@ -292,7 +304,10 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
         // and the tensor pipe executes in issue order.  S(t+2) may be the next item's
         // first tile (its Q tile must have landed); an item's first PV overwrites O,
         // so it waits until the softmax warps have read the previous item's O out.
-        if (lane == 0) {
+        // The whole warp walks the stream and waits; one elected lane issues (the
+        // tcgen05 ops under elect.sync compile to single UTCHMMA/UTCBAR instructions,
+        // not per-lane loops: the MMA thread's instruction stream paced the tile loop).
+        {
             constexpr uint32_t idS = idesc_bf16(PF_M, PF_N, 0);   // B = K tile, K-major
             constexpr uint32_t idO = idesc_bf16(PF_M, PF_D, 1);   // A = P (TMEM, K-major), B = V tile, MN-major
             const uint32_t qa = smem_u32(sm.q);
@@ -311,14 +326,19 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
                 mbar_wait(&sm.k_full[b2], (ts >> 1) & 1);
                 tc_fence_after();
                 const uint32_t ka = smem_u32(sm.k[b2]);
+                const bool last = ws.j == ws.it.n_kt - 1;
+                if (elect_one()) {
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {   // K = head_dim in steps of 16 (32 B)
-                    umma_f16(tS + 64 * b2, smem_desc(qa + (k >> 2) * Q_REGION + (k & 3) * 32, 16, 1024),
-                             smem_desc(ka + (k >> 2) * KV_REGION + (k & 3) * 32, 16, 1024), idS, k > 0);
+                    for (int k = 0; k < 8; ++k) {   // K = head_dim in steps of 16 (32 B)
+                        umma_f16(tS + 64 * b2, smem_desc(qa + (k >> 2) * Q_REGION + (k & 3) * 32, 16, 1024),
+                                 smem_desc(ka + (k >> 2) * KV_REGION + (k & 3) * 32, 16, 1024), idS, k > 0);
+                    }
+                    umma_commit(&sm.s_full[b2]);
+                    PFT(ts, 0);
+                    umma_commit(&sm.k_empty[b2]);
+                    if (last) umma_commit(&sm.q_empty);   // the item's last S: Q may go
                 }
-                umma_commit(&sm.s_full[b2]);
-                umma_commit(&sm.k_empty[b2]);
-                if (ws.j == ws.it.n_kt - 1) umma_commit(&sm.q_empty);   // the item's last S: Q may go
+                __syncwarp();
                 ++ts;
                 ws.advance();
             };
@@ -327,17 +347,23 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
             for (int t = 0; wp.valid; ++t) {
                 const int s = t & 1;
                 mbar_wait(&sm.p_full[s], (t >> 1) & 1);           // P(t) in TMEM, O rescaled
+                if (lane == 0) PFT(t, 3);
                 mbar_wait(&sm.v_full[s], (t >> 1) & 1);
                 if (wp.j == 0 && wp.seq > 0) mbar_wait(&sm.o_free, (wp.seq - 1) & 1);   // previous O read out
                 tc_fence_after();
                 const uint32_t va = smem_u32(sm.v[s]);
+                const bool first = wp.j == 0;
+                if (elect_one()) {
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {   // K = 64 keys in steps of 16 (8 TMEM columns of bf16 pairs)
-                    umma_f16_ts(tO, tS + 64 * s + 8 * k, smem_desc(va + k * 2048, KV_REGION, 1024), idO,
-                                (wp.j > 0 || k > 0));
+                    for (int k = 0; k < 4; ++k) {   // K = 64 keys in steps of 16 (8 TMEM columns of bf16 pairs)
+                        umma_f16_ts(tO, tS + 64 * s + 8 * k, smem_desc(va + k * 2048, KV_REGION, 1024), idO,
+                                    (!first || k > 0));
+                    }
+                    umma_commit(&sm.pv_done[s]);
+                    PFT(t, 4);
+                    umma_commit(&sm.v_empty[s]);
                 }
-                umma_commit(&sm.pv_done[s]);
-                umma_commit(&sm.v_empty[s]);
+                __syncwarp();
                 wp.advance();
                 if (ws.valid) issue_s();
             }
@@ -370,6 +396,7 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
                 const int sb = t & 1;
                 const uint32_t tSj = tS + 64 * sb + lane_off;
                 mbar_wait(&sm.s_full[sb], (t >> 1) & 1);
+                if (threadIdx.x == 0) PFT(t, 1);
                 // one thread observes PV(t-2)'s completion on its barrier: already done (S(t)
                 // was issued after it and its commit covers every earlier MMA), so this never
                 // blocks; it keeps every phase of pv_done waited on (compute-sanitizer
@@ -499,6 +526,7 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
                 }
                 tc_fence_before();
                 mbar_arrive(&sm.p_full[sb]);
+                if (threadIdx.x == 0) PFT(t, 2);
             }
             // epilogue: O / l -> bf16 once the item's last PV is done (the tensor pipe
             // completes in order); then O is released to the next item's first PV
@@ -532,6 +560,7 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_
     }
     tc_fence_before();
     __syncthreads();
+    if (BATON_EXPERIMENTS && g_pft_on && threadIdx.x == 0 && blockIdx.x < PFT_CTAS) g_pft[blockIdx.x][1] = clock64();
     if (warp == 0) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
@@ -816,4 +845,26 @@ extern "C" int baton_debug_prefill_plan(const int32_t *cu_lens, int n, int kv_he
     const int ne = baton::pf_plan(cu_lens, n, kv_heads, head_dim, p);
     for (int i = 0; i < ne && i < cap; ++i) out[i] = p.vl_tile[i];
     return ne;
+}
+// baton_debug_prefill_trace (experiment builds): on >= 0 switches the per-tile clock64
+// timeline on (zeroed) or off; host != nullptr copies it out ([CTA][62] int64).
+extern "C" int baton_debug_prefill_trace(int on, void *host, size_t bytes) {
+#if !BATON_EXPERIMENTS
+    (void)on;
+    (void)host;
+    (void)bytes;
+    return -1;
+#else
+    if (host && cudaMemcpyFromSymbol(host, baton::g_pft, bytes < sizeof(baton::g_pft) ? bytes : sizeof(baton::g_pft)) !=
+                    cudaSuccess)
+        return -1;
+    if (on >= 0) {
+        if (on) {
+            static long long zero[baton::PFT_CTAS][baton::PFT_W];
+            cudaMemcpyToSymbol(baton::g_pft, zero, sizeof(zero));
+        }
+        if (cudaMemcpyToSymbol(baton::g_pft_on, &on, sizeof(int)) != cudaSuccess) return -1;
+    }
+    return 0;
+#endif
 }
