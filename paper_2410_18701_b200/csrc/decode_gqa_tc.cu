@@ -309,7 +309,10 @@ decode_gqa_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_cons
         }
     } else if (warp == 9) {
         // ============================ S issuer ============================
-        if (lane == 0) {
+        // The whole warp walks the stages and waits; the tcgen05 ops go under elect.sync
+        // (single UTCHMMA / UTCBAR instructions, not ptxas's per-lane loops under a
+        // `lane == 0` test), lanes 0-15 patch the appended row, lane 0 writes the queues.
+        {
             constexpr uint32_t idS = idesc_bf16_ab(TK, NH, 0, 0);   // A = K (K-major), B = q (K-major)
             int stage = 0;
             uint32_t phase = 0;
@@ -323,44 +326,50 @@ decode_gqa_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_cons
                     for (int g = 0; g < 2; ++g) {   // end entries for both groups and P.V issuers
                         const int n = cnt[g], sb = n & 1;
                         if (n >= 2) mbar_wait(&sm.s_free[g][sb], ((n >> 1) - 1) & 1);
-                        sm.gq[g][sb].flags = F_END;
-                        sm.pvq[g][n & 3].flags = F_END;
-                        mbar_arrive(&sm.s_full[g][sb]);
-                        mbar_arrive(&sm.s_full[g][sb]);
+                        if (lane == 0) {
+                            sm.gq[g][sb].flags = F_END;
+                            sm.pvq[g][n & 3].flags = F_END;
+                            mbar_arrive(&sm.s_full[g][sb]);
+                            mbar_arrive(&sm.s_full[g][sb]);
+                        }
                     }
                     break;
                 }
                 const int g = d.item & 1, n = cnt[g], sb = n & 1;
                 if (n >= 2) mbar_wait(&sm.s_free[g][sb], ((n >> 1) - 1) & 1);   // S(n-2) read
-                if (d.flags & F_WRITE) {
+                if ((d.flags & F_WRITE) && lane < 16) {
                     // a2: row nrows-1 is the new token -- patch the swizzled K/V tiles
-                    // the MMAs read, then the cache row
-                    const int rr = d.nrows - 1;
+                    // the MMAs read, then the cache row (16-B chunk `lane` of each)
+                    const int rr = d.nrows - 1, ch = lane;
                     const size_t dst = (((size_t)d.b * p.Hkv + d.g) * p.max_ctx + d.wrow) * D;
-                    for (int ch = 0; ch < 16; ++ch) {
-                        const uint4 kv = reinterpret_cast<const uint4 *>(st.knew)[ch];
-                        const uint4 vv = reinterpret_cast<const uint4 *>(st.vnew)[ch];
-                        *reinterpret_cast<uint4 *>(st.k + swz(rr, ch, KREG)) = kv;
-                        *reinterpret_cast<uint4 *>(st.v + swz(rr, ch, KREG)) = vv;
-                        reinterpret_cast<uint4 *>(p.k_w + dst)[ch] = kv;
-                        reinterpret_cast<uint4 *>(p.v_w + dst)[ch] = vv;
-                    }
+                    const uint4 kv = reinterpret_cast<const uint4 *>(st.knew)[ch];
+                    const uint4 vv = reinterpret_cast<const uint4 *>(st.vnew)[ch];
+                    *reinterpret_cast<uint4 *>(st.k + swz(rr, ch, KREG)) = kv;
+                    *reinterpret_cast<uint4 *>(st.v + swz(rr, ch, KREG)) = vv;
+                    reinterpret_cast<uint4 *>(p.k_w + dst)[ch] = kv;
+                    reinterpret_cast<uint4 *>(p.v_w + dst)[ch] = vv;
                     fence_async_smem();
                 }
+                __syncwarp();
                 const uint32_t ka = smem_u32(st.k), qa = smem_u32(sm.q[g]);
                 const uint32_t tS = tmem + 32 * g + 16 * sb;
                 tc_fence_after();
+                if (elect_one()) {
 #pragma unroll
-                for (int k = 0; k < 8; ++k)   // K = 128 dims in steps of 16
-                    umma_f16(tS, smem_desc(ka + (k >> 2) * KREG + (k & 3) * 32, 16, 1024),
-                             smem_desc(qa + (k >> 2) * QREG + (k & 3) * 32, 16, 1024), idS, k > 0);
-                umma_commit(&sm.s_full[g][sb]);
-                if (d.flags & F_LAST) umma_commit(&sm.q_empty[g]);
-                sm.gq[g][sb] = d;
-                sm.pvq[g][n & 3] = PvEntry{d.stage, d.flags, d.b * p.Hq + d.g * GS,
-                                           (d.flags & F_LAST) && d.nchunks > 1};
-                mbar_arrive(&sm.s_full[g][sb]);            // release: the queue entries
-                if (trace && g == 0 && n < 16) tr[4 + 4 * n] = tt_now();
+                    for (int k = 0; k < 8; ++k)   // K = 128 dims in steps of 16
+                        umma_f16(tS, smem_desc(ka + (k >> 2) * KREG + (k & 3) * 32, 16, 1024),
+                                 smem_desc(qa + (k >> 2) * QREG + (k & 3) * 32, 16, 1024), idS, k > 0);
+                    umma_commit(&sm.s_full[g][sb]);
+                    if (d.flags & F_LAST) umma_commit(&sm.q_empty[g]);
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    sm.gq[g][sb] = d;
+                    sm.pvq[g][n & 3] = PvEntry{d.stage, d.flags, d.b * p.Hq + d.g * GS,
+                                               (d.flags & F_LAST) && d.nchunks > 1};
+                    mbar_arrive(&sm.s_full[g][sb]);            // release: the queue entries
+                    if (trace && g == 0 && n < 16) tr[4 + 4 * n] = tt_now();
+                }
                 cnt[g] = n + 1;
                 if (++stage == STAGES) {
                     stage = 0;
@@ -370,7 +379,8 @@ decode_gqa_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_cons
         }
     } else if (warp >= 10) {
         // ============================ P.V issuer of group (warp - 10) ============================
-        if (lane == 0) {
+        // whole warp waits, one elected lane issues (as the S issuer)
+        {
             const int g = warp - 10;
             constexpr uint32_t idO = idesc_bf16_ab(D, NH, 1, 0);    // A = V (MN-major), B = P^T (K-major)
             const uint32_t tO = tmem + 64 + 16 * g, pa = smem_u32(sm.p[g]);
@@ -383,7 +393,7 @@ decode_gqa_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_cons
                 if (pending < 0) return;
                 mbar_wait(&sm.pub[g], pub_phase);
                 pub_phase ^= 1;
-                red_add_release_gpu(p.tickets + pending, 1);
+                if (lane == 0) red_add_release_gpu(p.tickets + pending, 1);
                 pending = -1;
             };
             for (int n = 0;; ++n) {
@@ -395,14 +405,17 @@ decode_gqa_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_cons
                 }
                 tc_fence_after();
                 const uint32_t va = smem_u32(sm.st[e.stage].v);
+                if (elect_one()) {
 #pragma unroll
-                for (int k = 0; k < 8; ++k)   // K = 128 keys in steps of 16
-                    umma_f16(tO, smem_desc(va + k * 2048, KREG, 1024),
-                             smem_desc(pa + (k >> 2) * PREG + (k & 3) * 32, 16, 1024), idO,
-                             !((e.flags & F_FIRST) && k == 0));
-                umma_commit(&sm.o_done[g]);
-                umma_commit(&sm.empty[e.stage]);
-                if (trace && g == 0 && n < 16) tr[7 + 4 * n] = tt_now();
+                    for (int k = 0; k < 8; ++k)   // K = 128 keys in steps of 16
+                        umma_f16(tO, smem_desc(va + k * 2048, KREG, 1024),
+                                 smem_desc(pa + (k >> 2) * PREG + (k & 3) * 32, 16, 1024), idO,
+                                 !((e.flags & F_FIRST) && k == 0));
+                    umma_commit(&sm.o_done[g]);
+                    umma_commit(&sm.empty[e.stage]);
+                }
+                __syncwarp();
+                if (trace && g == 0 && n < 16 && lane == 0) tr[7 + 4 * n] = tt_now();
                 if (BATON_EXPERIMENTS && p.publish) {   // variant 23 (experiment builds)
                     publish();
                     if (e.multi) pending = e.bh0;
