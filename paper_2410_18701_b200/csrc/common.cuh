@@ -135,6 +135,16 @@ BATON_DEV int atom_add_acq_rel_gpu(int32_t *p, int v) {
 BATON_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 BATON_DEV void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// One lane of a converged warp (elect.sync): uniform-datapath ops under this
+// predicate (tcgen05.mma / commit, TMA and bulk copies) issue once, without the per-lane
+// ELECT loop ptxas wraps around them under a plain `lane == 0` test
+BATON_DEV bool elect_one() {
+    uint32_t e;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(e));
+    return e != 0;
+}
 // named barrier among `nthreads` threads (ids >= 1; 0 is __syncthreads)
 BATON_DEV void named_bar_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");

@@ -185,12 +185,19 @@ decode_gqa_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_cons
     if (warp == 8) {
         // ============================ producer ============================
         sched_build(sm.ws, p.lens, p.pad, p.B, p.Hkv, lane);
-        if (lane == 0) {
-            prefetch_tmap(&kmap);
-            prefetch_tmap(&vmap);
-            prefetch_tmap(&qmap);
-            prefetch_tmap(&kmap32);
-            prefetch_tmap(&vmap32);
+        // The whole warp walks the work list (identical state in every lane; the dynamic
+        // counter is drawn by lane 0 and broadcast) and waits on the ring; one elected
+        // lane per tile writes the stage descriptor and issues its loads, so the TMA ops
+        // compile to single UTMALDG instructions rather than per-lane loops.
+        {
+            if (elect_one()) {
+                prefetch_tmap(&kmap);
+                prefetch_tmap(&vmap);
+                prefetch_tmap(&qmap);
+                prefetch_tmap(&kmap32);
+                prefetch_tmap(&vmap32);
+            }
+            __syncwarp();
             const int total = sched_total(sm.ws, p.Hkv);
             int stage = 0, b = 0, item = 0, issued = 0;
             uint32_t phase = 0;
@@ -204,11 +211,17 @@ decode_gqa_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_cons
                 griddep_wait();
                 griddep_launch_dependents();
                 waited = true;
-                if (late_row >= 0) load_q(late_row, late_stage, late_par);
+                if (late_row >= 0 && elect_one()) load_q(late_row, late_stage, late_par);
+                __syncwarp();
                 late_row = -1;
             };
+            auto draw = [&]() {   // next dynamic item, one atomic per warp
+                int v = 0;
+                if (lane == 0) v = sched_next(p.counters);
+                return (int)gridDim.x + __shfl_sync(FULL_MASK, v, 0);
+            };
             int w = blockIdx.x;
-            int w_next = waited ? (int)gridDim.x + sched_next(p.counters) : -1;
+            int w_next = waited ? draw() : -1;
             while (w < total) {
                 int c, g;
                 sched_item(sm.ws, w, p.Hkv, b, c, g);
@@ -247,47 +260,47 @@ decode_gqa_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_cons
                     }
                     if (t == 0) bytes += 2 * QREG;
                     if (app_tile) bytes += 2 * D * 2;
-                    st.desc.b = b;
-                    st.desc.g = g;
-                    st.desc.c = c;
-                    st.desc.nrows = nr;
-                    st.desc.flags = (t == 0 ? F_FIRST : 0) | (t == ntiles - 1 ? F_LAST : 0) | (app_tile ? F_WRITE : 0);
-                    st.desc.moff = moff;
-                    st.desc.nchunks = nch;
-                    st.desc.wrow = L - 1;
-                    st.desc.item = item;
-                    st.desc.stage = stage;
-                    mbar_arrive_expect_tx(&sm.full[stage], bytes);
-                    const int row = row_base + t * TK;
-                    if (nbox == 0) {
-                        tma_2d(st.k, &kmap, 0, row, &sm.full[stage]);
-                        tma_2d(st.k + KREG, &kmap, 64, row, &sm.full[stage]);
-                        tma_2d(st.v, &vmap, 0, row, &sm.full[stage]);
-                        tma_2d(st.v + KREG, &vmap, 64, row, &sm.full[stage]);
-                    } else {
-                        for (int i = 0; i < nbox; ++i) {   // 4 KB pieces, 1024-B aligned: same swizzle
-                            const uint32_t o = i * TAIL * 128;
-                            tma_2d(st.k + o, &kmap32, 0, row + i * TAIL, &sm.full[stage]);
-                            tma_2d(st.k + KREG + o, &kmap32, 64, row + i * TAIL, &sm.full[stage]);
-                            tma_2d(st.v + o, &vmap32, 0, row + i * TAIL, &sm.full[stage]);
-                            tma_2d(st.v + KREG + o, &vmap32, 64, row + i * TAIL, &sm.full[stage]);
-                        }
-                    }
-                    if (mbytes) bulk_g2s(st.mask, msrc, mbytes, &sm.full[stage]);
-                    if (app_tile) {   // always after the wait (flush above)
-                        const size_t nb = ((size_t)b * p.Hkv + g) * D;
-                        bulk_g2s(st.knew, p.k_new + nb, D * 2, &sm.full[stage]);
-                        bulk_g2s(st.vnew, p.v_new + nb, D * 2, &sm.full[stage]);
-                    }
-                    if (t == 0) {
-                        const int qrow = b * p.Hq + g * GS;
-                        if (waited) {
-                            load_q(qrow, stage, par);
+                    const int qrow = b * p.Hq + g * GS;
+                    if (elect_one()) {
+                        st.desc.b = b;
+                        st.desc.g = g;
+                        st.desc.c = c;
+                        st.desc.nrows = nr;
+                        st.desc.flags = (t == 0 ? F_FIRST : 0) | (t == ntiles - 1 ? F_LAST : 0) | (app_tile ? F_WRITE : 0);
+                        st.desc.moff = moff;
+                        st.desc.nchunks = nch;
+                        st.desc.wrow = L - 1;
+                        st.desc.item = item;
+                        st.desc.stage = stage;
+                        mbar_arrive_expect_tx(&sm.full[stage], bytes);
+                        const int row = row_base + t * TK;
+                        if (nbox == 0) {
+                            tma_2d(st.k, &kmap, 0, row, &sm.full[stage]);
+                            tma_2d(st.k + KREG, &kmap, 64, row, &sm.full[stage]);
+                            tma_2d(st.v, &vmap, 0, row, &sm.full[stage]);
+                            tma_2d(st.v + KREG, &vmap, 64, row, &sm.full[stage]);
                         } else {
-                            late_row = qrow;
-                            late_stage = stage;
-                            late_par = par;
+                            for (int i = 0; i < nbox; ++i) {   // 4 KB pieces, 1024-B aligned: same swizzle
+                                const uint32_t o = i * TAIL * 128;
+                                tma_2d(st.k + o, &kmap32, 0, row + i * TAIL, &sm.full[stage]);
+                                tma_2d(st.k + KREG + o, &kmap32, 64, row + i * TAIL, &sm.full[stage]);
+                                tma_2d(st.v + o, &vmap32, 0, row + i * TAIL, &sm.full[stage]);
+                                tma_2d(st.v + KREG + o, &vmap32, 64, row + i * TAIL, &sm.full[stage]);
+                            }
                         }
+                        if (mbytes) bulk_g2s(st.mask, msrc, mbytes, &sm.full[stage]);
+                        if (app_tile) {   // always after the wait (flush above)
+                            const size_t nb = ((size_t)b * p.Hkv + g) * D;
+                            bulk_g2s(st.knew, p.k_new + nb, D * 2, &sm.full[stage]);
+                            bulk_g2s(st.vnew, p.v_new + nb, D * 2, &sm.full[stage]);
+                        }
+                        if (t == 0 && waited) load_q(qrow, stage, par);
+                    }
+                    __syncwarp();
+                    if (t == 0 && !waited) {
+                        late_row = qrow;
+                        late_stage = stage;
+                        late_par = par;
                     }
                     ++issued;
                     if (++stage == STAGES) {
@@ -297,15 +310,17 @@ decode_gqa_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_cons
                 }
                 ++item;
                 if (!waited) flush();
-                if (w_next < 0) w_next = (int)gridDim.x + sched_next(p.counters);
+                if (w_next < 0) w_next = draw();
                 w = w_next;
-                w_next = w < total ? (int)gridDim.x + sched_next(p.counters) : total;
+                w_next = w < total ? draw() : total;
             }
             if (!waited) flush();
-            sched_done(p.counters);
+            if (lane == 0) sched_done(p.counters);
             mbar_wait(&sm.empty[stage], phase ^ 1);
-            sm.st[stage].desc.flags = F_END;
-            mbar_arrive(&sm.full[stage]);
+            if (lane == 0) {
+                sm.st[stage].desc.flags = F_END;
+                mbar_arrive(&sm.full[stage]);
+            }
         }
     } else if (warp == 9) {
         // ============================ S issuer ============================

@@ -26,15 +26,6 @@ BATON_DEV void tma_load_4d(void *dst, const CUtensorMap *map, int c0, int c1, in
 BATON_DEV void prefetch_tmap(const CUtensorMap *map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
-// One lane of a converged warp (elect.sync): tcgen05 ops under this predicate issue once,
-// without the per-lane loop ptxas wraps around them under a plain `lane == 0` test
-BATON_DEV bool elect_one() {
-    uint32_t e;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(e));
-    return e != 0;
-}
 BATON_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 BATON_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 BATON_DEV void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
