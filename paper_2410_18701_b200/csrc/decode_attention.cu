@@ -146,8 +146,11 @@ __global__ void __launch_bounds__((CWARPS + 1) * 32, MINB) decode_attention_kern
     if (warp == CWARPS) {
         // ============================ producer warp ============================
         sched_build(sm.ws, p.lens, p.pad, p.B, p.Hq, lane);
-        if (lane != 0) return;
-        if (trace) tr[1] = mtimer();
+        // The whole warp walks the work list (identical state in every lane; the dynamic
+        // counter is drawn by lane 0 and broadcast) and waits on the ring; one elected
+        // lane per tile writes the stage descriptor and issues its copies, so the bulk
+        // copies compile to single UBLKCP instructions rather than per-lane loops.
+        if (trace && lane == 0) tr[1] = mtimer();
         int titem = 0;
         const int total = sched_total(sm.ws, p.Hq);
         const uint64_t pol = policy_evict_first();
@@ -161,14 +164,20 @@ __global__ void __launch_bounds__((CWARPS + 1) * 32, MINB) decode_attention_kern
             griddep_wait();
             griddep_launch_dependents();
             waited = true;
-            if (trace) tr[5] = mtimer();
-            if (late_q) bulk_g2s(sm.st[late_stage].q, late_q, D * 2, &sm.full[late_stage]);
+            if (trace && lane == 0) tr[5] = mtimer();
+            if (late_q && elect_one()) bulk_g2s(sm.st[late_stage].q, late_q, D * 2, &sm.full[late_stage]);
+            __syncwarp();
             late_q = nullptr;
+        };
+        auto draw = [&]() {   // next dynamic item, one atomic per warp
+            int v = 0;
+            if (lane == 0) v = sched_next(p.counters);
+            return (int)gridDim.x + __shfl_sync(FULL_MASK, v, 0);
         };
         // items [0, gridDim.x) are static (CTA i takes item i: no counter before the
         // wait), the rest are handed out by the dynamic counter
         int w = blockIdx.x;
-        int w_next = waited ? (int)gridDim.x + sched_next(p.counters) : -1;
+        int w_next = waited ? draw() : -1;
         while (w < total) {
             int c, h;
             sched_item(sm.ws, w, p.Hq, b, c, h);
@@ -184,7 +193,7 @@ __global__ void __launch_bounds__((CWARPS + 1) * 32, MINB) decode_attention_kern
             // fused append (a2): the item holding row L-1 takes the new token's k/v
             // from k_new/v_new; the first q head of the kv group writes it to the cache
             const bool app = p.k_new != nullptr && c == nch - 1;
-            if (trace && titem < 6) {
+            if (trace && titem < 6 && lane == 0) {
                 tr[8 + 4 * titem] = w;
                 tr[9 + 4 * titem] = mtimer();
             }
@@ -214,35 +223,35 @@ __global__ void __launch_bounds__((CWARPS + 1) * 32, MINB) decode_attention_kern
                     bytes += mbytes;
                 }
                 if (t == 0) bytes += D * 2;
-                st.desc.b = b;
-                st.desc.h = h;
-                st.desc.c = c;
-                st.desc.nrows = nr;
-                st.desc.flags = (t == 0 ? F_FIRST : 0) | (t == ntiles - 1 ? F_LAST : 0) |
-                                (app_tile && h * p.Hkv % p.Hq == 0 ? F_WRITE : 0);
-                st.desc.moff = moff;
-                st.desc.nchunks = nch;
-                st.desc.wrow = L - 1;
-                mbar_arrive_expect_tx(&sm.full[stage], bytes);
-                const int ncache = app_tile ? nr - 1 : nr;
-                if (ncache > 0) {
-                    bulk_g2s_evict_first(st.k, kb + (size_t)t * TILE * D, ncache * D * 2, &sm.full[stage], pol);
-                    bulk_g2s_evict_first(st.v, vb + (size_t)t * TILE * D, ncache * D * 2, &sm.full[stage], pol);
-                }
-                if (app_tile) {   // (always after the wait: see the flush above)
-                    const size_t nb = ((size_t)b * p.Hkv + g) * D;
-                    bulk_g2s(st.k + (nr - 1) * D, p.k_new + nb, D * 2, &sm.full[stage]);
-                    bulk_g2s(st.v + (nr - 1) * D, p.v_new + nb, D * 2, &sm.full[stage]);
-                }
-                if (mbytes) bulk_g2s(st.mask, msrc, mbytes, &sm.full[stage]);
-                if (t == 0) {
-                    const __nv_bfloat16 *qsrc = p.q + (size_t)(b * p.Hq + h) * D;
-                    if (waited) {
-                        bulk_g2s(st.q, qsrc, D * 2, &sm.full[stage]);
-                    } else {
-                        late_q = qsrc;
-                        late_stage = stage;
+                const __nv_bfloat16 *qsrc = p.q + (size_t)(b * p.Hq + h) * D;
+                if (elect_one()) {
+                    st.desc.b = b;
+                    st.desc.h = h;
+                    st.desc.c = c;
+                    st.desc.nrows = nr;
+                    st.desc.flags = (t == 0 ? F_FIRST : 0) | (t == ntiles - 1 ? F_LAST : 0) |
+                                    (app_tile && h * p.Hkv % p.Hq == 0 ? F_WRITE : 0);
+                    st.desc.moff = moff;
+                    st.desc.nchunks = nch;
+                    st.desc.wrow = L - 1;
+                    mbar_arrive_expect_tx(&sm.full[stage], bytes);
+                    const int ncache = app_tile ? nr - 1 : nr;
+                    if (ncache > 0) {
+                        bulk_g2s_evict_first(st.k, kb + (size_t)t * TILE * D, ncache * D * 2, &sm.full[stage], pol);
+                        bulk_g2s_evict_first(st.v, vb + (size_t)t * TILE * D, ncache * D * 2, &sm.full[stage], pol);
                     }
+                    if (app_tile) {   // (always after the wait: see the flush above)
+                        const size_t nb = ((size_t)b * p.Hkv + g) * D;
+                        bulk_g2s(st.k + (nr - 1) * D, p.k_new + nb, D * 2, &sm.full[stage]);
+                        bulk_g2s(st.v + (nr - 1) * D, p.v_new + nb, D * 2, &sm.full[stage]);
+                    }
+                    if (mbytes) bulk_g2s(st.mask, msrc, mbytes, &sm.full[stage]);
+                    if (t == 0 && waited) bulk_g2s(st.q, qsrc, D * 2, &sm.full[stage]);
+                }
+                __syncwarp();
+                if (t == 0 && !waited) {
+                    late_q = qsrc;
+                    late_stage = stage;
                 }
                 ++issued;
                 if (++stage == STAGES) {
@@ -251,13 +260,14 @@ __global__ void __launch_bounds__((CWARPS + 1) * 32, MINB) decode_attention_kern
                 }
             }
             if (!waited) flush();
-            if (w_next < 0) w_next = (int)gridDim.x + sched_next(p.counters);
+            if (w_next < 0) w_next = draw();
             w = w_next;
-            w_next = w < total ? (int)gridDim.x + sched_next(p.counters) : total;
+            w_next = w < total ? draw() : total;
         }
         if (!waited) flush();
-        sched_done(p.counters);
+        if (lane == 0) sched_done(p.counters);
         mbar_wait(&sm.empty[stage], phase ^ 1);
+        if (lane != 0) return;
         sm.st[stage].desc.flags = F_END;
         mbar_arrive(&sm.full[stage]);
         return;
