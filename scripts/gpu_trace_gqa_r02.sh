@@ -2,7 +2,7 @@
 # GQA decode chain between two consecutive layers of the decode-step graph (70B shard,
 # deferred split-K merge): experiment build, globaltimer trace, product build restored
 cd "$(dirname "$0")/.."
-O=gpurun_out/trg
+O=${OUT:-gpurun_out/trg}
 mkdir -p $O
 python -m paper_2410_18701_b200.build --experiments > $O/build.log 2>&1
 for rep in 1 2 3; do
