@@ -68,3 +68,36 @@ def test_gqa_tcgen05_kernel_uses_tensor_cores_tmem_and_tma():
 def test_prefill_extend_kernel_uses_tensor_cores_tmem_and_tma():
     for body in _find(_sass(), "prefill_attention_kernel").values():
         assert "UTCHMMA" in body and "LDTM" in body and "STTM" in body and "UTMALDG" in body
+
+
+def _issue_loops(body):
+    """Uniform-datapath issue ops (tcgen05.mma/commit, TMA tensor loads, bulk copies)
+    that ptxas wrapped in a per-lane ELECT / BRA.U.ANY loop: an op whose next few
+    instructions branch back with BRA.U.ANY."""
+    lines = [l for l in body.splitlines() if "/*" in l and not l.strip().startswith("/* 0x")]
+    hits = 0
+    for i, l in enumerate(lines):
+        if re.search(r"\b(UTCHMMA|UTCBAR|UTMALDG|UBLKCP)\b", l):
+            if any("BRA.U.ANY" in x for x in lines[i + 1:i + 5]):
+                hits += 1
+    return hits
+
+
+@pytest.mark.parametrize("kernel", ["decode_gqa_tc_kernel", "decode_attention_kernel"])
+def test_decode_issuers_have_no_per_lane_loops(kernel):
+    """DESIGN §6.1/§6.2: the producers and the tcgen05 issuers run as converged warps with
+    the uniform-datapath ops under elect.sync, so each op is ONE instruction (under
+    `if (lane == 0)` ptxas wrapped every tcgen05.mma / commit / TMA issue in a per-lane
+    ELECT loop, and the prefill's MMA thread paced its tile loop)."""
+    for name, body in _find(_sass(), kernel).items():
+        assert _issue_loops(body) == 0, name
+
+
+def test_prefill_mma_issuer_has_no_per_lane_loops():
+    """The prefill's MMA warp (§6.3): every UTCHMMA / UTCBAR outside per-lane loops (its
+    producer keeps a lane-0 TMA issuer: the converged version measured neutral)."""
+    for name, body in _find(_sass(), "prefill_attention_kernel").items():
+        lines = [l for l in body.splitlines() if "/*" in l and not l.strip().startswith("/* 0x")]
+        for i, l in enumerate(lines):
+            if re.search(r"\b(UTCHMMA|UTCBAR)\b", l):
+                assert not any("BRA.U.ANY" in x for x in lines[i + 1:i + 5]), (name, l.strip())
