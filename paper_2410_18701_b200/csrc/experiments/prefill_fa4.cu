@@ -203,7 +203,10 @@ prefill_fa4_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
         }
     } else if (warp == 9) {
         // ======================= MMA issuer =======================
-        if (lane == 0) {
+        // whole warp: decisions from lane 0's barrier polls broadcast to every lane, the
+        // tcgen05 ops under elect.sync (round 2; under `lane == 0` ptxas wrapped each one
+        // in a per-lane ELECT loop)
+        {
             constexpr uint32_t idS = idesc_bf16(FM, FN, 0);   // B = K tile, K-major
             constexpr uint32_t idO = idesc_bf16(FM, FD, 1);   // A = P (TMEM), B = V tile, MN-major
             int nq[2] = {0, 0}, np[2] = {0, 0}, kc = 0;
@@ -212,20 +215,30 @@ prefill_fa4_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
             auto issue_s = [&](int i, int j, int ni) {
                 const int s = (kc + j) & 1;
                 const uint32_t qa = smem_u32(sm.q[i]), ka = smem_u32(sm.k[s]);
+                if (elect_one()) {
 #pragma unroll
-                for (int k = 0; k < 8; ++k)        // K = head_dim in steps of 16 (32 B)
-                    umma_f16(tmem + 128 * i, smem_desc(qa + (k >> 2) * FQ_REG + (k & 3) * 32, 16, 1024),
-                             smem_desc(ka + (k >> 2) * FKV_REG + (k & 3) * 32, 16, 1024), idS, k > 0);
-                umma_commit(&sm.s_full[i]);
-                if (j == ni - 1) umma_commit(&sm.q_empty[i]);
+                    for (int k = 0; k < 8; ++k)        // K = head_dim in steps of 16 (32 B)
+                        umma_f16(tmem + 128 * i, smem_desc(qa + (k >> 2) * FQ_REG + (k & 3) * 32, 16, 1024),
+                                 smem_desc(ka + (k >> 2) * FKV_REG + (k & 3) * 32, 16, 1024), idS, k > 0);
+                    umma_commit(&sm.s_full[i]);
+                    if (j == ni - 1) umma_commit(&sm.q_empty[i]);
+                }
+                __syncwarp();
             };
             auto issue_pv = [&](int i, int j) {    // O_i += P_i(j) V(j)
                 const int s = (kc + j) & 1;
                 const uint32_t va = smem_u32(sm.v[s]);
+                if (elect_one()) {
 #pragma unroll
-                for (int k = 0; k < 8; ++k)        // K = 128 keys in steps of 16 (8 TMEM columns of bf16 pairs)
-                    umma_f16_ts(tmem + 256 + 128 * i, tmem + 128 * i + 64 + 8 * k,
-                                smem_desc(va + k * 2048, FKV_REG, 1024), idO, (j > 0 || k > 0));
+                    for (int k = 0; k < 8; ++k)        // K = 128 keys in steps of 16 (8 TMEM columns of bf16 pairs)
+                        umma_f16_ts(tmem + 256 + 128 * i, tmem + 128 * i + 64 + 8 * k,
+                                    smem_desc(va + k * 2048, FKV_REG, 1024), idO, (j > 0 || k > 0));
+                }
+                __syncwarp();
+            };
+            auto commit = [&](uint64_t *bar) {
+                if (elect_one()) umma_commit(bar);
+                __syncwarp();
             };
             auto wait_k = [&](int j) {
                 const int t = kc + j;
@@ -245,7 +258,7 @@ prefill_fa4_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
                 wait_k(0);
                 issue_s(0, 0, wk.n0);
                 if (wk.has1) issue_s(1, 0, wk.n1);
-                umma_commit(&sm.k_empty[kc & 1]);
+                commit(&sm.k_empty[kc & 1]);
                 int next[2] = {0, wk.has1 ? 0 : n[1]};     // next P.V per group
                 int k_ready = 0, v_ready = -1;              // K(<= k_ready), V(<= v_ready) waited
                 int s_cnt[4] = {0, 0, 0, 0}, v_cnt[4] = {0, 0, 0, 0};   // per j & 3: S / P.V issued
@@ -265,10 +278,12 @@ prefill_fa4_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
                         return true;
                     };
                     int i = -1;
-                    for (int t = 1; t <= 2 && i < 0; ++t) {   // round robin over ready groups
-                        const int c = (last + t) & 1;
-                        if (ready(c)) i = c;
-                    }
+                    if (lane == 0)
+                        for (int t = 1; t <= 2 && i < 0; ++t) {   // round robin over ready groups
+                            const int c = (last + t) & 1;
+                            if (ready(c)) i = c;
+                        }
+                    i = __shfl_sync(FULL_MASK, i, 0);   // one decision for the whole warp
                     if (i < 0) continue;                     // spin (test_wait does not suspend)
                     last = i;
                     const int j = next[i]++;
@@ -281,11 +296,11 @@ prefill_fa4_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
                     }
                     tc_fence_after();
                     issue_pv(i, j);
-                    if (j == n[i] - 1) umma_commit(&sm.o_done[i]);
+                    if (j == n[i] - 1) commit(&sm.o_done[i]);
                     const int v_need = (j < n[0]) + (j < n[1]);
                     if (++v_cnt[j & 3] == v_need) {          // V(j) consumed by every group
                         v_cnt[j & 3] = 0;
-                        umma_commit(&sm.v_empty[(kc + j) & 1]);
+                        commit(&sm.v_empty[(kc + j) & 1]);
                     }
                     if (j + 1 < n[i]) {
                         if (j + 1 > k_ready) {
@@ -296,7 +311,7 @@ prefill_fa4_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_consta
                         const int k_need = (j + 1 < n[0]) + (j + 1 < n[1]);
                         if (++s_cnt[(j + 1) & 3] == k_need) {   // K(j+1) consumed
                             s_cnt[(j + 1) & 3] = 0;
-                            umma_commit(&sm.k_empty[(kc + j + 1) & 1]);
+                            commit(&sm.k_empty[(kc + j + 1) & 1]);
                         }
                     }
                 }
