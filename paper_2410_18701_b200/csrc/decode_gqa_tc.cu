@@ -22,7 +22,8 @@
 //   (exp2), P^T -> bf16 in the SW128 K-major layout, O rescale in TMEM only when a
 //   head's max moved.  Row sums are kept per thread and reduced once per item.
 //   warp 8: TMA producer (K/V 2-D boxes 64 dims x 128 rows, q 64 x 16, mask bytes,
-//   the appended row).  Three single-thread MMA issuers with blocking waits: warp 9
+//   the appended row).  Three MMA issuer warps with blocking waits (each a converged
+//   warp issuing its tcgen05 ops from one elect.sync lane): warp 9
 //   issues S for the tiles in order (into the owning group's free S buffer) and
 //   hands each group its tiles through small smem queues; warps 10 and 11 issue
 //   P.V for group 0 and group 1 as soon as that group published P, so one group's
